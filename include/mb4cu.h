@@ -1,0 +1,171 @@
+/*
+ * mb4cu.h -- C ABI of the B200-native MB4 time-stepping core.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/nls2d/mb4_integrator.hpp:107-110 `mb4_step`,
+ *  integrators.hpp:51 `StepDriver::advance`, lattice.hpp:88 `observables`).
+ * The reference has no FFI layer; its boundary is the C++ API in
+ * proj/include/nls2d.  The C++ mirror of that API (include/nls2d/*.hpp) calls
+ * these entry points, and so do the Python tests (ctypes) and bench.py.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no exceptions cross this boundary;
+ *  - every call returns an int status (MB4CU_*); mb4cu_last_error(ctx) has text;
+ *  - a state is N interleaved complex doubles (re, im), site k = j*nx + i
+ *    (lattice.hpp:13-14,32) -- byte-identical to std::vector<std::complex<double>>;
+ *  - the context owns all device memory and its CUDA stream; the caller owns
+ *    host buffers.  One host thread per context at a time.
+ *
+ * FP64 throughout.  The per-step implicit stage solve is a matrix-free,
+ * stage-decoupled (T / T^-1) Neumann-preconditioned fixed-point iteration of
+ * fused sm_100a stencil kernels; see DESIGN.md.
+ */
+#ifndef MB4CU_H
+#define MB4CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+enum {
+    MB4CU_OK = 0,
+    MB4CU_INVALID = 1,        /* invalid argument (reference: std::invalid_argument)      */
+    MB4CU_NONCONVERGED = 2,   /* reference: NonConvergenceError (mb4_integrator.hpp:17-23) */
+    MB4CU_CUDA_ERROR = 3,
+    MB4CU_COMM_ERROR = 4,
+    MB4CU_OOM = 5,
+    MB4CU_NUMERIC = 6         /* observables health check (lattice.cpp:123-126)           */
+};
+
+/* Scheme constants (reference Mb4Scheme, mb4_scheme.hpp:26-64), computed on the
+ * host in long double and rounded, plus the Gauss-Legendre-6 tables of the
+ * quadrature form of the cubic term (not exposed by the reference):
+ *   L[q][a]  = l_a(zeta_q)            (Lagrange basis over {0, c1, c2, c3})
+ *   WA[i][q] = w_q * A(c_{i+1}, zeta_q)
+ * so that W[i][a][b][c] = sum_q WA[i][q] L[q][a] L[q][b] L[q][c] and
+ *         E[i][j]       = sum_q WA[i][q] L[q][j]. */
+typedef struct {
+    double alpha1;
+    double nodes[4];
+    double E[3][4];
+    double W[3][4][4][4];
+    double lam[3];
+    double T[3][3];
+    double Tinv[3][3];
+    double zeta6[6];
+    double w6[6];
+    double L[6][4];
+    double WA[3][6];
+} mb4cu_scheme;
+
+/* Replaces Mb4Scheme::Mb4Scheme(alpha1, nodes) (mb4_scheme.cpp:83-125).
+ * Returns MB4CU_INVALID for the reference's validation failures and for
+ * ComplexEigenvalueError (small_dense.cpp:100-101,127-128,151-152,171-172). */
+int mb4cu_scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* out);
+
+/* Problem description (replaces GridModel + NewtonConfig, lattice.hpp:49-73,
+ * mb4_integrator.hpp:25-35). */
+typedef struct {
+    int nx, ny;               /* lattice (>= 2 each; lattice.cpp:117-121)               */
+    double cx, cy;            /* 1/hx^2, 1/hy^2 of the periodic 5-point K (lattice.cpp:33-49) */
+    double gamma;             /* reference gamma: i du/dt = K u - gamma |u|^2 u + V u   */
+    const double* V;          /* host, nx*ny potential values (copied at create)        */
+    double epsilon;           /* stop when ||r||_inf <= epsilon (split reals)          */
+    int max_iters;            /* cap on stage sweeps per (sub)step                      */
+    int max_step_halvings;    /* halving-on-failure policy (mb4_integrator.cpp:287-315) */
+    int neumann_terms;        /* m in 0..3: preconditioner sum_{k<=m} (h lam J)^k; -1 = default */
+    int device;               /* CUDA device ordinal                                    */
+    int kernel;               /* 0 = default (fastest), 1 = tiled reference kernel      */
+} mb4cu_problem;
+
+typedef struct {
+    int newton_iters;         /* stage sweeps executed (all sub-steps)  (StepStats)      */
+    int halvings;             /* halvings applied                                        */
+    double solve_seconds;     /* device time of the stage solve (CUDA events)            */
+    double last_residual;     /* ||r||_inf of the last sweep                             */
+} mb4cu_stats;
+
+typedef struct {
+    double u_kinetic, u_nonlinear, u_external, total_energy, probability, participation,
+        raw_quartic;          /* lattice.hpp:78-86 */
+} mb4cu_obs;
+
+typedef struct mb4cu_ctx mb4cu_ctx;
+
+int mb4cu_create(const mb4cu_problem* prob, const mb4cu_scheme* scheme, mb4cu_ctx** out);
+int mb4cu_destroy(mb4cu_ctx* ctx);
+const char* mb4cu_last_error(const mb4cu_ctx* ctx);
+/* text of the last failed mb4cu_create / mb4cu_scheme_init in this thread */
+const char* mb4cu_create_error(void);
+
+/* State transfer (host buffers: 2*nx*ny doubles). */
+int mb4cu_set_state(mb4cu_ctx* ctx, const double* u_host);
+int mb4cu_get_state(mb4cu_ctx* ctx, double* u_host);
+/* Device-resident transfer (device pointers, async on the context stream). */
+int mb4cu_set_state_device(mb4cu_ctx* ctx, const double* u_dev);
+int mb4cu_get_state_device(mb4cu_ctx* ctx, double* u_dev);
+
+/* One MB4 step of size h on the resident state (mb4_step, mb4_integrator.cpp:275-316).
+ * On MB4CU_NONCONVERGED the state is unchanged. */
+int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats);
+
+/* nsteps steps; obs_series (may be NULL) receives (nsteps+1) rows of 7 doubles
+ * (mb4cu_obs order), the t=0 row first (harness.cpp:105-122).  iters_series (may
+ * be NULL) receives the sweeps of each step. */
+int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* iters_series,
+              mb4cu_stats* stats);
+
+/* Energy monitor of the resident state (observables, lattice.cpp:106-137). */
+int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out);
+
+/* Bind the context to an external CUDA stream (e.g. torch's current stream);
+ * NULL restores the context's own stream. */
+int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
+
+/* ---- Lattice operators on caller-supplied host arrays (device-computed) -------
+ * Used by the parity tests for the vector-field evaluator rows of SURVEY 8a. */
+/* y = (K + V) u   (GridModel::apply_kv, lattice.cpp:86-89) */
+int mb4cu_apply_kv(mb4cu_ctx* ctx, const double* u_host, double* y_host);
+/* y = f(u) = -i(Ku + Vu - gamma|u|^2 u)   (rhs, lattice.cpp:91-104) */
+int mb4cu_rhs(mb4cu_ctx* ctx, const double* u_host, double* y_host);
+/* Stage residuals Phi_1..3 (eval_phi, mb4_integrator.cpp:159-192), evaluated
+ * with the GL-6 quadrature form the sweep kernels use. */
+int mb4cu_eval_phi(mb4cu_ctx* ctx, const double* u0, const double* s1, const double* s2,
+                   const double* s3, double h, double* p1, double* p2, double* p3);
+
+/* ---- BASELINE input generator (host, deterministic, counter-based RNG) --------
+ * Seeded delta-defect potential and Gaussian wave packets.  Fills
+ * the sub-block [x0, x0+lnx) x [y0, y0+lny) of the global gnx x gny lattice.
+ * psi is NOT normalised; *psum receives sum |psi|^2 over the block so callers
+ * can normalise globally (mb4cu_scale_state). */
+typedef struct {
+    int gnx, gny;             /* global lattice                                        */
+    double defect_frac;       /* Bernoulli(frac) per site                              */
+    uint64_t defect_seed;
+    double vd_min, vd_max;    /* V at defects: vd_min if vd_max <= vd_min, else U[vd_min, vd_max) */
+    int npackets;             /* Gaussian packets                                      */
+    double sigma;
+    /* explicit packet (used when random_packets == 0 and npackets == 1) */
+    double x0, y0, kx, ky;
+    int random_packets;       /* 1: centres, momenta, phases drawn from packet_seed    */
+    uint64_t packet_seed;
+    double k_max;             /* random momenta uniform in [-k_max, k_max]^2           */
+    int threads;              /* host threads (<= 0: hardware concurrency)             */
+} mb4cu_inputs;
+
+int mb4cu_make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny, double* V,
+                      double* psi, double* psum);
+/* psi *= s  (host, multithreaded) */
+int mb4cu_scale_state(double* psi, size_t nsites, double s, int threads);
+
+/* Library version / build string. */
+const char* mb4cu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,474 @@
+// C ABI of libmb4cu: context management, the per-step stage-iteration driver
+// with the reference's halving policy, the energy monitor, and the parity
+// entry points.  See include/mb4cu.h for the contract and the reference
+// interfaces each entry point replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+
+#include "mb4cu.h"
+#include "mb4cu_internal.hpp"
+
+using mb4cu::SweepArgs;
+using mb4cu::SweepConsts;
+
+struct mb4cu_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int nx = 0, ny = 0;
+    size_t n = 0;
+    double cx = 0, cy = 0, gamma = 0, eps = 0;
+    int max_iters = 0, max_halvings = 0, m = 2, kernel = 0;
+    mb4cu_scheme scheme{};
+    double2* u0 = nullptr;
+    double* V = nullptr;
+    double2* U[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    double2* ubak = nullptr;
+    unsigned long long* d_rmax = nullptr;
+    unsigned long long* h_rmax = nullptr;  // pinned
+    double* d_obs_partial = nullptr;
+    double* d_obs5 = nullptr;
+    double* h_obs5 = nullptr;  // pinned
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int fail(mb4cu_ctx* ctx, int code, const std::string& what) {
+    if (ctx) ctx->err = what;
+    return code;
+}
+
+int cuda_fail(mb4cu_ctx* ctx, cudaError_t e, const char* where) {
+    const int code = e == cudaErrorMemoryAllocation ? MB4CU_OOM : MB4CU_CUDA_ERROR;
+    return fail(ctx, code, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MB4_CUDA(ctx, call)                                  \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
+    SweepConsts c{};
+    const mb4cu_scheme& s = ctx->scheme;
+    std::memcpy(c.E, s.E, sizeof(c.E));
+    std::memcpy(c.L, s.L, sizeof(c.L));
+    std::memcpy(c.WA, s.WA, sizeof(c.WA));
+    std::memcpy(c.T, s.T, sizeof(c.T));
+    std::memcpy(c.Tinv, s.Tinv, sizeof(c.Tinv));
+    for (int k = 0; k < 3; ++k) c.hlam[k] = h * s.lam[k];
+    c.h = h;
+    c.gamma = ctx->gamma;
+    c.cx = ctx->cx;
+    c.cy = ctx->cy;
+    c.diag = 2.0 * ctx->cx + 2.0 * ctx->cy;
+    return c;
+}
+
+double decode_bits(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+// One MB4 sub-step of size h on ctx->u0: sweeps until ||r||_inf <= eps
+// (newton_solve, mb4_integrator.cpp:194-255).  On success u0 <- U3 (c3 = 1).
+int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
+    const SweepConsts c = make_consts(ctx, h);
+    int cur = -1;
+    *sweeps = 0;
+    for (int it = 1; it <= ctx->max_iters; ++it) {
+        const int nxt = cur < 0 ? 0 : 1 - cur;
+        SweepArgs a{};
+        a.nx = ctx->nx;
+        a.ny = ctx->ny;
+        a.u0 = ctx->u0;
+        a.V = ctx->V;
+        for (int i = 0; i < 3; ++i) {
+            a.uin[i] = cur < 0 ? ctx->u0 : ctx->U[cur][i];
+            a.uout[i] = ctx->U[nxt][i];
+        }
+        a.rmax = ctx->d_rmax;
+        MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
+        MB4_CUDA(ctx, mb4cu::launch_sweep_tiled(ctx->m, cur < 0, a, c, ctx->stream));
+        MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        *sweeps = it;
+        const double r = decode_bits(*ctx->h_rmax);
+        *last_res = r;
+        cur = nxt;
+        if (!std::isfinite(r)) {
+            *last_res = INFINITY;
+            return fail(ctx, MB4CU_NONCONVERGED, "stage iteration diverged (non-finite update)");
+        }
+        if (r <= ctx->eps) {
+            std::swap(ctx->u0, ctx->U[cur][2]);
+            return MB4CU_OK;
+        }
+    }
+    return fail(ctx, MB4CU_NONCONVERGED,
+                "stage iteration: no convergence after " + std::to_string(ctx->max_iters) + " sweeps");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mb4cu_version(void) { return "mb4cu 0.1 (sm_100a, FP64)"; }
+
+const char* mb4cu_create_error(void) { return g_create_error.c_str(); }
+
+int mb4cu_scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* out) {
+    g_create_error.clear();
+    return mb4cu::scheme_init(alpha1, c1, c2, c3, out, g_create_error);
+}
+
+int mb4cu_make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny, double* V,
+                      double* psi, double* psum) {
+    g_create_error.clear();
+    return mb4cu::make_inputs(spec, x0, y0, lnx, lny, V, psi, psum, g_create_error);
+}
+
+int mb4cu_scale_state(double* psi, size_t nsites, double s, int threads) {
+    return mb4cu::scale_state(psi, nsites, s, threads);
+}
+
+int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx** out) {
+    g_create_error.clear();
+    if (!p || !scheme || !out) {
+        g_create_error = "mb4cu_create: null argument";
+        return MB4CU_INVALID;
+    }
+    *out = nullptr;
+    if (p->nx < 2 || p->ny < 2) {
+        g_create_error = "GridSpec: nx and ny must be >= 2";
+        return MB4CU_INVALID;
+    }
+    if (!(p->cx > 0.0) || !(p->cy > 0.0) || !std::isfinite(p->gamma) || !p->V) {
+        g_create_error = "mb4cu_create: bad stencil / potential";
+        return MB4CU_INVALID;
+    }
+    if (!(p->epsilon > 0.0)) {
+        g_create_error = "NewtonConfig: epsilon must be > 0";
+        return MB4CU_INVALID;
+    }
+    if (p->max_iters < 1) {
+        g_create_error = "NewtonConfig: max_iters must be >= 1";
+        return MB4CU_INVALID;
+    }
+    if (p->max_step_halvings < 0) {
+        g_create_error = "NewtonConfig: negative halvings";
+        return MB4CU_INVALID;
+    }
+    const int m = p->neumann_terms < 0 ? 2 : p->neumann_terms;
+    if (m > 3) {
+        g_create_error = "mb4cu_create: neumann_terms must be in 0..3";
+        return MB4CU_INVALID;
+    }
+    auto* ctx = new mb4cu_ctx();
+    ctx->device = p->device;
+    ctx->nx = p->nx;
+    ctx->ny = p->ny;
+    ctx->n = static_cast<size_t>(p->nx) * p->ny;
+    ctx->cx = p->cx;
+    ctx->cy = p->cy;
+    ctx->gamma = p->gamma;
+    ctx->eps = p->epsilon;
+    ctx->max_iters = p->max_iters;
+    ctx->max_halvings = p->max_step_halvings;
+    ctx->m = m;
+    ctx->kernel = p->kernel;
+    ctx->scheme = *scheme;
+
+    auto bail = [&](cudaError_t e, const char* where) {
+        g_create_error = std::string(where) + ": " + cudaGetErrorString(e);
+        const int code = e == cudaErrorMemoryAllocation ? MB4CU_OOM : MB4CU_CUDA_ERROR;
+        mb4cu_destroy(ctx);
+        return code;
+    };
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return bail(e, "cudaSetDevice");
+    if ((e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "cudaStreamCreate");
+    ctx->stream = ctx->own_stream;
+    const size_t sb = ctx->n * sizeof(double2);
+    if ((e = cudaMalloc(&ctx->u0, sb)) != cudaSuccess) return bail(e, "cudaMalloc(u0)");
+    if ((e = cudaMalloc(&ctx->V, ctx->n * sizeof(double))) != cudaSuccess) return bail(e, "cudaMalloc(V)");
+    for (int b = 0; b < 2; ++b)
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaMalloc(&ctx->U[b][i], sb)) != cudaSuccess) return bail(e, "cudaMalloc(U)");
+    if ((e = cudaMalloc(&ctx->d_rmax, 64)) != cudaSuccess) return bail(e, "cudaMalloc(rmax)");
+    if ((e = cudaMallocHost(&ctx->h_rmax, 64)) != cudaSuccess) return bail(e, "cudaMallocHost");
+    const int nb = mb4cu::obs_blocks(ctx->nx, ctx->ny);
+    if ((e = cudaMalloc(&ctx->d_obs_partial, sizeof(double) * mb4cu::kObsFields * nb)) != cudaSuccess)
+        return bail(e, "cudaMalloc(obs)");
+    if ((e = cudaMalloc(&ctx->d_obs5, sizeof(double) * 8)) != cudaSuccess) return bail(e, "cudaMalloc(obs5)");
+    if ((e = cudaMallocHost(&ctx->h_obs5, sizeof(double) * 8)) != cudaSuccess) return bail(e, "cudaMallocHost");
+    if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    if ((e = cudaMemcpy(ctx->V, p->V, ctx->n * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(e, "cudaMemcpy(V)");
+    if ((e = cudaMemset(ctx->u0, 0, sb)) != cudaSuccess) return bail(e, "cudaMemset(u0)");
+    *out = ctx;
+    return MB4CU_OK;
+}
+
+int mb4cu_destroy(mb4cu_ctx* ctx) {
+    if (!ctx) return MB4CU_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+    cudaFree(ctx->u0);
+    cudaFree(ctx->V);
+    for (auto& set : ctx->U)
+        for (auto* p : set) cudaFree(p);
+    cudaFree(ctx->ubak);
+    cudaFree(ctx->d_rmax);
+    cudaFreeHost(ctx->h_rmax);
+    cudaFree(ctx->d_obs_partial);
+    cudaFree(ctx->d_obs5);
+    cudaFreeHost(ctx->h_obs5);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return MB4CU_OK;
+}
+
+const char* mb4cu_last_error(const mb4cu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int mb4cu_set_stream(mb4cu_ctx* ctx, void* s) {
+    if (!ctx) return MB4CU_INVALID;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    return MB4CU_OK;
+}
+
+int mb4cu_set_state(mb4cu_ctx* ctx, const double* u) {
+    if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, u, ctx->n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_get_state(mb4cu_ctx* ctx, double* u) {
+    if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "get_state: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    MB4_CUDA(ctx, cudaMemcpyAsync(u, ctx->u0, ctx->n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_set_state_device(mb4cu_ctx* ctx, const double* u) {
+    if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state_device: null argument");
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, u, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_get_state_device(mb4cu_ctx* ctx, double* u) {
+    if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "get_state_device: null argument");
+    MB4_CUDA(ctx, cudaMemcpyAsync(u, ctx->u0, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats) {
+    if (!ctx) return MB4CU_INVALID;
+    if (!(h > 0.0)) return fail(ctx, MB4CU_INVALID, "mb4_step: h must be positive");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    MB4_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    double last = 0.0;
+    int rc = MB4CU_NONCONVERGED;
+    int used_halvings = 0, sweeps_total = 0;
+    for (int hv = 0; hv <= ctx->max_halvings; ++hv) {
+        const int sub = 1 << hv;
+        const double hs = h / sub;
+        if (hv == 1) {
+            if (!ctx->ubak) MB4_CUDA(ctx, cudaMalloc(&ctx->ubak, ctx->n * sizeof(double2)));
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->ubak, ctx->u0, ctx->n * sizeof(double2),
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+        } else if (hv > 1) {
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, ctx->ubak, ctx->n * sizeof(double2),
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        bool ok = true;
+        int attempt = 0;
+        for (int s = 0; s < sub; ++s) {
+            int sw = 0;
+            rc = substep(ctx, hs, &sw, &last);
+            attempt += sw;
+            if (rc == MB4CU_NONCONVERGED) {
+                ok = false;
+                break;
+            }
+            if (rc != MB4CU_OK) return rc;
+        }
+        if (ok) {
+            used_halvings = hv;
+            sweeps_total = attempt;
+            rc = MB4CU_OK;
+            break;
+        }
+    }
+    if (rc != MB4CU_OK) {
+        if (ctx->max_halvings >= 1)
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, ctx->ubak, ctx->n * sizeof(double2),
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (stats) stats->last_residual = last;
+        return fail(ctx, MB4CU_NONCONVERGED,
+                    "mb4_step: no convergence after " + std::to_string(ctx->max_halvings) +
+                        " step halvings");
+    }
+    MB4_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    MB4_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (stats) {
+        stats->newton_iters += sweeps_total;
+        stats->halvings += used_halvings;
+        stats->solve_seconds += 1e-3 * ms;
+        stats->last_residual = last;
+    }
+    return MB4CU_OK;
+}
+
+int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out) {
+    if (!ctx || !out) return fail(ctx, MB4CU_INVALID, "observables: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    mb4cu::ObsArgs a{};
+    a.nx = ctx->nx;
+    a.ny = ctx->ny;
+    a.cx = ctx->cx;
+    a.cy = ctx->cy;
+    a.diag = 2.0 * ctx->cx + 2.0 * ctx->cy;
+    a.u = ctx->u0;
+    a.V = ctx->V;
+    a.partial = ctx->d_obs_partial;
+    MB4_CUDA(ctx, mb4cu::launch_observables(a, ctx->d_obs5, ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_obs5, ctx->d_obs5, sizeof(double) * mb4cu::kObsFields,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const double qr = ctx->h_obs5[0], qi = ctx->h_obs5[1], prob = ctx->h_obs5[2],
+                 quart = ctx->h_obs5[3], ext = ctx->h_obs5[4];
+    // u^H K u is real for symmetric K; imaginary residue is a health check (lattice.cpp:123-126)
+    const double imag_scale = std::max(std::fabs(qr), (4.0 * ctx->cx + 4.0 * ctx->cy) * prob);
+    if (std::fabs(qi) > 1e-12 * imag_scale && imag_scale > 0.0)
+        return fail(ctx, MB4CU_NUMERIC, "observables: non-real kinetic quadratic form");
+    out->u_kinetic = qr;
+    out->u_nonlinear = -0.5 * ctx->gamma * quart;
+    out->u_external = ext;
+    out->total_energy = out->u_kinetic + out->u_nonlinear + out->u_external;
+    out->probability = prob;
+    out->raw_quartic = quart;
+    out->participation = prob > 0.0 ? quart / (prob * prob) : 0.0;
+    return MB4CU_OK;
+}
+
+static void put_obs(double* row, const mb4cu_obs& o) {
+    row[0] = o.u_kinetic;
+    row[1] = o.u_nonlinear;
+    row[2] = o.u_external;
+    row[3] = o.total_energy;
+    row[4] = o.probability;
+    row[5] = o.participation;
+    row[6] = o.raw_quartic;
+}
+
+int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* iters_series,
+              mb4cu_stats* stats) {
+    if (!ctx) return MB4CU_INVALID;
+    if (nsteps < 0) return fail(ctx, MB4CU_INVALID, "run: nsteps must be >= 0");
+    mb4cu_obs o{};
+    if (obs_series) {
+        const int rc = mb4cu_observables(ctx, &o);
+        if (rc) return rc;
+        put_obs(obs_series, o);
+    }
+    for (int s = 1; s <= nsteps; ++s) {
+        mb4cu_stats st{};
+        const int rc = mb4cu_step(ctx, h, &st);
+        if (stats) {
+            stats->newton_iters += st.newton_iters;
+            stats->halvings += st.halvings;
+            stats->solve_seconds += st.solve_seconds;
+            stats->last_residual = st.last_residual;
+        }
+        if (rc) return rc;
+        if (iters_series) iters_series[s - 1] = st.newton_iters;
+        if (obs_series) {
+            const int rc2 = mb4cu_observables(ctx, &o);
+            if (rc2) return rc2;
+            put_obs(obs_series + 7 * s, o);
+        }
+    }
+    return MB4CU_OK;
+}
+
+// ---- parity entry points on host arrays -------------------------------------
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+}  // namespace
+
+static int kv_common(mb4cu_ctx* ctx, const double* u, double* y, bool rhs) {
+    if (!ctx || !u || !y) return fail(ctx, MB4CU_INVALID, "apply_kv: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBuf du, dy;
+    const size_t sb = ctx->n * sizeof(double2);
+    MB4_CUDA(ctx, cudaMalloc(&du.p, sb));
+    MB4_CUDA(ctx, cudaMalloc(&dy.p, sb));
+    MB4_CUDA(ctx, cudaMemcpyAsync(du.p, u, sb, cudaMemcpyHostToDevice, ctx->stream));
+    MB4_CUDA(ctx, mb4cu::launch_apply_kv(ctx->nx, ctx->ny, ctx->cx, ctx->cy,
+                                         static_cast<const double2*>(du.p), ctx->V, ctx->gamma, rhs,
+                                         static_cast<double2*>(dy.p), ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(y, dy.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_apply_kv(mb4cu_ctx* ctx, const double* u, double* y) { return kv_common(ctx, u, y, false); }
+
+int mb4cu_rhs(mb4cu_ctx* ctx, const double* u, double* y) { return kv_common(ctx, u, y, true); }
+
+int mb4cu_eval_phi(mb4cu_ctx* ctx, const double* u0, const double* s1, const double* s2,
+                   const double* s3, double h, double* p1, double* p2, double* p3) {
+    if (!ctx || !u0 || !s1 || !s2 || !s3 || !p1 || !p2 || !p3)
+        return fail(ctx, MB4CU_INVALID, "eval_phi: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    const size_t sb = ctx->n * sizeof(double2);
+    DevBuf bufs[7];
+    for (auto& b : bufs) MB4_CUDA(ctx, cudaMalloc(&b.p, sb));
+    const double* hin[4] = {u0, s1, s2, s3};
+    for (int i = 0; i < 4; ++i)
+        MB4_CUDA(ctx, cudaMemcpyAsync(bufs[i].p, hin[i], sb, cudaMemcpyHostToDevice, ctx->stream));
+    const double2* st[3] = {static_cast<const double2*>(bufs[1].p), static_cast<const double2*>(bufs[2].p),
+                            static_cast<const double2*>(bufs[3].p)};
+    double2* ph[3] = {static_cast<double2*>(bufs[4].p), static_cast<double2*>(bufs[5].p),
+                      static_cast<double2*>(bufs[6].p)};
+    const SweepConsts c = make_consts(ctx, h);
+    MB4_CUDA(ctx, mb4cu::launch_eval_phi(ctx->nx, ctx->ny, static_cast<const double2*>(bufs[0].p),
+                                         ctx->V, st, ph, c, ctx->stream));
+    double* hout[3] = {p1, p2, p3};
+    for (int i = 0; i < 3; ++i)
+        MB4_CUDA(ctx, cudaMemcpyAsync(hout[i], ph[i], sb, cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// Internal declarations shared by the host and device translation units of libmb4cu.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "mb4cu.h"
+
+namespace mb4cu {
+
+int scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* out,
+                std::string& why);
+int make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny, double* V,
+                double* psi, double* psum, std::string& why);
+int scale_state(double* psi, size_t nsites, double s, int threads);
+
+// Per-sweep constants, passed by value as a __grid_constant__ kernel parameter
+// (lives in the constant bank; no per-context __constant__ symbol juggling).
+struct SweepConsts {
+    double E[3][4];     // combos c_i = sum_j E[i][j] z_j
+    double L[6][4];     // U_q = sum_a L[q][a] z_a
+    double WA[3][6];    // cubic_i = sum_q WA[i][q] |U_q|^2 U_q
+    double T[3][3];
+    double Tinv[3][3];
+    double hlam[3];     // h * lambda_k
+    double h;
+    double gamma;
+    double cx, cy, diag;  // stencil: diag = 2cx + 2cy
+};
+
+// Lattice geometry and buffers of one sweep.
+struct SweepArgs {
+    int nx, ny;
+    const double2* u0;
+    const double* V;
+    const double2* uin[3];
+    double2* uout[3];
+    unsigned long long* rmax;   // bit pattern of max |r| (non-negative double)
+};
+
+// Energy-monitor partial sums per block: quad_re, quad_im, prob, quart, ext.
+constexpr int kObsFields = 5;
+
+struct ObsArgs {
+    int nx, ny;
+    double cx, cy, diag;
+    const double2* u;
+    const double* V;
+    double* partial;   // [nblocks][kObsFields]
+};
+
+// Launchers (sweep_kernels.cu).
+size_t tiled_smem_bytes(int m, bool first);
+cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
+                               cudaStream_t s);
+int obs_blocks(int nx, int ny);
+cudaError_t launch_observables(const ObsArgs& a, double* out5, cudaStream_t s);
+cudaError_t launch_apply_kv(int nx, int ny, double cx, double cy, const double2* u, const double* V,
+                            double gamma, bool rhs, double2* y, cudaStream_t s);
+cudaError_t launch_eval_phi(int nx, int ny, const double2* u0, const double* V,
+                            const double2* const st[3], double2* const phi[3],
+                            const SweepConsts& c, cudaStream_t s);
+
+}  // namespace mb4cu

@@ -1,0 +1,358 @@
+// Tiled reference sweep kernel + lattice operator kernels (energy monitor,
+// (K+V)u, f(u), Phi).  The tiled sweep is the simple, obviously-correct form
+// of one stage iteration; the production path is the persistent marching
+// kernel in sweep_march.cu, which is checked against this one.
+//
+// One stage sweep with Neumann depth M:
+//   Phi     = Phi(u0, U)                         (eval_phi, mb4_integrator.cpp:159-192)
+//   phibar  = T^-1 Phi                           (:212-219)
+//   b_0     = phibar,  b_n = phibar + h lam_k J b_{n-1}   (n = 1..M)
+//   rbar    = -b_M    ~= -(I - h lam_k J)^{-1} phibar    (replaces the LU solves :221-229)
+//   r = T rbar;  U += r;  ||r||_inf                (:231-250)
+// Each level needs its input on a one-site-wider region, so a tile of TX x TY
+// outputs stages z on a halo of M+1 sites.
+#include <cuda_runtime.h>
+
+#include "mb4cu_internal.hpp"
+#include "site_math.cuh"
+
+namespace mb4cu {
+namespace {
+
+constexpr int kTX = 16, kTY = 16;
+
+template <int M>
+struct TiledGeom {
+    static constexpr int H = M + 1;
+    static constexpr int PX = kTX + 2 * H;
+    static constexpr int PY = kTY + 2 * H;
+    static constexpr int NP = PX * PY;
+    static constexpr int NPE = (NP + 1) & ~1;  // even count keeps double2 alignment
+};
+
+template <int M, bool FIRST>
+__global__ void __launch_bounds__(kTX * kTY)
+sweep_tiled_kernel(const SweepArgs a, const __grid_constant__ SweepConsts c) {
+    using G = TiledGeom<M>;
+    constexpr int NZ = FIRST ? 1 : 4;
+    extern __shared__ double2 smem[];
+    double2* zs = smem;                                   // [NZ][NP]
+    double* vs = reinterpret_cast<double*>(zs + NZ * G::NP);  // [NPE]
+    double2* lev = reinterpret_cast<double2*>(vs + G::NPE);   // [M][3][NP]
+
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int gx0 = blockIdx.x * kTX - G::H;
+    const int gy0 = blockIdx.y * kTY - G::H;
+
+    for (int idx = tid; idx < G::NP; idx += nthr) {
+        const int ly = idx / G::PX, lx = idx - ly * G::PX;
+        const size_t g = static_cast<size_t>(wrap_index(gy0 + ly, a.ny)) * a.nx +
+                         wrap_index(gx0 + lx, a.nx);
+        zs[idx] = a.u0[g];
+        if (!FIRST) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) zs[(j + 1) * G::NP + idx] = a.uin[j][g];
+        }
+        vs[idx] = a.V[g];
+    }
+    __syncthreads();
+
+    auto zat = [&](int j, int idx) -> double2 { return FIRST ? zs[idx] : zs[j * G::NP + idx]; };
+
+    unsigned long long rmax = 0ull;
+    auto emit = [&](int lx, int ly, const double2 r[3]) {
+        const int gx = gx0 + lx, gy = gy0 + ly;
+        if (gx >= a.nx || gy >= a.ny) return;
+        const size_t g = static_cast<size_t>(gy) * a.nx + gx;
+        const int idx = ly * G::PX + lx;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double2 u = zat(i + 1, idx);
+            a.uout[i][g] = make_double2(u.x + r[i].x, u.y + r[i].y);
+            const unsigned long long bx = abs_bits(r[i].x), by = abs_bits(r[i].y);
+            rmax = bx > rmax ? bx : rmax;
+            rmax = by > rmax ? by : rmax;
+        }
+    };
+
+    // ---- level 0: Phi (and phibar) on the tile grown by M --------------------
+    {
+        constexpr int W = G::PX - 2, Hh = G::PY - 2;
+        for (int it = tid; it < W * Hh; it += nthr) {
+            const int ly = it / W + 1, lx = it % W + 1;
+            const int idx = ly * G::PX + lx;
+            if (M == 0 && (lx < G::H || lx >= G::H + kTX || ly < G::H || ly >= G::H + kTY)) continue;
+            double2 z[4], w[4];
+            const double v = vs[idx];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                z[j] = zat(j, idx);
+                w[j] = kv_site(c, v, z[j], zat(j, idx - 1), zat(j, idx + 1), zat(j, idx - G::PX),
+                               zat(j, idx + G::PX));
+            }
+            double2 phi[3];
+            phi_site(c, z, w, phi);
+            if (M == 0) {
+                double2 r[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) r[i] = make_double2(-phi[i].x, -phi[i].y);
+                emit(lx, ly, r);
+            } else {
+                double2 pb[3];
+                to_eigen(c, phi, pb);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) lev[k * G::NP + idx] = pb[k];
+            }
+        }
+    }
+    // ---- levels 1..M: b_n = phibar + h lam J b_{n-1} --------------------------
+#pragma unroll
+    for (int n = 1; n <= M; ++n) {
+        __syncthreads();
+        const double2* prev = lev + (n - 1) * 3 * G::NP;
+        double2* cur = lev + n * 3 * G::NP;
+        const int lo = n + 1, W = G::PX - 2 * lo, Hh = G::PY - 2 * lo;
+        for (int it = tid; it < W * Hh; it += nthr) {
+            const int ly = it / W + lo, lx = it % W + lo;
+            const int idx = ly * G::PX + lx;
+            const double v = vs[idx];
+            const JDiag d = jdiag(zs[idx]);
+            double2 b[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double2* p = prev + k * G::NP;
+                const double2 t = p[idx];
+                const double2 ak = kv_site(c, v, t, p[idx - 1], p[idx + 1], p[idx - G::PX], p[idx + G::PX]);
+                const double2 jt = j_site(c, d, t, ak);
+                const double2 pb = lev[k * G::NP + idx];
+                b[k] = make_double2(fma(c.hlam[k], jt.x, pb.x), fma(c.hlam[k], jt.y, pb.y));
+            }
+            if (n == M) {
+                double2 rb[3], r[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b[k].x, -b[k].y);
+                from_eigen(c, rb, r);
+                emit(lx, ly, r);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cur[k * G::NP + idx] = b[k];
+            }
+        }
+    }
+    block_max_to(rmax, a.rmax);
+}
+
+template <int M, bool FIRST>
+size_t tiled_smem() {
+    using G = TiledGeom<M>;
+    const int nz = FIRST ? 1 : 4;
+    const int nlev = M == 0 ? 0 : M;  // lev[0..M-1] (level M goes to global)
+    return sizeof(double2) * nz * G::NP + sizeof(double) * G::NPE + sizeof(double2) * 3 * G::NP * nlev;
+}
+
+template <int M, bool FIRST>
+cudaError_t launch_tiled(const SweepArgs& a, const SweepConsts& c, cudaStream_t s) {
+    const size_t smem = tiled_smem<M, FIRST>();
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(sweep_tiled_kernel<M, FIRST>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const dim3 grid((a.nx + kTX - 1) / kTX, (a.ny + kTY - 1) / kTY);
+    sweep_tiled_kernel<M, FIRST><<<grid, kTX * kTY, smem, s>>>(a, c);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Energy monitor: observables (lattice.cpp:106-137), deterministic reduction.
+// ---------------------------------------------------------------------------
+constexpr int kObsThreads = 256;
+
+__global__ void __launch_bounds__(kObsThreads) observables_partial_kernel(const ObsArgs a) {
+    double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const size_t n = static_cast<size_t>(a.nx) * a.ny;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(k / a.nx), i = static_cast<int>(k - static_cast<size_t>(j) * a.nx);
+        const double2 u = a.u[k];
+        const double2 l = a.u[static_cast<size_t>(j) * a.nx + wrap_index(i - 1, a.nx)];
+        const double2 r = a.u[static_cast<size_t>(j) * a.nx + wrap_index(i + 1, a.nx)];
+        const double2 d = a.u[static_cast<size_t>(wrap_index(j - 1, a.ny)) * a.nx + i];
+        const double2 up = a.u[static_cast<size_t>(wrap_index(j + 1, a.ny)) * a.nx + i];
+        const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
+        const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
+        acc[0] += fma(u.x, kx, u.y * ky);   // Re conj(u) Ku
+        acc[1] += fma(u.x, ky, -u.y * kx);  // Im conj(u) Ku
+        const double n2 = fma(u.x, u.x, u.y * u.y);
+        acc[2] += n2;
+        acc[3] += n2 * n2;
+        acc[4] += a.V[k] * n2;
+    }
+    __shared__ double red[kObsFields][kObsThreads / 32];
+#pragma unroll
+    for (int f = 0; f < kObsFields; ++f) {
+        double v = acc[f];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kObsFields) {
+        double v = 0.0;
+        for (int w = 0; w < kObsThreads / 32; ++w) v += red[threadIdx.x][w];
+        a.partial[blockIdx.x * kObsFields + threadIdx.x] = v;
+    }
+}
+
+// Fixed-order final sum of the block partials (bit-reproducible).
+__global__ void observables_finalize_kernel(const double* partial, int nblocks, double* out) {
+    __shared__ double red[kObsFields][256];
+    double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+#pragma unroll
+        for (int f = 0; f < kObsFields; ++f) acc[f] += partial[b * kObsFields + f];
+#pragma unroll
+    for (int f = 0; f < kObsFields; ++f) red[f][threadIdx.x] = acc[f];
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+#pragma unroll
+            for (int f = 0; f < kObsFields; ++f) red[f][threadIdx.x] += red[f][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x < kObsFields) out[threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void apply_kv_kernel(int nx, int ny, double cx, double cy, const double2* __restrict__ u,
+                                const double* __restrict__ V, double gamma, bool rhs,
+                                double2* __restrict__ y) {
+    const size_t n = static_cast<size_t>(nx) * ny;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(k / nx), i = static_cast<int>(k - static_cast<size_t>(j) * nx);
+        const double2 c = u[k];
+        const double2 l = u[static_cast<size_t>(j) * nx + wrap_index(i - 1, nx)];
+        const double2 r = u[static_cast<size_t>(j) * nx + wrap_index(i + 1, nx)];
+        const double2 d = u[static_cast<size_t>(wrap_index(j - 1, ny)) * nx + i];
+        const double2 up = u[static_cast<size_t>(wrap_index(j + 1, ny)) * nx + i];
+        const double dg = 2.0 * cx + 2.0 * cy;
+        double ax = fma(dg, c.x, -(cx * (l.x + r.x) + cy * (d.x + up.x))) + V[k] * c.x;
+        double ay = fma(dg, c.y, -(cx * (l.y + r.y) + cy * (d.y + up.y))) + V[k] * c.y;
+        if (rhs) {
+            const double n2 = fma(c.x, c.x, c.y * c.y);
+            ax = fma(-gamma * n2, c.x, ax);
+            ay = fma(-gamma * n2, c.y, ay);
+            y[k] = make_double2(ay, -ax);  // -i (ax + i ay)
+        } else {
+            y[k] = make_double2(ax, ay);
+        }
+    }
+}
+
+struct PhiArgs {
+    int nx, ny;
+    const double2* u0;
+    const double* V;
+    const double2* st[3];
+    double2* phi[3];
+};
+
+__global__ void eval_phi_kernel(const PhiArgs a, const __grid_constant__ SweepConsts c) {
+    const size_t n = static_cast<size_t>(a.nx) * a.ny;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(k / a.nx), i = static_cast<int>(k - static_cast<size_t>(j) * a.nx);
+        const size_t kl = static_cast<size_t>(j) * a.nx + wrap_index(i - 1, a.nx);
+        const size_t kr = static_cast<size_t>(j) * a.nx + wrap_index(i + 1, a.nx);
+        const size_t kd = static_cast<size_t>(wrap_index(j - 1, a.ny)) * a.nx + i;
+        const size_t ku = static_cast<size_t>(wrap_index(j + 1, a.ny)) * a.nx + i;
+        const double2* zp[4] = {a.u0, a.st[0], a.st[1], a.st[2]};
+        double2 z[4], w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            z[q] = zp[q][k];
+            w[q] = kv_site(c, a.V[k], z[q], zp[q][kl], zp[q][kr], zp[q][kd], zp[q][ku]);
+        }
+        double2 phi[3];
+        phi_site(c, z, w, phi);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.phi[q][k] = phi[q];
+    }
+}
+
+int grid_for(size_t n, int threads) {
+    const size_t b = (n + threads - 1) / threads;
+    return static_cast<int>(b < 148 * 16 ? (b ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+size_t tiled_smem_bytes(int m, bool first) {
+    switch (m * 2 + (first ? 1 : 0)) {
+        case 0: return tiled_smem<0, false>();
+        case 1: return tiled_smem<0, true>();
+        case 2: return tiled_smem<1, false>();
+        case 3: return tiled_smem<1, true>();
+        case 4: return tiled_smem<2, false>();
+        case 5: return tiled_smem<2, true>();
+        case 6: return tiled_smem<3, false>();
+        case 7: return tiled_smem<3, true>();
+    }
+    return 0;
+}
+
+cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
+                               cudaStream_t s) {
+    switch (m * 2 + (first ? 1 : 0)) {
+        case 0: return launch_tiled<0, false>(a, c, s);
+        case 1: return launch_tiled<0, true>(a, c, s);
+        case 2: return launch_tiled<1, false>(a, c, s);
+        case 3: return launch_tiled<1, true>(a, c, s);
+        case 4: return launch_tiled<2, false>(a, c, s);
+        case 5: return launch_tiled<2, true>(a, c, s);
+        case 6: return launch_tiled<3, false>(a, c, s);
+        case 7: return launch_tiled<3, true>(a, c, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int obs_blocks(int nx, int ny) {
+    return grid_for(static_cast<size_t>(nx) * ny, kObsThreads);
+}
+
+cudaError_t launch_observables(const ObsArgs& a, double* out5, cudaStream_t s) {
+    const int nb = obs_blocks(a.nx, a.ny);
+    observables_partial_kernel<<<nb, kObsThreads, 0, s>>>(a);
+    observables_finalize_kernel<<<1, 256, 0, s>>>(a.partial, nb, out5);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_kv(int nx, int ny, double cx, double cy, const double2* u, const double* V,
+                            double gamma, bool rhs, double2* y, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(nx) * ny;
+    apply_kv_kernel<<<grid_for(n, 256), 256, 0, s>>>(nx, ny, cx, cy, u, V, gamma, rhs, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_phi(int nx, int ny, const double2* u0, const double* V,
+                            const double2* const st[3], double2* const phi[3],
+                            const SweepConsts& c, cudaStream_t s) {
+    PhiArgs a;
+    a.nx = nx;
+    a.ny = ny;
+    a.u0 = u0;
+    a.V = V;
+    for (int q = 0; q < 3; ++q) {
+        a.st[q] = st[q];
+        a.phi[q] = phi[q];
+    }
+    const size_t n = static_cast<size_t>(nx) * ny;
+    eval_phi_kernel<<<grid_for(n, 128), 128, 0, s>>>(a, c);
+    return cudaGetLastError();
+}
+
+}  // namespace mb4cu

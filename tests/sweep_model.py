@@ -1,0 +1,58 @@
+"""TEST INFRASTRUCTURE: numpy model of one matrix-free stage sweep (the GPU algorithm).
+
+Used to check single GPU sweeps and sweep counts; it is not the oracle (the
+oracle restates the reference's simplified Newton, oracle/mb4_oracle.c).
+"""
+import numpy as np
+
+
+def kv(u, V, nx, ny, cx=1.0, cy=1.0):
+    U = u.reshape(ny, nx)
+    y = (2 * cx + 2 * cy) * U - cx * (np.roll(U, 1, 1) + np.roll(U, -1, 1)) \
+        - cy * (np.roll(U, 1, 0) + np.roll(U, -1, 0)) + V.reshape(ny, nx) * U
+    return y.reshape(-1)
+
+
+def jac(t, u0, V, gamma, nx, ny, cx=1.0, cy=1.0):
+    a = kv(t, V, nx, ny, cx, cy)
+    nl = 2 * np.abs(u0) ** 2 * t + u0 ** 2 * np.conj(t)
+    return -1j * a + 1j * gamma * nl
+
+
+def sweep(u0, U, V, gamma, h, scheme, m, nx, ny, cx=1.0, cy=1.0):
+    """One stage iteration; returns (U_new, ||r||_inf over split reals)."""
+    E, L, WA = scheme.E(), scheme.gl6_L(), scheme.gl6_WA()
+    T, Ti, lam = scheme.t(), scheme.t_inv(), np.array(scheme.eigenvalues())
+    if U is None:
+        U = [u0, u0, u0]
+    z = [u0] + list(U)
+    w = [kv(zj, V, nx, ny, cx, cy) for zj in z]
+    Uq = [sum(L[q, a] * z[a] for a in range(4)) for q in range(6)]
+    gq = [np.abs(x) ** 2 * x for x in Uq]
+    phi = []
+    for i in range(3):
+        kc = sum(E[i, j] * w[j] for j in range(4))
+        cub = sum(WA[i, q] * gq[q] for q in range(6))
+        R = -1j * kc + 1j * gamma * cub
+        phi.append(U[i] - u0 - h * R)
+    if m == 0:
+        r = [-p for p in phi]
+    else:
+        pb = [sum(Ti[k, i] * phi[i] for i in range(3)) for k in range(3)]
+        b = list(pb)
+        for _ in range(m):
+            b = [pb[k] + h * lam[k] * jac(b[k], u0, V, gamma, nx, ny, cx, cy) for k in range(3)]
+        rb = [-x for x in b]
+        r = [sum(T[i, k] * rb[k] for k in range(3)) for i in range(3)]
+    Un = [U[i] + r[i] for i in range(3)]
+    rmax = max(max(np.abs(x.real).max(), np.abs(x.imag).max()) for x in r)
+    return Un, rmax
+
+
+def step(u0, V, gamma, h, scheme, m, nx, ny, eps, max_iters=50):
+    U = None
+    for it in range(1, max_iters + 1):
+        U, r = sweep(u0, U, V, gamma, h, scheme, m, nx, ny)
+        if r <= eps:
+            return U[2], it
+    raise RuntimeError("no convergence")

@@ -1,0 +1,142 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Tolerances (written here, per BASELINE.json north_star):
+  - state after 10 steps: relative L2 <= 1e-10 against the reference oracle;
+  - relative energy drift |H(t)-H(0)|/|H(0)| <= 1e-13 over the run;
+  - operators (Phi, (K+V)u, f(u), observables) <= 1e-12 / 1e-13 as the
+    reference's own tests use (test_mb4_integrator.cpp:78-91, test_lattice.cpp:177-198).
+"""
+import numpy as np
+import pytest
+
+import sweep_model as SM
+from oracle import oracle as O
+from paper_2003_04345_b200 import configs, nls2d
+
+pytestmark = pytest.mark.gpu
+
+TWO_PI = 2.0 * np.pi
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def random_state(n, seed, amp=1.0):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-amp, amp, n) + 1j * rng.uniform(-amp, amp, n)).astype(np.complex128)
+
+
+# ----------------------------------------------------------------------------- operators
+
+
+@pytest.mark.parametrize("nx,ny", [(4, 4), (5, 4), (2, 3), (64, 48)])
+def test_apply_kv_and_rhs_match_oracle(nx, ny):
+    g = nls2d.GridSpec(nx, ny, TWO_PI, 4.0)
+    V = np.linspace(-2.0, 3.0, nx * ny)
+    model = nls2d.GridModel(g, 0.3, V)
+    o = O.Oracle(nx, ny, 0.3, V, cx=model.cx, cy=model.cy)
+    u = random_state(nx * ny, 5)
+    scale = np.abs(o.apply_kv(u)).max()
+    assert np.abs(model.apply_kv(u) - o.apply_kv(u)).max() <= 1e-13 * scale
+    assert np.abs(nls2d.rhs(model, u) - o.rhs(u)).max() <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("gamma", [0.0, 0.1, -2.0])
+def test_eval_phi_matches_reference_w_form(gamma):
+    # Phi via the GL-6 quadrature form vs the reference's W contraction
+    # (mb4_integrator.cpp:159-192); tolerance of test_mb4_integrator.cpp:89.
+    g = nls2d.GridSpec(4, 4, TWO_PI, TWO_PI)
+    V = nls2d.build_delta_potential(g, 0.0 if gamma == 0.0 else -2.0)
+    model = nls2d.GridModel(g, gamma, V)
+    scheme = nls2d.Mb4Scheme()
+    u0 = random_state(16, 31)
+    st = [random_state(16, 40 + i) for i in range(3)]
+    phi = nls2d.eval_phi(model, scheme, u0, st, 0.01)
+    o = O.Oracle(4, 4, gamma, V, cx=model.cx, cy=model.cy)
+    ref = o.eval_phi(u0, st, 0.01)
+    assert max(np.abs(a - b).max() for a, b in zip(phi, ref)) <= 1e-12
+    if O.ref_available():
+        rr = O.ref_eval_phi(4, 4, TWO_PI, TWO_PI, gamma, V, u0, st, 0.01)
+        assert max(np.abs(a - b).max() for a, b in zip(phi, rr)) <= 1e-12
+
+
+def test_eval_phi_fixed_point_at_zero_step():
+    # test_mb4_integrator.cpp:67-76
+    g = nls2d.GridSpec(4, 4, TWO_PI, TWO_PI)
+    model = nls2d.GridModel(g, 0.1)
+    u0 = random_state(16, 9)
+    phi = nls2d.eval_phi(model, nls2d.Mb4Scheme(), u0, [u0, u0, u0], 0.0)
+    assert all(np.abs(p).max() == 0.0 for p in phi)
+
+
+def test_observables_match_oracle():
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    model = configs.model_for(cfg, V)
+    got = nls2d.observables(model, psi)
+    o = O.Oracle(cfg.nx, cfg.ny, cfg.gamma, V).observables(psi)
+    for f in nls2d.OBS_FIELDS:
+        a, b = getattr(got, f), getattr(o, f)
+        assert abs(a - b) <= 1e-13 * max(1.0, abs(b)), (f, a, b)
+
+
+# ----------------------------------------------------------------------------- single sweeps
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    model = configs.model_for(cfg, V)
+    scheme = nls2d.Mb4Scheme()
+    ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon)
+    with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=m, kernel=kernel) as s:
+        s.set_state(psi)
+        st = nls2d.StepStats()
+        s.step(cfg.dt, st)
+        got = s.get_state()
+    assert st.newton_iters == its
+    assert rel(got, ref) <= 1e-13
+
+
+# ----------------------------------------------------------------------------- stepping parity
+
+
+def _oracle_steps(cfg, V, psi, nsteps):
+    if O.ref_available():
+        solver = "direct" if cfg.sites <= 4096 else "gmres"
+        u, obs, iters, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi,
+                                     cfg.dt, nsteps, eps=cfg.epsilon, solver=solver)
+        return u, obs
+    u, obs, _ = O.Oracle(cfg.nx, cfg.ny, cfg.gamma, V).run(psi, cfg.dt, nsteps, eps=cfg.epsilon)
+    return u, obs
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("m", [0, 2, 3])
+def test_ten_steps_match_oracle(name, m):
+    cfg = configs.CONFIGS[name]
+    V, psi = configs.make_inputs(cfg)
+    ref, ref_obs = _oracle_steps(cfg, V, psi, 10)
+    model = configs.model_for(cfg, V)
+    with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg), neumann_terms=m) as s:
+        s.set_state(psi)
+        obs, iters = s.run(cfg.dt, 10)
+        got = s.get_state()
+    assert rel(got, ref) <= 1e-10
+    H0 = ref_obs[0, 3]
+    assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * abs(H0)
+    assert np.abs(obs[:, 3] - obs[0, 3]).max() <= 1e-13 * abs(obs[0, 3])
+
+
+def test_mb4_step_drop_in_matches_oracle():
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    model = configs.model_for(cfg, V)
+    stats = nls2d.StepStats()
+    u1 = nls2d.mb4_step(model, nls2d.Mb4Scheme(), psi, cfg.dt, configs.newton_for(cfg), stats=stats)
+    ref, _ = _oracle_steps(cfg, V, psi, 1)
+    assert rel(u1, ref) <= 1e-10
+    assert stats.newton_iters > 0 and stats.halvings == 0
