@@ -1,0 +1,451 @@
+#!/usr/bin/env python3
+"""MB4 FP64 lattice-site*steps/s on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+
+Workload (default): BASELINE configs[4] ("cfg5"), the weak-scaling lattice of
+8192^2 sites per GPU (the metric's 1/2/4/8-GPU, % HBM roofline configuration
+and the largest single-GPU config); --config cfg1..cfg4 selects the others.
+One "step" = one MB4 time step (all stage sweeps to ||r||_inf <= 1e-14) over the
+whole lattice.  Inputs are synthetic and seeded (configs.py); the state and the
+stage buffers (>= 3 GiB at 8192^2) are far larger than the 126 MB L2.  For
+lattices whose working set fits in L2 the bench times every step separately
+and flushes L2 between steps.
+
+Rank 0 prints ONE JSON line.  Under torchrun (N > 1) every rank steps its own
+8192^2 block; `value` is the whole-job total, timed as the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "MB4 FP64 lattice-site*steps/s"
+UNIT = "site*steps/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--neumann", type=int, default=-1)
+    ap.add_argument("--kernel", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="warm-up + a few steps, no JSON extras (for ncu captures)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world: int, rank: int, local: int):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.dist = dist
+            self.torch = torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(cfg, V, psi, budget_s: float = 20.0):
+    """The reference path (oracle/_ref, StepDriver(MB4) -> mb4_step, solver=gmres,
+    workers=3) on a bounded sample of the workload: a 256x256 window of the
+    same V / psi arrays stepped with the config's dt, g and tolerance."""
+    from oracle import oracle as O
+
+    win = min(256, cfg.nx, cfg.ny)
+    Vs = np.ascontiguousarray(V.reshape(cfg.ny, cfg.nx)[:win, :win]).reshape(-1)
+    ps = np.ascontiguousarray(psi.reshape(cfg.ny, cfg.nx)[:win, :win]).reshape(-1)
+    if np.vdot(ps, ps).real < 1e-30:
+        ps = ps + 1e-3
+    kind = "reference" if O.ref_available() else "port"
+    steps, total_steps, total_s = 1, 0, 0.0
+    u = ps
+    while total_s < budget_s and total_steps < 64:
+        if kind == "reference":
+            u, _, _, secs = O.ref_run(win, win, float(win), float(win), cfg.gamma, Vs, u, cfg.dt,
+                                      steps, eps=cfg.epsilon, solver="gmres", workers=3,
+                                      record=False)
+        else:
+            t0 = time.perf_counter()
+            u, _, _ = O.Oracle(win, win, cfg.gamma, Vs).run(u, cfg.dt, steps, eps=cfg.epsilon)
+            secs = time.perf_counter() - t0
+        total_steps += steps
+        total_s += secs
+        steps = min(steps * 2, 16)
+    return {
+        "value": win * win * total_steps / total_s,
+        "unit": UNIT,
+        "cores": 3 if kind == "reference" else 1,
+        "kind": kind,
+        "sample": (f"{win}x{win} window of the {cfg.name} inputs, {total_steps} MB4 steps "
+                   f"(dt={cfg.dt}, eps={cfg.epsilon}), reference solver=gmres (ILU0+GMRES(50)), "
+                   f"workers=3, {total_s:.1f} s"),
+    }
+
+
+# ----------------------------------------------------------------------------- our arm
+
+
+def run_ours(args, d: Dist):
+    import torch
+
+    from paper_2003_04345_b200 import configs, nls2d
+
+    torch.cuda.set_device(d.local)
+    base = configs.CONFIGS[args.config]
+    cfg = base
+    if args.config == "cfg5":
+        cfg = base.with_lattice(8192, 8192)
+    # each rank steps its own lattice block of the configured size (weak scaling)
+    t_gen = time.perf_counter()
+    V, psi = configs.make_inputs(cfg)
+    t_gen = time.perf_counter() - t_gen
+    model = configs.model_for(cfg, V)
+    sess = nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg),
+                         neumann_terms=None if args.neumann < 0 else args.neumann,
+                         device=d.local, kernel=args.kernel)
+    sess.set_state(psi)
+    obs0 = sess.observables()
+    n = cfg.sites
+    working_set = n * (16 + 8 + 96)
+    flush = working_set < 2 * L2_BYTES
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if flush else None
+
+    # warm-up
+    for _ in range(args.warmup):
+        sess.step(cfg.dt)
+    torch.cuda.synchronize()
+
+    sess.profile_reset()
+    sess.profile_enable(True)
+    stats = nls2d.StepStats()
+    clocks = ClockSampler(d.local)
+    d.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    if not flush:
+        t0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            sess.step(cfg.dt, stats)
+        ev1.record()
+        torch.cuda.synchronize()
+        step_ms_total = ev0.elapsed_time(ev1)
+        wall = time.perf_counter() - t0
+    else:
+        step_ms_total = 0.0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush_buf.zero_()
+            torch.cuda.synchronize()
+            st = nls2d.StepStats()
+            sess.step(cfg.dt, st)
+            stats.newton_iters += st.newton_iters
+            stats.halvings += st.halvings
+            step_ms_total += 1e3 * st.solve_seconds
+        wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    d.barrier()
+    prof = sess.profile()
+    sess.profile_enable(False)
+    obs1 = sess.observables()
+    ms = d.max(step_ms_total)
+    total_sites = d.sum(float(n))
+    value = total_sites * args.steps / (ms * 1e-3)
+    drift = abs(obs1.total_energy - obs0.total_energy) / abs(obs0.total_energy)
+    drift = d.max(drift)
+
+    peak, peak_kind = measured_peaks()
+    kern_ms = prof["kernel_ms"]
+    launches = max(1, prof["launches"])
+    achieved = prof["alg_bytes"] / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+    sweeps_per_step = prof["sweeps"] / max(1, args.steps)
+    step_alg_bytes = prof["alg_bytes"] / max(1, args.steps)
+
+    result = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": d.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded defects + Gaussian packets, configs.py)",
+        "config": {
+            "workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} sites per GPU, dt={cfg.dt}, g={cfg.g}, "
+                        f"{cfg.defect_frac:.0%} defects, {cfg.npackets} packet(s) sigma={cfg.sigma}, eps={cfg.epsilon}",
+            "lattice": [cfg.nx, cfg.ny],
+            "sites_per_gpu": n,
+            "neumann_terms": args.neumann if args.neumann >= 0 else 2,
+            "kernel": "tiled" if args.kernel == 1 else "default",
+            "l2": "flushed between steps" if flush else "inputs larger than L2 (state+stages >= 3 GiB)",
+            "parallelism": "replicas" if d.world > 1 else "single",
+        },
+        "sweeps_per_step": sweeps_per_step,
+        "energy_drift": drift,
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": None,
+            "peak_kind": peak_kind,
+            "kernel": "stage sweep",
+            "alg_bytes_per_step": step_alg_bytes,
+            "kernel_ms_per_launch": kern_ms / launches,
+            "step_share": kern_ms / max(1e-9, step_ms_total),
+        },
+        "gpu_launches": int(prof["launches"] + prof["other_launches"]),
+        "clocks": clk,
+        "wall_s_timed": wall,
+        "input_gen_s": t_gen,
+    }
+
+    # end-to-end through the public API with host buffers (mb4_step contract)
+    if not args.no_e2e:
+        host = torch.empty(2 * n, dtype=torch.float64, pin_memory=True)
+        host.numpy()[:] = psi.view(np.float64)
+        hv = host.numpy().view(np.complex128)
+        import ctypes as C
+
+        from paper_2003_04345_b200 import _lib
+
+        L = _lib.lib()
+        ptr = C.cast(host.data_ptr(), C.POINTER(C.c_double))
+        k_e2e = max(1, min(args.steps, 10))
+        d.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            L.mb4cu_set_state(sess._ctx, ptr)   # H2D of the step's input state
+            sess.step(cfg.dt)
+            L.mb4cu_get_state(sess._ctx, ptr)   # D2H of the step's result
+        e2e_s = d.max(time.perf_counter() - t0)
+        result["e2e"] = {
+            "value": total_sites * k_e2e / e2e_s,
+            "unit": UNIT,
+            "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 16 * n,
+            "steps": k_e2e,
+            "api": "mb4cu_set_state -> mb4cu_step -> mb4cu_get_state (host pinned buffers)",
+        }
+        del hv
+
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = cpu_baseline(cfg, V, psi)
+        except Exception as exc:  # keep the GPU line even if the CPU leg fails
+            result["cpu_baseline"] = {"value": None, "error": str(exc)}
+    sess.close()
+    return result
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args, d: Dist):
+    """The reference CPU path (oracle/_ref) on the host cores, same metric/config."""
+    from oracle import oracle as O
+    from paper_2003_04345_b200 import configs
+
+    base = configs.CONFIGS[args.config]
+    cfg = base.with_lattice(8192, 8192) if args.config == "cfg5" else base
+    win = min(256, cfg.nx, cfg.ny)
+    # sample: a 256x256 window of the same config's inputs (generated directly)
+    sample = cfg.with_lattice(win, win)
+    V, psi, psum = configs.make_block(cfg, 0, 0, win, win)
+    if psum <= 1e-30:
+        psi = psi + 1e-3
+    kind = "reference" if O.ref_available() else "port"
+    u = psi
+    for _ in range(args.warmup):
+        u = _ref_step(O, kind, sample, V, u)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u = _ref_step(O, kind, sample, V, u)
+    secs = time.perf_counter() - t0
+    value = win * win * args.steps / secs
+    cores = 3 if kind == "reference" else 1
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "impl": "reference",
+        "n_gpus": d.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded defects + Gaussian packets, configs.py)",
+        "config": {"workload": f"{cfg.name} (sampled: {win}x{win} window per step)",
+                   "lattice": [cfg.nx, cfg.ny]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{win}x{win} window of {cfg.name} inputs, one MB4 step per "
+                                   f"bench step, reference StepDriver(MB4) solver=gmres workers=3"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def _ref_step(O, kind, cfg, V, u):
+    if kind == "reference":
+        u, _, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, u, cfg.dt, 1,
+                               eps=cfg.epsilon, solver="gmres", workers=3, record=False)
+    else:
+        u, _, _ = O.Oracle(cfg.nx, cfg.ny, cfg.gamma, V).run(u, cfg.dt, 1, eps=cfg.epsilon)
+    return u
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        res = run_reference(args, Dist(1, 0, 0))
+        print(json.dumps(res))
+        return 0
+    d = Dist(world, rank, local)
+    res = run_ours(args, d)
+    if rank == 0:
+        print(json.dumps(res))
+    d.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -162,6 +162,22 @@ int mb4cu_make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny
 /* psi *= s  (host, multithreaded) */
 int mb4cu_scale_state(double* psi, size_t nsites, double s, int threads);
 
+/* Kernel-level profiling of the stage sweeps (CUDA events around every sweep
+ * launch, on the context stream).  alg_bytes counts the algorithmic HBM bytes
+ * of the sweeps: 72 B/site for the first sweep of a step (u0, V in; U out) and
+ * 120 B/site for the others (u0, V, U in; U out) -- see DESIGN.md. */
+typedef struct {
+    double kernel_ms;         /* summed device time of the sweep launches            */
+    long long launches;       /* sweep-kernel launches                                */
+    long long sweeps;         /* stage sweeps executed                                */
+    double alg_bytes;         /* algorithmic bytes of those sweeps                    */
+    long long other_launches; /* energy-monitor / helper kernels                      */
+} mb4cu_profile;
+
+int mb4cu_profile_enable(mb4cu_ctx* ctx, int on);
+int mb4cu_profile_reset(mb4cu_ctx* ctx);
+int mb4cu_profile_get(mb4cu_ctx* ctx, mb4cu_profile* out);
+
 /* Library version / build string. */
 const char* mb4cu_version(void);
 

@@ -71,6 +71,16 @@ class Obs(C.Structure):
         "participation", "raw_quartic")]
 
 
+class Profile(C.Structure):
+    _fields_ = [
+        ("kernel_ms", D),
+        ("launches", C.c_longlong),
+        ("sweeps", C.c_longlong),
+        ("alg_bytes", D),
+        ("other_launches", C.c_longlong),
+    ]
+
+
 class Inputs(C.Structure):
     _fields_ = [
         ("gnx", I), ("gny", I),
@@ -124,6 +134,9 @@ def lib() -> C.CDLL:
         "mb4cu_make_inputs": (I, [C.POINTER(Inputs), I, I, I, I, DP, DP, DP]),
         "mb4cu_scale_state": (I, [DP, C.c_size_t, D, I]),
         "mb4cu_version": (C.c_char_p, []),
+        "mb4cu_profile_enable": (I, [P, I]),
+        "mb4cu_profile_reset": (I, [P]),
+        "mb4cu_profile_get": (I, [P, C.POINTER(Profile)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -144,5 +157,6 @@ EXPORTED = [
     "mb4cu_create_error", "mb4cu_set_state", "mb4cu_get_state", "mb4cu_set_state_device",
     "mb4cu_get_state_device", "mb4cu_step", "mb4cu_run", "mb4cu_observables",
     "mb4cu_set_stream", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
-    "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version",
+    "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
+    "mb4cu_profile_reset", "mb4cu_profile_get",
 ]

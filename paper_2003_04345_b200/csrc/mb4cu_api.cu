@@ -36,6 +36,17 @@ struct mb4cu_ctx {
     double* d_obs5 = nullptr;
     double* h_obs5 = nullptr;  // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t pev0 = nullptr, pev1 = nullptr;
+    // persistent-kernel path
+    unsigned long long* d_rmax_arr = nullptr;  // [max_iters]
+    double* d_obs_march = nullptr;             // [grid][kObsFields]
+    mb4cu::StepStatus* d_status = nullptr;
+    mb4cu::StepStatus* h_status = nullptr;     // pinned
+    bool obs_cached = false;                   // energy sums of the current u0 known
+    double obs_cache[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
+    double entry_obs[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
+    bool profiling = false;
+    mb4cu_profile prof{};
     std::string err;
 };
 
@@ -82,9 +93,51 @@ double decode_bits(unsigned long long b) {
     return d;
 }
 
+// Persistent path: the whole stage iteration of one sub-step in one cooperative
+// launch (sweep_march.cu); the host reads back a 80-byte status block.
+int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
+    const SweepConsts c = make_consts(ctx, h);
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * ctx->max_iters,
+                                  ctx->stream));
+    if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
+    MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
+                                           ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
+                                           ctx->max_iters, ctx->eps, 1, c, ctx->device, ctx->stream));
+    if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(mb4cu::StepStatus),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const mb4cu::StepStatus st = *ctx->h_status;
+    if (ctx->profiling) {
+        float ms = 0.f;
+        MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->pev0, ctx->pev1));
+        ctx->prof.kernel_ms += ms;
+        ctx->prof.launches += 1;
+        ctx->prof.sweeps += st.sweeps;
+        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (st.sweeps - 1));
+    }
+    // the first sweep evaluated the energy sums of the entry state
+    for (int f = 0; f < mb4cu::kObsFields; ++f) ctx->obs_cache[f] = st.obs[f];
+    ctx->obs_cached = true;
+    *sweeps = st.sweeps;
+    *last_res = st.rlast;
+    if (!std::isfinite(st.rlast)) {
+        *last_res = INFINITY;
+        return fail(ctx, MB4CU_NONCONVERGED, "stage iteration diverged (non-finite update)");
+    }
+    if (st.converged) {
+        std::swap(ctx->u0, ctx->U[st.set][2]);
+        ctx->obs_cached = false;
+        return MB4CU_OK;
+    }
+    return fail(ctx, MB4CU_NONCONVERGED,
+                "stage iteration: no convergence after " + std::to_string(ctx->max_iters) + " sweeps");
+}
+
 // One MB4 sub-step of size h on ctx->u0: sweeps until ||r||_inf <= eps
 // (newton_solve, mb4_integrator.cpp:194-255).  On success u0 <- U3 (c3 = 1).
 int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
+    if (ctx->kernel == 0) return substep_march(ctx, h, sweeps, last_res);
     const SweepConsts c = make_consts(ctx, h);
     int cur = -1;
     *sweeps = 0;
@@ -101,10 +154,20 @@ int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         }
         a.rmax = ctx->d_rmax;
         MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
+        if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
         MB4_CUDA(ctx, mb4cu::launch_sweep_tiled(ctx->m, cur < 0, a, c, ctx->stream));
+        if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
         MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long),
                                       cudaMemcpyDeviceToHost, ctx->stream));
         MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (ctx->profiling) {
+            float ms = 0.f;
+            MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->pev0, ctx->pev1));
+            ctx->prof.kernel_ms += ms;
+            ctx->prof.launches += 1;
+            ctx->prof.sweeps += 1;
+            ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (cur < 0 ? 72.0 : 120.0);
+        }
         *sweeps = it;
         const double r = decode_bits(*ctx->h_rmax);
         *last_res = r;
@@ -218,6 +281,20 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if ((e = cudaMallocHost(&ctx->h_obs5, sizeof(double) * 8)) != cudaSuccess) return bail(e, "cudaMallocHost");
     if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    if (ctx->kernel == 0) {
+        const int grid = mb4cu::march_grid_size(ctx->m, ctx->device);
+        if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
+        if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * ctx->max_iters)) != cudaSuccess)
+            return bail(e, "cudaMalloc(rmax_arr)");
+        if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * grid)) != cudaSuccess)
+            return bail(e, "cudaMalloc(obs_march)");
+        if ((e = cudaMalloc(&ctx->d_status, sizeof(mb4cu::StepStatus))) != cudaSuccess)
+            return bail(e, "cudaMalloc(status)");
+        if ((e = cudaMallocHost(&ctx->h_status, sizeof(mb4cu::StepStatus))) != cudaSuccess)
+            return bail(e, "cudaMallocHost(status)");
+    }
+    if ((e = cudaEventCreate(&ctx->pev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    if ((e = cudaEventCreate(&ctx->pev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if ((e = cudaMemcpy(ctx->V, p->V, ctx->n * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
         return bail(e, "cudaMemcpy(V)");
     if ((e = cudaMemset(ctx->u0, 0, sb)) != cudaSuccess) return bail(e, "cudaMemset(u0)");
@@ -239,8 +316,14 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs_partial);
     cudaFree(ctx->d_obs5);
     cudaFreeHost(ctx->h_obs5);
+    cudaFree(ctx->d_rmax_arr);
+    cudaFree(ctx->d_obs_march);
+    cudaFree(ctx->d_status);
+    cudaFreeHost(ctx->h_status);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->pev0) cudaEventDestroy(ctx->pev0);
+    if (ctx->pev1) cudaEventDestroy(ctx->pev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return MB4CU_OK;
@@ -306,6 +389,8 @@ int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats) {
         for (int s = 0; s < sub; ++s) {
             int sw = 0;
             rc = substep(ctx, hs, &sw, &last);
+            if (hv == 0 && s == 0)  // energy sums of the step's entry state (fused path)
+                std::memcpy(ctx->entry_obs, ctx->obs_cache, sizeof(ctx->entry_obs));
             attempt += sw;
             if (rc == MB4CU_NONCONVERGED) {
                 ok = false;
@@ -343,6 +428,41 @@ int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats) {
     return MB4CU_OK;
 }
 
+int mb4cu_profile_enable(mb4cu_ctx* ctx, int on) {
+    if (!ctx) return MB4CU_INVALID;
+    ctx->profiling = on != 0;
+    return MB4CU_OK;
+}
+
+int mb4cu_profile_reset(mb4cu_ctx* ctx) {
+    if (!ctx) return MB4CU_INVALID;
+    ctx->prof = mb4cu_profile{};
+    return MB4CU_OK;
+}
+
+int mb4cu_profile_get(mb4cu_ctx* ctx, mb4cu_profile* out) {
+    if (!ctx || !out) return MB4CU_INVALID;
+    *out = ctx->prof;
+    return MB4CU_OK;
+}
+
+// Energy sums -> Observables with the reference's health check (lattice.cpp:113-127).
+static int finish_obs(mb4cu_ctx* ctx, const double* sums, mb4cu_obs* out) {
+    const double qr = sums[0], qi = sums[1], prob = sums[2], quart = sums[3], ext = sums[4];
+    // u^H K u is real for symmetric K; imaginary residue is a health check (lattice.cpp:123-126)
+    const double imag_scale = std::max(std::fabs(qr), (4.0 * ctx->cx + 4.0 * ctx->cy) * prob);
+    if (std::fabs(qi) > 1e-12 * imag_scale && imag_scale > 0.0)
+        return fail(ctx, MB4CU_NUMERIC, "observables: non-real kinetic quadratic form");
+    out->u_kinetic = qr;
+    out->u_nonlinear = -0.5 * ctx->gamma * quart;
+    out->u_external = ext;
+    out->total_energy = out->u_kinetic + out->u_nonlinear + out->u_external;
+    out->probability = prob;
+    out->raw_quartic = quart;
+    out->participation = prob > 0.0 ? quart / (prob * prob) : 0.0;
+    return MB4CU_OK;
+}
+
 int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out) {
     if (!ctx || !out) return fail(ctx, MB4CU_INVALID, "observables: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -356,23 +476,11 @@ int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out) {
     a.V = ctx->V;
     a.partial = ctx->d_obs_partial;
     MB4_CUDA(ctx, mb4cu::launch_observables(a, ctx->d_obs5, ctx->stream));
+    ctx->prof.other_launches += 2;
     MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_obs5, ctx->d_obs5, sizeof(double) * mb4cu::kObsFields,
                                   cudaMemcpyDeviceToHost, ctx->stream));
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    const double qr = ctx->h_obs5[0], qi = ctx->h_obs5[1], prob = ctx->h_obs5[2],
-                 quart = ctx->h_obs5[3], ext = ctx->h_obs5[4];
-    // u^H K u is real for symmetric K; imaginary residue is a health check (lattice.cpp:123-126)
-    const double imag_scale = std::max(std::fabs(qr), (4.0 * ctx->cx + 4.0 * ctx->cy) * prob);
-    if (std::fabs(qi) > 1e-12 * imag_scale && imag_scale > 0.0)
-        return fail(ctx, MB4CU_NUMERIC, "observables: non-real kinetic quadratic form");
-    out->u_kinetic = qr;
-    out->u_nonlinear = -0.5 * ctx->gamma * quart;
-    out->u_external = ext;
-    out->total_energy = out->u_kinetic + out->u_nonlinear + out->u_external;
-    out->probability = prob;
-    out->raw_quartic = quart;
-    out->participation = prob > 0.0 ? quart / (prob * prob) : 0.0;
-    return MB4CU_OK;
+    return finish_obs(ctx, ctx->h_obs5, out);
 }
 
 static void put_obs(double* row, const mb4cu_obs& o) {
@@ -390,12 +498,15 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     if (!ctx) return MB4CU_INVALID;
     if (nsteps < 0) return fail(ctx, MB4CU_INVALID, "run: nsteps must be >= 0");
     mb4cu_obs o{};
-    if (obs_series) {
-        const int rc = mb4cu_observables(ctx, &o);
-        if (rc) return rc;
-        put_obs(obs_series, o);
-    }
+    // With the persistent kernel the energy monitor of each step's entry state is
+    // fused into that step's first sweep; only the final state needs its own pass.
+    const bool fused = ctx->kernel == 0;
     for (int s = 1; s <= nsteps; ++s) {
+        if (obs_series && !fused) {
+            const int rc0 = mb4cu_observables(ctx, &o);
+            if (rc0) return rc0;
+            put_obs(obs_series + 7 * (s - 1), o);
+        }
         mb4cu_stats st{};
         const int rc = mb4cu_step(ctx, h, &st);
         if (stats) {
@@ -406,11 +517,16 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
         }
         if (rc) return rc;
         if (iters_series) iters_series[s - 1] = st.newton_iters;
-        if (obs_series) {
-            const int rc2 = mb4cu_observables(ctx, &o);
-            if (rc2) return rc2;
-            put_obs(obs_series + 7 * s, o);
+        if (obs_series && fused) {
+            const int rc1 = finish_obs(ctx, ctx->entry_obs, &o);
+            if (rc1) return rc1;
+            put_obs(obs_series + 7 * (s - 1), o);
         }
+    }
+    if (obs_series) {
+        const int rc2 = mb4cu_observables(ctx, &o);
+        if (rc2) return rc2;
+        put_obs(obs_series + 7 * nsteps, o);
     }
     return MB4CU_OK;
 }

@@ -52,7 +52,22 @@ struct ObsArgs {
     double* partial;   // [nblocks][kObsFields]
 };
 
-// Launchers (sweep_kernels.cu).
+// Result block of one persistent step launch (sweep_march.cu), copied to the host.
+struct StepStatus {
+    int sweeps;        // sweeps executed
+    int set;           // stage set holding the last iterate (0/1)
+    int converged;     // 1: ||r||_inf <= eps reached
+    int pad;
+    double rlast;      // ||r||_inf of the last sweep
+    double obs[kObsFields];  // energy sums of u0 (first sweep)
+};
+
+// Launchers (sweep_tiled.cu, sweep_march.cu).
+cudaError_t launch_step_march(int m, int nx, int ny, const double2* u0, const double* V,
+                              double2* const U[2][3], unsigned long long* rmax,
+                              double* obs_partial, void* status, int max_iters, double eps,
+                              int want_obs, const SweepConsts& c, int device, cudaStream_t s);
+int march_grid_size(int m, int device);
 size_t tiled_smem_bytes(int m, bool first);
 cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
                                cudaStream_t s);

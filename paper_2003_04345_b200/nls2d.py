@@ -364,6 +364,17 @@ class Session:
         self._check(rc, st.last_residual)
         return obs, iters
 
+    def profile_enable(self, on: bool = True):
+        self._check(self._L.mb4cu_profile_enable(self._ctx, int(on)))
+
+    def profile_reset(self):
+        self._check(self._L.mb4cu_profile_reset(self._ctx))
+
+    def profile(self) -> dict:
+        p = _lib.Profile()
+        self._check(self._L.mb4cu_profile_get(self._ctx, C.byref(p)))
+        return {f: getattr(p, f) for f, _ in _lib.Profile._fields_}
+
     def observables(self) -> Observables:
         o = _lib.Obs()
         self._check(self._L.mb4cu_observables(self._ctx, C.byref(o)))
