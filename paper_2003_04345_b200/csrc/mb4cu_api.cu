@@ -79,6 +79,14 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
     std::memcpy(c.T, s.T, sizeof(c.T));
     std::memcpy(c.Tinv, s.Tinv, sizeof(c.Tinv));
     for (int k = 0; k < 3; ++k) c.hlam[k] = h * s.lam[k];
+    // First sweep from U = (u0, u0, u0): Phi_i = -h c_i f(u0) with c_i = sum_j E[i][j]
+    // (the Lagrange basis sums to one), so phibar_k = -h (T^-1 c)_k f(u0).
+    double csum[3];
+    for (int i = 0; i < 3; ++i) csum[i] = s.E[i][0] + s.E[i][1] + s.E[i][2] + s.E[i][3];
+    for (int k = 0; k < 3; ++k) {
+        c.first_s[k] = -h * (s.Tinv[k][0] * csum[0] + s.Tinv[k][1] * csum[1] + s.Tinv[k][2] * csum[2]);
+        c.first_c[k] = h * csum[k];
+    }
     c.h = h;
     c.gamma = ctx->gamma;
     c.cx = ctx->cx;
@@ -100,9 +108,17 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * ctx->max_iters,
                                   ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
-    MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
-                                           ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
-                                           ctx->max_iters, ctx->eps, 1, c, ctx->device, ctx->stream));
+    if (ctx->kernel == 0 && ctx->m <= 2) {
+        MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
+                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
+                                                ctx->max_iters, ctx->eps, 1, c, ctx->device,
+                                                ctx->stream));
+    } else {
+        MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
+                                               ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
+                                               ctx->max_iters, ctx->eps, 1, c, ctx->device,
+                                               ctx->stream));
+    }
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
     MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(mb4cu::StepStatus),
                                   cudaMemcpyDeviceToHost, ctx->stream));
@@ -137,7 +153,7 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
 // One MB4 sub-step of size h on ctx->u0: sweeps until ||r||_inf <= eps
 // (newton_solve, mb4_integrator.cpp:194-255).  On success u0 <- U3 (c3 = 1).
 int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
-    if (ctx->kernel == 0) return substep_march(ctx, h, sweeps, last_res);
+    if (ctx->kernel != 1) return substep_march(ctx, h, sweeps, last_res);
     const SweepConsts c = make_consts(ctx, h);
     int cur = -1;
     *sweeps = 0;
@@ -281,8 +297,9 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if ((e = cudaMallocHost(&ctx->h_obs5, sizeof(double) * 8)) != cudaSuccess) return bail(e, "cudaMallocHost");
     if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
-    if (ctx->kernel == 0) {
-        const int grid = mb4cu::march_grid_size(ctx->m, ctx->device);
+    if (ctx->kernel != 1) {
+        const int grid = std::max(mb4cu::march_grid_size(ctx->m, ctx->device),
+                                  ctx->m <= 2 ? mb4cu::march2_grid_size(ctx->m, ctx->device) : 0);
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
         if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * ctx->max_iters)) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
@@ -500,7 +517,7 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     mb4cu_obs o{};
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
-    const bool fused = ctx->kernel == 0;
+    const bool fused = ctx->kernel != 1;
     for (int s = 1; s <= nsteps; ++s) {
         if (obs_series && !fused) {
             const int rc0 = mb4cu_observables(ctx, &o);

@@ -26,6 +26,8 @@ struct SweepConsts {
     double T[3][3];
     double Tinv[3][3];
     double hlam[3];     // h * lambda_k
+    double first_s[3];  // -h * (T^-1 rowsum(E))_k: phibar of the first sweep = first_s * f(u0)
+    double first_c[3];  // h * rowsum(E)_i: U_i after a Picard first sweep = u0 + first_c * f(u0)
     double h;
     double gamma;
     double cx, cy, diag;  // stencil: diag = 2cx + 2cy
@@ -62,12 +64,33 @@ struct StepStatus {
     double obs[kObsFields];  // energy sums of u0 (first sweep)
 };
 
+// Arguments of one persistent step launch (sweep_march*.cu).
+struct StepArgs {
+    int nx, ny;
+    int nbands;
+    long long total;            // nbands * ny band-rows
+    const double2* u0;
+    const double* V;
+    double2* U[2][3];
+    unsigned long long* rmax;   // [max_iters], zeroed by the host before launch
+    double* obs_partial;        // [gridDim.x][kObsFields]
+    StepStatus* status;
+    int max_iters;
+    double eps;
+    int want_obs;
+};
+
 // Launchers (sweep_tiled.cu, sweep_march.cu).
 cudaError_t launch_step_march(int m, int nx, int ny, const double2* u0, const double* V,
                               double2* const U[2][3], unsigned long long* rmax,
                               double* obs_partial, void* status, int max_iters, double eps,
                               int want_obs, const SweepConsts& c, int device, cudaStream_t s);
 int march_grid_size(int m, int device);
+cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const double* V,
+                               double2* const U[2][3], unsigned long long* rmax,
+                               double* obs_partial, void* status, int max_iters, double eps,
+                               int want_obs, const SweepConsts& c, int device, cudaStream_t s);
+int march2_grid_size(int m, int device);
 size_t tiled_smem_bytes(int m, bool first);
 cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
                                cudaStream_t s);

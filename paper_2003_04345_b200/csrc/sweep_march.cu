@@ -27,28 +27,12 @@
 
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
+#include "async_copy.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace mb4cu {
 namespace {
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 template <int M, int NT>
 struct MarchGeom {
@@ -67,21 +51,6 @@ struct MarchGeom {
     static constexpr size_t L0_bytes = M >= 1 ? sizeof(double2) * S0 * 3 * NT : 0;
     static constexpr size_t Ln_bytes = M >= 2 ? sizeof(double2) * (M - 1) * SL * 3 * NT : 0;
     static constexpr size_t bytes = u0_bytes + v_bytes + U_bytes + L0_bytes + Ln_bytes;
-};
-
-struct StepArgs {
-    int nx, ny;
-    int nbands;
-    long long total;            // nbands * ny band-rows
-    const double2* u0;
-    const double* V;
-    double2* U[2][3];
-    unsigned long long* rmax;   // [max_iters], zeroed by the host before launch
-    double* obs_partial;        // [gridDim.x][kObsFields]
-    StepStatus* status;
-    int max_iters;
-    double eps;
-    int want_obs;
 };
 
 template <int M, int NT, bool FIRST>

@@ -85,7 +85,7 @@ def test_observables_match_oracle():
 
 
 @pytest.mark.parametrize("m", [0, 1, 2, 3])
-@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("kernel", [0, 1, 2])
 def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
     cfg = configs.CONFIGS["cfg1"]
     V, psi = configs.make_inputs(cfg)
@@ -115,7 +115,7 @@ def _oracle_steps(cfg, V, psi, nsteps):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-@pytest.mark.parametrize("m", [0, 2, 3])
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
 def test_ten_steps_match_oracle(name, m):
     cfg = configs.CONFIGS[name]
     V, psi = configs.make_inputs(cfg)
