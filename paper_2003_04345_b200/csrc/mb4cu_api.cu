@@ -92,6 +92,17 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
     c.cx = ctx->cx;
     c.cy = ctx->cy;
     c.diag = 2.0 * ctx->cx + 2.0 * ctx->cy;
+    c.iso = ctx->cx == ctx->cy ? 1 : 0;
+    const double cc = ctx->cx;
+    c.inv_c = 1.0 / cc;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 4; ++j) c.Es[i][j] = cc * s.E[i][j];
+    c.gs = ctx->gamma / cc;
+    for (int k = 0; k < 3; ++k) {
+        c.hls[k] = cc * c.hlam[k];
+        c.first_ss[k] = cc * c.first_s[k];
+        c.first_cs[k] = cc * c.first_c[k];
+    }
     return c;
 }
 

@@ -28,6 +28,15 @@ struct SweepConsts {
     double hlam[3];     // h * lambda_k
     double first_s[3];  // -h * (T^-1 rowsum(E))_k: phibar of the first sweep = first_s * f(u0)
     double first_c[3];  // h * rowsum(E)_i: U_i after a Picard first sweep = u0 + first_c * f(u0)
+    // Isotropic form (cx == cy =: c): the stencil is evaluated as c * K' with K' the
+    // unit 5-point stencil; c is folded into these pre-scaled coefficients.
+    int iso;            // 1 if cx == cy
+    double inv_c;       // 1 / c
+    double Es[3][4];    // c * E
+    double gs;          // gamma / c
+    double hls[3];      // c * h * lambda_k
+    double first_ss[3]; // c * first_s
+    double first_cs[3]; // c * first_c
     double h;
     double gamma;
     double cx, cy, diag;  // stencil: diag = 2cx + 2cy

@@ -1,23 +1,28 @@
-// Production stage-sweep kernel, v2: persistent cooperative launch per MB4 step,
-// marching column bands with register windows.
+// Production stage-sweep kernel (v3): one persistent cooperative launch per MB4
+// step, marching column bands; vertical neighbours in registers / own-column
+// smem history, horizontal neighbours through shared-memory rows.
 //
-// Same algorithm as sweep_march.cu (Phi -> T^-1 -> M-term Neumann
-// (I - h lam_k J)^-1 -> T -> update -> ||r||_inf; see site_math.cuh) and the
-// same band / work split, but reorganised around the measured bottleneck of
-// v1 (shared-memory wavefronts and FP64 latency, profiles/):
-//  - Each thread keeps the VERTICAL neighbours of its own column in registers:
-//    a 3-row window of z = (u0, U1..U3), and 3-row windows of the Neumann
-//    level values (phibar, b1) and of the Jacobian diagonal.  Shared memory
-//    carries only the HORIZONTAL neighbours: z rows arrive by cp.async into a
-//    row ring; every level publishes its freshly computed row into a
-//    double-buffered row that the neighbours read one iteration later.
-//  - Level n works on row i - n at iteration i (level n-1 produced row i-n+1
-//    this iteration, in registers; the horizontal neighbours of row i-n were
-//    published last iteration), so one __syncthreads per row suffices.
-//  - The iteration loop is unrolled by 3 so every window slot is static.
+// Same algorithm as sweep_march.cu and sweep_tiled.cu (Phi -> T^-1 -> M-term
+// Neumann (I - h lam_k J)^-1 -> T -> update -> ||r||_inf; site_math.cuh) and
+// the same band / work split.  Organised around the measured limits of the
+// earlier versions (profiles/r01_*): shared-memory wavefronts, FP64 latency
+// with 8 warps/SM, and integer overhead.
+//  - Each thread keeps a 3-row register window of its own column of
+//    z = (u0, U1..U3).  z rows arrive by cp.async in a 6-row ring; only the
+//    centre row's left/right neighbours and the new own-column row are read
+//    from it.
+//  - Neumann level n works on row i - n at iteration i.  Every level publishes
+//    its row into a double-buffered smem row; the neighbours read it one
+//    iteration later, and the publishing thread reads its own column two rows
+//    back from the same buffers, so one __syncthreads per row suffices and no
+//    level history lives in registers.
+//  - The Jacobian diagonal is recomputed from u0 where it is needed.
+//  - Isotropic lattices (cx == cy, all BASELINE configs) evaluate the unit
+//    stencil and fold c into pre-scaled coefficients (SweepConsts::Es, gs, hls).
 //  - The first sweep of a step (U = (u0,u0,u0)) uses the closed form
 //    Phi_i = -h c_i f(u0), c_i = sum_j E[i][j].
-// HBM traffic per sweep is unchanged: 120 B/site (72 B/site for the first).
+//  - The iteration loop is unrolled by 3 so register-window slots are static.
+// HBM traffic per sweep: 120 B/site (72 B/site for the first sweep).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -31,40 +36,69 @@ namespace mb4cu {
 namespace {
 
 template <int M, int NT>
-struct Geom2 {
-    static_assert(M >= 0 && M <= 2, "march v2 supports Neumann depth 0..2");
-    static constexpr int TX = NT - 2 * M;  // output columns per band
-    static constexpr int ZW = NT + 2;      // columns per smem row (1-site pad each side)
-    static constexpr int P = 4;            // cp.async prefetch depth (rows)
-    static constexpr int S = P + 2;        // z ring rows (6: divisible by the unroll of 3)
+struct Geom3 {
+    static_assert(M >= 0 && M <= 2, "march v3 supports Neumann depth 0..2");
+    static constexpr int TX = NT - 2 * M;   // output columns per band
+    static constexpr int ZW = NT + 2;       // columns per smem row (1-site pad each side)
+    static constexpr int S = 6;             // z ring rows (divisible by the unroll of 3)
+    static constexpr int BACK = M == 2 ? 3 : 1;  // oldest z row still read: j - BACK
+    static constexpr int P = S - 1 - BACK;  // rows in flight
     static constexpr size_t zu0_bytes = sizeof(double2) * S * ZW;
     static constexpr size_t zv_bytes = ((sizeof(double) * S * ZW + 15) / 16) * 16;
     static constexpr size_t zU_bytes = sizeof(double2) * S * 3 * ZW;
     static constexpr size_t pub_bytes = sizeof(double2) * 2 * 3 * ZW;  // one level, 2 parities
-    static constexpr int NPUB = M;                                      // levels 0..M-1 publish
-    static constexpr size_t bytes = zu0_bytes + zv_bytes + zU_bytes + NPUB * pub_bytes;
+    static constexpr size_t bytes = zu0_bytes + zv_bytes + zU_bytes + M * pub_bytes;
+    static constexpr int MINB = 2;  // CTAs per SM (register / smem budget)
 };
 
-struct JD {  // Jacobian diagonal at a site plus (diag + V)
-    double alpha, beta, delta, dv;
+// Coefficient views: isotropic (unit stencil, pre-scaled constants) or general.
+template <bool ISO>
+struct Coef {
+    const SweepConsts& c;
+    __device__ __forceinline__ double E(int i, int j) const { return ISO ? c.Es[i][j] : c.E[i][j]; }
+    __device__ __forceinline__ double g() const { return ISO ? c.gs : c.gamma; }
+    __device__ __forceinline__ double hl(int k) const { return ISO ? c.hls[k] : c.hlam[k]; }
+    __device__ __forceinline__ double fs(int k) const { return ISO ? c.first_ss[k] : c.first_s[k]; }
+    __device__ __forceinline__ double fc(int k) const { return ISO ? c.first_cs[k] : c.first_c[k]; }
+    // stencil diagonal incl. potential
+    __device__ __forceinline__ double dv(double v) const { return ISO ? fma(v, c.inv_c, 4.0) : c.diag + v; }
+    // (K+V) x (general) or (K+V) x / c (isotropic)
+    __device__ __forceinline__ double2 kv(double d, double2 x, double2 l, double2 r, double2 dn,
+                                          double2 up) const {
+        double2 y;
+        if (ISO) {
+            y.x = fma(d, x.x, -((l.x + r.x) + (dn.x + up.x)));
+            y.y = fma(d, x.y, -((l.y + r.y) + (dn.y + up.y)));
+        } else {
+            y.x = fma(d, x.x, -(c.cx * (l.x + r.x) + c.cy * (dn.x + up.x)));
+            y.y = fma(d, x.y, -(c.cx * (l.y + r.y) + c.cy * (dn.y + up.y)));
+        }
+        return y;
+    }
+    // b = base + h lam_k J t, with a = kv(...) of t and the J diagonal of u0
+    __device__ __forceinline__ double2 horner(int k, double2 base, double2 t, double2 a, double2 u0) const {
+        const double pp = u0.x * u0.x, qq = u0.y * u0.y;
+        const double al = fma(3.0, pp, qq), be = 2.0 * u0.x * u0.y, de = fma(3.0, qq, pp);
+        const double nlx = fma(al, t.x, be * t.y);
+        const double nly = fma(be, t.x, de * t.y);
+        const double jx = fma(-g(), nly, a.y);
+        const double jy = fma(g(), nlx, -a.x);
+        return make_double2(fma(hl(k), jx, base.x), fma(hl(k), jy, base.y));
+    }
 };
 
-template <int M, int NT, bool FIRST>
-struct March2 {
-    using G = Geom2<M, NT>;
+template <int M, int NT, bool FIRST, bool ISO>
+struct March3 {
+    using G = Geom3<M, NT>;
     double2* zu0;  // [S][ZW]
     double* zv;    // [S][ZW]
     double2* zU;   // [S][3][ZW]
-    double2* pub;  // [NPUB][2][3][ZW]
+    double2* pub;  // [M][2][3][ZW]
 
-    // register windows, slot = (level-0 row + 2) mod 3 == (iteration j) mod 3
-    double2 zw[3][4];   // own-column z rows (slot of z row k: k mod 3)
-    double vw[3];       // own-column V
-    double2 pbw[3][3];  // phibar of level-0 rows
-    JD jdw[3];
-    double2 b1w[3][3];  // level-1 values (M == 2)
+    double2 zw[3][4];  // own-column z rows; slot of z row k = k mod 3
+    double vw[3];
 
-    __device__ March2(unsigned char* smem) {
+    __device__ March3(unsigned char* smem) {
         zu0 = reinterpret_cast<double2*>(smem);
         zv = reinterpret_cast<double*>(smem + G::zu0_bytes);
         zU = reinterpret_cast<double2*>(smem + G::zu0_bytes + G::zv_bytes);
@@ -76,17 +110,20 @@ struct March2 {
     }
 
     struct Seg {
-        int X0, Y0, R;
-        int xz0, yz0, nzrows;
+        int X0, Y0, R, yz0, nzrows;
+        int gxa, gxb;  // global columns of smem columns t and t + NT (t < 2)
     };
 
     __device__ __forceinline__ void issue_row(const StepArgs& a, const double2* const uin[3],
-                                              const Seg& s, int k) {
+                                              const Seg& s, int k, int slot) {
         if (k < s.nzrows) {
             const size_t rowoff = static_cast<size_t>(wrap_index(s.yz0 + k, a.ny)) * a.nx;
-            const int slot = k % G::S;
-            for (int col = threadIdx.x; col < G::ZW; col += NT) {
-                const size_t g = rowoff + wrap_index(s.xz0 + col, a.nx);
+            const int t = threadIdx.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && t >= 2) break;
+                const int col = t + h * NT;
+                const size_t g = rowoff + (h ? s.gxb : s.gxa);
                 cp_async16(&zu0[slot * G::ZW + col], a.u0 + g);
                 cp_async8(&zv[slot * G::ZW + col], a.V + g);
                 if (!FIRST) {
@@ -98,42 +135,45 @@ struct March2 {
         cp_async_commit();
     }
 
-    // One iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); zs = j mod S.
+    __device__ __forceinline__ static void track(unsigned long long& rmax, double2 r) {
+        const unsigned long long bx = abs_bits(r.x), by = abs_bits(r.y);
+        rmax = bx > rmax ? bx : rmax;
+        rmax = by > rmax ? by : rmax;
+    }
+
+    // Iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); h3 = 3 * ((j / 3) & 1).
     template <int PH>
-    __device__ __forceinline__ void body(const StepArgs& a, const SweepConsts& c,
+    __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf,
                                          const double2* const uin[3], double2* const uout[3],
-                                         const Seg& s, int j, unsigned long long& rmax,
+                                         const Seg& s, int j, int h3, unsigned long long& rmax,
                                          double acc[kObsFields]) {
         constexpr int S_NEW = PH;            // z row j      (own column, newly loaded)
         constexpr int S_CEN = (PH + 2) % 3;  // z row j - 1  (level-0 centre row)
         constexpr int S_DN = (PH + 1) % 3;   // z row j - 2
+        const SweepConsts& c = cf.c;
         const int t = threadIdx.x;
         const int cc = t + 1;
-        const int i = j - 2;                 // level-0 row (relative to Y0 - M)
+        const int i = j - 2;
+
+        // ring slots: row j - k lives in slot (j - k) mod 6 = (h3 + PH - k) mod 6
+        auto ring = [&](int k) {
+            int x = h3 + PH - k + 6;
+            x = x >= 6 ? x - 6 : x;
+            return x >= 6 ? x - 6 : x;
+        };
+        const int slot_new = ring(0);
+        const int slot_cen = ring(1);
 
         cp_async_wait<G::P - 1>();
         __syncthreads();
-        issue_row(a, uin, s, j + G::P);
+        issue_row(a, uin, s, j + G::P, ring(-G::P));
 
-        const int slot_new = j % G::S;
-        const int slot_cen = (j + G::S - 1) % G::S;
-
-        // final-level output coordinates (row i - M at level M)
-        const int yrel = i - 2 * M;          // output row offset from Y0
+        const int yrel = i - 2 * M;  // output row offset from Y0
         const int xout = s.X0 - M + t;
         const bool out_ok = yrel >= 0 && yrel < s.R && t >= M && t < NT - M && xout < a.nx;
-        double2 uold[3];
-        if (M == 2 && out_ok) {
-            const size_t g = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
-            if (FIRST) {
-                uold[0] = __ldcg(a.u0 + g);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) uold[q] = __ldcg(uin[q] + g);
-            }
-        }
+        const int par = j & 1, ppar = par ^ 1;
 
-        // ---- own column: new z row j into the window -------------------------
+        // ---- own column: new z row j --------------------------------------------
         zw[S_NEW][0] = zu0[slot_new * G::ZW + cc];
         vw[S_NEW] = zv[slot_new * G::ZW + cc];
         if (!FIRST) {
@@ -141,40 +181,51 @@ struct March2 {
             for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZW + cc];
         }
 
-        // ---- level 0 at row i: phibar (centre z row j-1) ------------------------
+        // own-column level history, read before this iteration overwrites it
+        double2 pb_m2[3];  // phibar row i-2 (M == 2)
+        double2 b1_m3[3];  // b1 row i-3   (M == 2)
+        if (M == 2) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                pb_m2[k] = pub_row(0, par, k)[cc];
+                b1_m3[k] = pub_row(1, par, k)[cc];
+            }
+        }
+
+        // ---- level 0 at row i ---------------------------------------------------
         const double v = vw[S_CEN];
+        const double d0 = cf.dv(v);
         const double2 u0c = zw[S_CEN][0];
         double2 pb[3];
         {
-            const double2 l0 = zu0[slot_cen * G::ZW + cc - 1], r0 = zu0[slot_cen * G::ZW + cc + 1];
-            const double2 w0 = kv_site(c, v, u0c, l0, r0, zw[S_DN][0], zw[S_NEW][0]);
+            const double2 w0 = cf.kv(d0, u0c, zu0[slot_cen * G::ZW + cc - 1], zu0[slot_cen * G::ZW + cc + 1],
+                                     zw[S_DN][0], zw[S_NEW][0]);
             if (FIRST) {
-                // f(u0) = -i((K+V)u0 - gamma |u0|^2 u0); phibar_k = first_s[k] * f
+                // f(u0)/scale = -i(w0 - g |u0|^2 u0); phibar_k = fs_k * f
                 const double n2 = fma(u0c.x, u0c.x, u0c.y * u0c.y);
-                const double gx = fma(-c.gamma * n2, u0c.x, w0.x);
-                const double gy = fma(-c.gamma * n2, u0c.y, w0.y);
+                const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
+                const double gy = fma(-cf.g() * n2, u0c.y, w0.y);
                 const double2 f = make_double2(gy, -gx);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) pb[k] = make_double2(c.first_s[k] * f.x, c.first_s[k] * f.y);
                 if (M == 0) {
-                    // Picard: U_i = u0 + h c_i f(u0)
                     if (out_ok) {
-                        const size_t g = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+                        const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
 #pragma unroll
                         for (int q = 0; q < 3; ++q) {
-                            const double2 r = make_double2(c.first_c[q] * f.x, c.first_c[q] * f.y);
-                            uout[q][g] = make_double2(u0c.x + r.x, u0c.y + r.y);
-                            const unsigned long long bx = abs_bits(r.x), by = abs_bits(r.y);
-                            rmax = bx > rmax ? bx : rmax;
-                            rmax = by > rmax ? by : rmax;
+                            const double2 r = make_double2(cf.fc(q) * f.x, cf.fc(q) * f.y);
+                            uout[q][gi] = make_double2(u0c.x + r.x, u0c.y + r.y);
+                            track(rmax, r);
                         }
                     }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) pb[k] = make_double2(cf.fs(k) * f.x, cf.fs(k) * f.y);
                 }
                 // energy monitor of u0 on owned sites (lattice.cpp:106-137)
                 if (i >= M && i < M + s.R && t >= M && t < NT - M && xout < a.nx) {
                     const double vn = v * n2;
-                    acc[0] += fma(u0c.x, w0.x, u0c.y * w0.y) - vn;
-                    acc[1] += fma(u0c.x, w0.y, -u0c.y * w0.x);
+                    const double sc = ISO ? c.cx : 1.0;
+                    acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
+                    acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
                     acc[2] += n2;
                     acc[3] += n2 * n2;
                     acc[4] += vn;
@@ -187,19 +238,49 @@ struct March2 {
                 for (int q = 1; q < 4; ++q) {
                     const double2* row = zU + (slot_cen * 3 + (q - 1)) * G::ZW;
                     z[q] = zw[S_CEN][q];
-                    w[q] = kv_site(c, v, z[q], row[cc - 1], row[cc + 1], zw[S_DN][q], zw[S_NEW][q]);
+                    w[q] = cf.kv(d0, z[q], row[cc - 1], row[cc + 1], zw[S_DN][q], zw[S_NEW][q]);
+                }
+                // cubic term at the 6 Gauss nodes of the collocation polynomial
+                double2 cub[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cub[k] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    double ur = c.L[q][0] * z[0].x, ui = c.L[q][0] * z[0].y;
+#pragma unroll
+                    for (int b = 1; b < 4; ++b) {
+                        ur = fma(c.L[q][b], z[b].x, ur);
+                        ui = fma(c.L[q][b], z[b].y, ui);
+                    }
+                    const double n2 = fma(ur, ur, ui * ui);
+                    const double gr = n2 * ur, gi = n2 * ui;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        cub[k].x = fma(c.WA[k][q], gr, cub[k].x);
+                        cub[k].y = fma(c.WA[k][q], gi, cub[k].y);
+                    }
                 }
                 double2 phi[3];
-                phi_site(c, z, w, phi);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    double kr = cf.E(k, 0) * w[0].x, ki = cf.E(k, 0) * w[0].y;
+#pragma unroll
+                    for (int b = 1; b < 4; ++b) {
+                        kr = fma(cf.E(k, b), w[b].x, kr);
+                        ki = fma(cf.E(k, b), w[b].y, ki);
+                    }
+                    const double rr = fma(-c.gamma, cub[k].y, ki);
+                    const double ri = fma(c.gamma, cub[k].x, -kr);
+                    phi[k].x = fma(-c.h, rr, z[k + 1].x - z[0].x);
+                    phi[k].y = fma(-c.h, ri, z[k + 1].y - z[0].y);
+                }
                 if (M == 0) {
                     if (out_ok) {
-                        const size_t g = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+                        const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
 #pragma unroll
                         for (int q = 0; q < 3; ++q) {
-                            uout[q][g] = make_double2(z[q + 1].x - phi[q].x, z[q + 1].y - phi[q].y);
-                            const unsigned long long bx = abs_bits(phi[q].x), by = abs_bits(phi[q].y);
-                            rmax = bx > rmax ? bx : rmax;
-                            rmax = by > rmax ? by : rmax;
+                            uout[q][gi] = make_double2(z[q + 1].x - phi[q].x, z[q + 1].y - phi[q].y);
+                            track(rmax, phi[q]);
                         }
                     }
                 } else {
@@ -209,134 +290,102 @@ struct March2 {
         }
         if (M == 0) return;
 
-        constexpr int R0 = PH;             // slot of level-0 row i   (== S_NEW)
-        constexpr int R1 = (PH + 2) % 3;   // row i - 1
-        constexpr int R2 = (PH + 1) % 3;   // row i - 2
-        const int par = j & 1;             // publish parity of this iteration
-        const int ppar = par ^ 1;          // parity published last iteration
-        {
-            const JD d = {fma(3.0, u0c.x * u0c.x, u0c.y * u0c.y), 2.0 * u0c.x * u0c.y,
-                          fma(3.0, u0c.y * u0c.y, u0c.x * u0c.x), c.diag + v};
-            jdw[R0] = d;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                pbw[R0][k] = pb[k];
-                pub_row(0, par, k)[cc] = pb[k];
-            }
-        }
-
-        // ---- level 1 at row i - 1 -------------------------------------------
+        // ---- level 1 at row i - 1 ----------------------------------------------
         double2 b1[3];
         {
-            const JD d = jdw[R1];
+            const double2 u0m = zw[S_DN][0];          // u0 of row i - 1 (z row j - 2)
+            const double dm = cf.dv(vw[S_DN]);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const double2* hrow = pub_row(0, ppar, k);
-                const double2 tc = pbw[R1][k];
-                const double2 tl = hrow[cc - 1], tr = hrow[cc + 1];
-                const double2 td = pbw[R2][k], tu = pbw[R0][k];
-                double2 ak;
-                ak.x = fma(d.dv, tc.x, -(c.cx * (tl.x + tr.x) + c.cy * (td.x + tu.x)));
-                ak.y = fma(d.dv, tc.y, -(c.cx * (tl.y + tr.y) + c.cy * (td.y + tu.y)));
-                const double nlx = fma(d.alpha, tc.x, d.beta * tc.y);
-                const double nly = fma(d.beta, tc.x, d.delta * tc.y);
-                const double jx = fma(-c.gamma, nly, ak.y);
-                const double jy = fma(c.gamma, nlx, -ak.x);
-                b1[k] = make_double2(fma(c.hlam[k], jx, tc.x), fma(c.hlam[k], jy, tc.y));
+                const double2* prow = pub_row(0, ppar, k);  // phibar row i - 1
+                const double2 tc = prow[cc];
+                const double2 td = M == 2 ? pb_m2[k] : pub_row(0, par, k)[cc];  // row i - 2
+                const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], td, pb[k]);
+                b1[k] = cf.horner(k, tc, tc, ak, u0m);
             }
         }
+        // publish phibar row i (after the own-column history reads above)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pub_row(0, par, k)[cc] = pb[k];
+
         if (M == 1) {
             if (out_ok) {
                 double2 rb[3], r[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b1[k].x, -b1[k].y);
                 from_eigen(c, rb, r);
-                const size_t g = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
-                // U_old of row i - 1 is z row j - 2 (window slot S_DN)
+                const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const double2 uo = FIRST ? zw[S_DN][0] : zw[S_DN][q + 1];
-                    uout[q][g] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
-                    const unsigned long long bx = abs_bits(r[q].x), by = abs_bits(r[q].y);
-                    rmax = bx > rmax ? bx : rmax;
-                    rmax = by > rmax ? by : rmax;
+                    uout[q][gi] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
+                    track(rmax, r[q]);
                 }
             }
             return;
         }
-        // M == 2: publish b1 (row i - 1), keep it in the window
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            b1w[R1][k] = b1[k];
-            pub_row(1, par, k)[cc] = b1[k];
-        }
 
-        // ---- level 2 at row i - 2 (final) ------------------------------------
+        // ---- level 2 at row i - 2 (final, M == 2) -------------------------------
         if (out_ok) {
-            const JD d = jdw[R2];
+            const int slot_m3 = ring(3);             // z row j - 3 == row i - 2
+            const double2 u0m = zu0[slot_m3 * G::ZW + cc];
+            const double dm = cf.dv(zv[slot_m3 * G::ZW + cc]);
             double2 b2[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const double2* hrow = pub_row(1, ppar, k);
-                // b1 rows: i-3 (slot R0, written 2 iterations ago), i-2 (R2), i-1 (R1)
-                const double2 tc = b1w[R2][k];
-                const double2 tl = hrow[cc - 1], tr = hrow[cc + 1];
-                const double2 td = b1w[R0][k], tu = b1w[R1][k];
-                double2 ak;
-                ak.x = fma(d.dv, tc.x, -(c.cx * (tl.x + tr.x) + c.cy * (td.x + tu.x)));
-                ak.y = fma(d.dv, tc.y, -(c.cx * (tl.y + tr.y) + c.cy * (td.y + tu.y)));
-                const double nlx = fma(d.alpha, tc.x, d.beta * tc.y);
-                const double nly = fma(d.beta, tc.x, d.delta * tc.y);
-                const double jx = fma(-c.gamma, nly, ak.y);
-                const double jy = fma(c.gamma, nlx, -ak.x);
-                const double2 p0 = pbw[R2][k];
-                b2[k] = make_double2(fma(c.hlam[k], jx, p0.x), fma(c.hlam[k], jy, p0.y));
+                const double2* prow = pub_row(1, ppar, k);  // b1 row i - 2
+                const double2 tc = prow[cc];
+                const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], b1_m3[k], b1[k]);
+                b2[k] = cf.horner(k, pb_m2[k], tc, ak, u0m);
             }
             double2 rb[3], r[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b2[k].x, -b2[k].y);
             from_eigen(c, rb, r);
-            const size_t g = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+            const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                const double2 uo = FIRST ? uold[0] : uold[q];
-                uout[q][g] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
-                const unsigned long long bx = abs_bits(r[q].x), by = abs_bits(r[q].y);
-                rmax = bx > rmax ? bx : rmax;
-                rmax = by > rmax ? by : rmax;
+                const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZW + cc];
+                uout[q][gi] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
+                track(rmax, r[q]);
             }
         }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pub_row(1, par, k)[cc] = b1[k];
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
                         double2* const uout[3], int band, int Y0, int R, unsigned long long& rmax,
                         double acc[kObsFields]) {
+        const Coef<ISO> cf{c};
         Seg s;
         s.X0 = band * G::TX;
         s.Y0 = Y0;
         s.R = R;
-        s.xz0 = s.X0 - M - 1;
         s.yz0 = Y0 - M - 1;
         s.nzrows = R + 2 * M + 2;
+        const int xz0 = s.X0 - M - 1;
+        s.gxa = wrap_index(xz0 + static_cast<int>(threadIdx.x), a.nx);
+        s.gxb = wrap_index(xz0 + static_cast<int>(threadIdx.x) + NT, a.nx);
 #pragma unroll
-        for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k);
-        // iterations j = 0 .. R + 2M + 1 (j = 0, 1 only fill the windows)
+        for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k, k);
         const int jend = R + 2 * M + 2;
         for (int j = 0; j < jend; j += 3) {
-            body<0>(a, c, uin, uout, s, j, rmax, acc);
-            body<1>(a, c, uin, uout, s, j + 1, rmax, acc);
-            body<2>(a, c, uin, uout, s, j + 2, rmax, acc);
+            const int h3 = ((j / 3) & 1) * 3;
+            body<0>(a, cf, uin, uout, s, j, h3, rmax, acc);
+            body<1>(a, cf, uin, uout, s, j + 1, h3, rmax, acc);
+            body<2>(a, cf, uin, uout, s, j + 2, h3, rmax, acc);
         }
         cp_async_wait<0>();
         __syncthreads();
     }
 };
 
-template <int M, int NT, bool FIRST>
-__device__ void sweep_all2(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
+template <int M, int NT, bool FIRST, bool ISO>
+__device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
                            unsigned long long& rmax, double acc[kObsFields]) {
-    March2<M, NT, FIRST> m(smem);
+    March3<M, NT, FIRST, ISO> m(smem);
     const long long G = gridDim.x;
     const long long b0 = a.total * blockIdx.x / G;
     const long long b1 = a.total * (blockIdx.x + 1) / G;
@@ -351,9 +400,9 @@ __device__ void sweep_all2(const StepArgs& a, const SweepConsts& c, unsigned cha
     }
 }
 
-template <int M, int NT>
-__global__ void __launch_bounds__(NT, 2)
-mb4_step2_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
+template <int M, int NT, bool ISO>
+__global__ void __launch_bounds__(NT, Geom3<M, NT>::MINB)
+mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -365,7 +414,7 @@ mb4_step2_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         unsigned long long rmax = 0ull;
         if (s == 0) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all2<M, NT, true>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, true, ISO>(a, c, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -385,7 +434,7 @@ mb4_step2_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         } else {
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            sweep_all2<M, NT, false>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, false, ISO>(a, c, smem, uin, uout, rmax, acc);
         }
         block_max_to(rmax, &a.rmax[s]);
         grid.sync();
@@ -412,16 +461,16 @@ mb4_step2_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     }
 }
 
-template <int M, int NT>
-struct Launcher2 {
+template <int M, int NT, bool ISO>
+struct Launcher3 {
     static int grid_size(int device) {
         static int cached[64] = {0};
         if (device >= 0 && device < 64 && cached[device]) return cached[device];
-        const size_t smem = Geom2<M, NT>::bytes;
-        cudaFuncSetAttribute(mb4_step2_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const size_t smem = Geom3<M, NT>::bytes;
+        cudaFuncSetAttribute(mb4_step3_kernel<M, NT, ISO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step2_kernel<M, NT>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<M, NT, ISO>, NT, smem);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
@@ -432,11 +481,11 @@ struct Launcher2 {
     static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
         const int grid = grid_size(device);
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
-        a.nbands = (a.nx + Geom2<M, NT>::TX - 1) / Geom2<M, NT>::TX;
+        a.nbands = (a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX;
         a.total = static_cast<long long>(a.nbands) * a.ny;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step2_kernel<M, NT>), dim3(grid),
-                                           dim3(NT), params, Geom2<M, NT>::bytes, s);
+        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<M, NT, ISO>),
+                                           dim3(grid), dim3(NT), params, Geom3<M, NT>::bytes, s);
     }
 };
 
@@ -459,21 +508,30 @@ cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const d
     a.max_iters = max_iters;
     a.eps = eps;
     a.want_obs = want_obs;
-    switch (m) {
-        case 0: return Launcher2<0, 128>::launch(a, c, device, s);
-        case 1: return Launcher2<1, 128>::launch(a, c, device, s);
-        case 2: return Launcher2<2, 128>::launch(a, c, device, s);
+    if (c.iso) {
+        switch (m) {
+            case 0: return Launcher3<0, 128, true>::launch(a, c, device, s);
+            case 1: return Launcher3<1, 128, true>::launch(a, c, device, s);
+            case 2: return Launcher3<2, 128, true>::launch(a, c, device, s);
+        }
+    } else {
+        switch (m) {
+            case 0: return Launcher3<0, 128, false>::launch(a, c, device, s);
+            case 1: return Launcher3<1, 128, false>::launch(a, c, device, s);
+            case 2: return Launcher3<2, 128, false>::launch(a, c, device, s);
+        }
     }
     return cudaErrorInvalidValue;
 }
 
 int march2_grid_size(int m, int device) {
+    int g = 0;
     switch (m) {
-        case 0: return Launcher2<0, 128>::grid_size(device);
-        case 1: return Launcher2<1, 128>::grid_size(device);
-        case 2: return Launcher2<2, 128>::grid_size(device);
+        case 0: g = Launcher3<0, 128, true>::grid_size(device); g = g > Launcher3<0, 128, false>::grid_size(device) ? g : Launcher3<0, 128, false>::grid_size(device); break;
+        case 1: g = Launcher3<1, 128, true>::grid_size(device); g = g > Launcher3<1, 128, false>::grid_size(device) ? g : Launcher3<1, 128, false>::grid_size(device); break;
+        case 2: g = Launcher3<2, 128, true>::grid_size(device); g = g > Launcher3<2, 128, false>::grid_size(device) ? g : Launcher3<2, 128, false>::grid_size(device); break;
     }
-    return 0;
+    return g;
 }
 
 }  // namespace mb4cu
