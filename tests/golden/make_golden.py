@@ -1,0 +1,103 @@
+#!/usr/bin/env python3
+"""Regenerate the golden fixtures in tests/golden/ (run in the build container).
+
+Sources (nothing here is hand-written data):
+  scheme_exact.json  -- the reference's own exact-rational generator
+                        (/root/reference/proj/tools/exact_scheme_tables.py, sympy),
+                        parsed from its stdout.
+  ref_*.npz          -- the reference library itself (oracle/_ref/libnls2d_ref.so,
+                        StepDriver(MB4) -> mb4_step, eps = 1e-14) on the BASELINE
+                        inputs produced by paper_2003_04345_b200.configs.
+
+usage: python tests/golden/make_golden.py
+"""
+import hashlib
+import json
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2003_04345_b200 import configs  # noqa: E402
+
+REF_TOOL = "/root/reference/proj/tools/exact_scheme_tables.py"
+
+
+def input_digest(V, psi):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(V).tobytes())
+    h.update(np.ascontiguousarray(psi).tobytes())
+    return h.hexdigest()
+
+
+def scheme_exact():
+    out = subprocess.run([sys.executable, REF_TOOL], capture_output=True, text=True, check=True).stdout
+
+    def nums(block):
+        return [float(x) for x in re.findall(r"-?\d+(?:\.\d+)?(?:e-?\d+)?", block)]
+
+    alpha = float(re.search(r"kAlpha1 = ([^;]+);", out).group(1))
+    e = nums(re.search(r"kE\[3\]\[4\] = \{(.*?)\};", out, re.S).group(1))
+    lam = nums(re.search(r"kEigenvalues\[3\] = \{(.*?)\};", out, re.S).group(1))
+    w_block = re.search(r"kW\[3\]\[4\]\[4\]\[4\] = \{(.*?)\n\};", out, re.S).group(1)
+    w = nums(w_block)
+    # strip the array-dimension digits picked up from the declaration (none inside block)
+    a_half = float(re.search(r"kAHalfHalf = ([^;]+);", out).group(1))
+    l3_half = float(re.search(r"kL3Half = ([^;]+);", out).group(1))
+    assert len(e) == 12 and len(lam) == 3 and len(w) == 192, (len(e), len(lam), len(w))
+    return {"source": "reference tools/exact_scheme_tables.py (sympy, exact rationals)",
+            "alpha1": alpha, "E": e, "eigenvalues": lam, "W": w, "A_half_half": a_half,
+            "l3_half": l3_half}
+
+
+def ref_case(name, nsteps, solver, keep_steps=(1, 10)):
+    cfg = configs.CONFIGS[name]
+    V, psi = configs.make_inputs(cfg)
+    u = psi.copy()
+    states = {}
+    obs_all = [None]
+    iters_all = []
+    done = 0
+    # step in chunks so intermediate states can be kept
+    marks = sorted(set(keep_steps) | {nsteps})
+    obs_series = []
+    for m in marks:
+        k = m - done
+        u, obs, iters, secs = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, u,
+                                        cfg.dt, k, eps=cfg.epsilon, solver=solver)
+        obs_series.append(obs if done == 0 else obs[1:])
+        iters_all.extend(iters.tolist())
+        done = m
+        if m in keep_steps:
+            states[m] = u.copy()
+    obs = np.concatenate(obs_series, axis=0)
+    out = {f"state_{k}": v for k, v in states.items()}
+    out.update(obs=obs, iters=np.array(iters_all, dtype=np.int32), input_sha256=input_digest(V, psi),
+               solver=solver, nsteps=nsteps)
+    return out
+
+
+def main():
+    os.makedirs(HERE, exist_ok=True)
+    with open(os.path.join(HERE, "scheme_exact.json"), "w") as f:
+        json.dump(scheme_exact(), f, indent=1)
+    # cfg1: direct solver (reference default), states after 1 and 10 steps, 10-step H series
+    np.savez_compressed(os.path.join(HERE, "ref_cfg1_10.npz"), **ref_case("cfg1", 10, "direct"))
+    # cfg1: full 1000-step energy record (GMRES path: equivalent to direct to ~1e-17)
+    full = ref_case("cfg1", 1000, "gmres", keep_steps=())
+    np.savez_compressed(os.path.join(HERE, "ref_cfg1_full.npz"), obs=full["obs"], iters=full["iters"],
+                        input_sha256=full["input_sha256"], solver="gmres", nsteps=1000)
+    # cfg2: 10 steps (GMRES path), state after 10 steps
+    np.savez_compressed(os.path.join(HERE, "ref_cfg2_10.npz"), **ref_case("cfg2", 10, "gmres", keep_steps=(10,)))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
