@@ -307,7 +307,7 @@ def run_ours(args, d: Dist):
                         f"{cfg.defect_frac:.0%} defects, {cfg.npackets} packet(s) sigma={cfg.sigma}, eps={cfg.epsilon}",
             "lattice": [cfg.nx, cfg.ny],
             "sites_per_gpu": n,
-            "neumann_terms": args.neumann if args.neumann >= 0 else 2,
+            "neumann_terms": args.neumann if args.neumann >= 0 else 1,
             "kernel": "tiled" if args.kernel == 1 else "default",
             "l2": "flushed between steps" if flush else "inputs larger than L2 (state+stages >= 3 GiB)",
             "parallelism": "replicas" if d.world > 1 else "single",

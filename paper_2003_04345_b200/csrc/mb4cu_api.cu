@@ -52,6 +52,10 @@ struct mb4cu_ctx {
 
 namespace {
 
+// Default Neumann depth m of the stage preconditioner (fastest measured on B200 at
+// the BASELINE sizes, profiles/).
+constexpr int kDefaultNeumann = 1;
+
 thread_local std::string g_create_error;
 
 int fail(mb4cu_ctx* ctx, int code, const std::string& what) {
@@ -262,7 +266,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         g_create_error = "NewtonConfig: negative halvings";
         return MB4CU_INVALID;
     }
-    const int m = p->neumann_terms < 0 ? 2 : p->neumann_terms;
+    const int m = p->neumann_terms < 0 ? kDefaultNeumann : p->neumann_terms;
     if (m > 3) {
         g_create_error = "mb4cu_create: neumann_terms must be in 0..3";
         return MB4CU_INVALID;
