@@ -1,0 +1,319 @@
+// C++ mirror of the reference's hot-path API (proj/include/nls2d), implemented
+// header-only on top of the C ABI in mb4cu.h (link with libmb4cu.so).
+//
+// Declarations follow the reference so existing callers compile unchanged:
+//   GridSpec / GridModel / rhs / observables      lattice.hpp:21-88
+//   Mb4Scheme                                     mb4_scheme.hpp:26-64
+//   NewtonConfig / StepStats / NonConvergenceError / eval_phi / mb4_step
+//                                                 mb4_integrator.hpp:17-110
+//   MethodId / StepDriver                         integrators.hpp:11-66
+// Differences (documented in INTEGRATION.md):
+//   - the kinetic operator is the periodic 5-point stencil (the custom-K ctor,
+//     lattice.hpp:54, is not offered);
+//   - WorkerPool / SolverKind / cached_order are accepted and ignored (no sparse
+//     factorization, no CPU threads on this path);
+//   - StepStats::newton_iters counts stage sweeps; solve_seconds is device time;
+//   - StepDriver supports MethodId::Mb4 only (other methods are out of scope).
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mb4cu.h"
+
+namespace nls2d {
+
+using Complex = std::complex<double>;
+using State = std::vector<Complex>;
+
+class NonConvergenceError : public std::runtime_error {
+public:
+    NonConvergenceError(const std::string& what, double residual)
+        : std::runtime_error(what), last_residual(residual) {}
+    double last_residual;
+    double at_time = -1.0;
+};
+
+class ComplexEigenvalueError : public std::runtime_error {
+public:
+    explicit ComplexEigenvalueError(const std::string& what) : std::runtime_error(what) {}
+};
+
+namespace detail {
+inline void throw_status(int rc, const std::string& text, double residual = 0.0) {
+    switch (rc) {
+        case MB4CU_OK: return;
+        case MB4CU_NONCONVERGED: throw NonConvergenceError(text, residual);
+        case MB4CU_INVALID:
+            if (text.rfind("eig3_real", 0) == 0) throw ComplexEigenvalueError(text);
+            throw std::invalid_argument(text);
+        default: throw std::runtime_error("mb4cu status " + std::to_string(rc) + ": " + text);
+    }
+}
+}  // namespace detail
+
+struct GridSpec {
+    int nx = 0, ny = 0;
+    double lx = 0.0, ly = 0.0;
+    GridSpec(int nx_, int ny_, double lx_, double ly_) : nx(nx_), ny(ny_), lx(lx_), ly(ly_) {
+        if (nx < 2 || ny < 2) throw std::invalid_argument("GridSpec: nx and ny must be >= 2");
+        if (!(lx > 0.0) || !(ly > 0.0))
+            throw std::invalid_argument("GridSpec: domain lengths must be positive");
+    }
+    double hx() const { return lx / nx; }
+    double hy() const { return ly / ny; }
+    int points() const { return nx * ny; }
+    int index(int i, int j) const { return j * nx + i; }
+};
+
+inline std::vector<double> build_delta_potential(const GridSpec& g, double v0) {
+    std::vector<double> v(g.points(), 0.0);
+    v[g.index(0, 0)] = v0;
+    return v;
+}
+
+inline State initial_condition(const GridSpec& g) {
+    State u(g.points());
+    for (int j = 0; j < g.ny; ++j)
+        for (int i = 0; i < g.nx; ++i)
+            u[g.index(i, j)] = Complex(1.0 + 2.0 * std::cos(i * g.hx()) + 2.0 * std::cos(j * g.hy()), 0.0);
+    return u;
+}
+
+struct NewtonConfig {
+    double epsilon = 1e-13;
+    int max_iters = 50;
+    int max_step_halvings = 4;
+    void validate() const {
+        if (!(epsilon > 0.0)) throw std::invalid_argument("NewtonConfig: epsilon must be > 0");
+        if (max_iters < 1) throw std::invalid_argument("NewtonConfig: max_iters must be >= 1");
+        if (max_step_halvings < 0) throw std::invalid_argument("NewtonConfig: negative halvings");
+    }
+};
+
+enum class SolverKind { Direct, Gmres };
+
+struct StepStats {
+    int newton_iters = 0;
+    int halvings = 0;
+    double solve_seconds = 0.0;
+};
+
+struct Observables {
+    double u_kinetic = 0.0, u_nonlinear = 0.0, u_external = 0.0, total_energy = 0.0,
+           probability = 0.0, participation = 0.0, raw_quartic = 0.0;
+};
+
+class WorkerPool {  // accepted for signature compatibility; the GPU path has no CPU workers
+public:
+    explicit WorkerPool(int workers = 1) : workers_(workers) {}
+    int workers() const { return workers_; }
+
+private:
+    int workers_;
+};
+
+class Mb4Scheme {
+public:
+    static constexpr double kAlpha1Bound = -300.0 * 0.7770503941;
+    explicit Mb4Scheme(double alpha1 = -300.0 * 19.0 / 8.0,
+                       std::array<double, 3> nodes = {1.0 / 3.0, 2.0 / 3.0, 1.0}) {
+        const int rc = mb4cu_scheme_init(alpha1, nodes[0], nodes[1], nodes[2], &s_);
+        detail::throw_status(rc, mb4cu_create_error());
+    }
+    double alpha1() const { return s_.alpha1; }
+    std::array<double, 4> nodes() const { return {s_.nodes[0], s_.nodes[1], s_.nodes[2], s_.nodes[3]}; }
+    double e_ext(int i, int j) const { return s_.E[i - 1][j]; }
+    double w(int i, int a, int b, int c) const { return s_.W[i - 1][a][b][c]; }
+    std::array<double, 3> eigenvalues() const { return {s_.lam[0], s_.lam[1], s_.lam[2]}; }
+    double t(int r, int c) const { return s_.T[r][c]; }
+    double t_inv(int r, int c) const { return s_.Tinv[r][c]; }
+    const mb4cu_scheme& raw() const { return s_; }
+
+private:
+    mb4cu_scheme s_{};
+};
+
+class GridModel;
+
+/// RAII device session: one mb4cu context, state resident in HBM.
+class DeviceSession {
+public:
+    DeviceSession(const GridModel& model, const Mb4Scheme& scheme, const NewtonConfig& cfg,
+                  int neumann_terms = -1, int device = 0, int kernel = 0);
+    ~DeviceSession() { mb4cu_destroy(ctx_); }
+    DeviceSession(const DeviceSession&) = delete;
+    DeviceSession& operator=(const DeviceSession&) = delete;
+
+    void set_state(const State& u) {
+        check(mb4cu_set_state(ctx_, reinterpret_cast<const double*>(u.data())));
+    }
+    State get_state() const {
+        State u(n_);
+        check(mb4cu_get_state(ctx_, reinterpret_cast<double*>(u.data())));
+        return u;
+    }
+    void step(double h, StepStats* stats = nullptr) {
+        mb4cu_stats st{};
+        const int rc = mb4cu_step(ctx_, h, &st);
+        if (stats) {
+            stats->newton_iters += st.newton_iters;
+            stats->halvings += st.halvings;
+            stats->solve_seconds += st.solve_seconds;
+        }
+        check(rc, st.last_residual);
+    }
+    /// nsteps device-resident steps; returns the (nsteps+1) x 7 energy record.
+    std::vector<Observables> run(double h, int nsteps, std::vector<int>* iters = nullptr) {
+        std::vector<Observables> rows(static_cast<size_t>(nsteps) + 1);
+        std::vector<int> it(static_cast<size_t>(nsteps));
+        mb4cu_stats st{};
+        static_assert(sizeof(Observables) == 7 * sizeof(double), "layout");
+        const int rc = mb4cu_run(ctx_, h, nsteps, reinterpret_cast<double*>(rows.data()), it.data(), &st);
+        check(rc, st.last_residual);
+        if (iters) *iters = it;
+        return rows;
+    }
+    Observables observables() const {
+        mb4cu_obs o{};
+        check(mb4cu_observables(ctx_, &o));
+        return {o.u_kinetic, o.u_nonlinear, o.u_external, o.total_energy, o.probability,
+                o.participation, o.raw_quartic};
+    }
+    mb4cu_ctx* handle() const { return ctx_; }
+
+    void check(int rc, double residual = 0.0) const {
+        if (rc != MB4CU_OK) detail::throw_status(rc, mb4cu_last_error(ctx_), residual);
+    }
+
+private:
+    mb4cu_ctx* ctx_ = nullptr;
+    int n_ = 0;
+};
+
+class GridModel {
+public:
+    GridModel(GridSpec grid, double gamma) : GridModel(grid, gamma, std::vector<double>(grid.points(), 0.0)) {}
+    GridModel(GridSpec grid, double gamma, std::vector<double> potential)
+        : grid_(grid), potential_(std::move(potential)), gamma_(gamma) {
+        if (static_cast<int>(potential_.size()) != grid_.points())
+            throw std::invalid_argument("GridModel: potential length mismatch");
+    }
+    const GridSpec& grid() const { return grid_; }
+    std::span<const double> potential() const { return potential_; }
+    double gamma() const { return gamma_; }
+    int points() const { return grid_.points(); }
+    double cx() const { return 1.0 / (grid_.hx() * grid_.hx()); }
+    double cy() const { return 1.0 / (grid_.hy() * grid_.hy()); }
+
+    /// y = (K + V) u, evaluated on the GPU
+    void apply_kv(std::span<const Complex> u, std::span<Complex> y) const {
+        DeviceSession s(*this, Mb4Scheme(), NewtonConfig{});
+        s.check(mb4cu_apply_kv(s.handle(), reinterpret_cast<const double*>(u.data()),
+                               reinterpret_cast<double*>(y.data())));
+    }
+
+private:
+    GridSpec grid_;
+    std::vector<double> potential_;
+    double gamma_;
+};
+
+inline DeviceSession::DeviceSession(const GridModel& model, const Mb4Scheme& scheme,
+                                    const NewtonConfig& cfg, int neumann_terms, int device,
+                                    int kernel) {
+    cfg.validate();
+    mb4cu_problem p{};
+    p.nx = model.grid().nx;
+    p.ny = model.grid().ny;
+    p.cx = model.cx();
+    p.cy = model.cy();
+    p.gamma = model.gamma();
+    p.V = model.potential().data();
+    p.epsilon = cfg.epsilon;
+    p.max_iters = cfg.max_iters;
+    p.max_step_halvings = cfg.max_step_halvings;
+    p.neumann_terms = neumann_terms;
+    p.device = device;
+    p.kernel = kernel;
+    const int rc = mb4cu_create(&p, &scheme.raw(), &ctx_);
+    if (rc != MB4CU_OK) detail::throw_status(rc, mb4cu_create_error());
+    n_ = model.points();
+}
+
+inline State rhs(const GridModel& model, const State& u) {
+    if (static_cast<int>(u.size()) != model.points()) throw std::invalid_argument("rhs: state length mismatch");
+    State y(u.size());
+    DeviceSession s(model, Mb4Scheme(), NewtonConfig{});
+    s.check(mb4cu_rhs(s.handle(), reinterpret_cast<const double*>(u.data()), reinterpret_cast<double*>(y.data())));
+    return y;
+}
+
+inline Observables observables(const GridModel& model, const State& u) {
+    if (static_cast<int>(u.size()) != model.points())
+        throw std::invalid_argument("observables: state length mismatch");
+    DeviceSession s(model, Mb4Scheme(), NewtonConfig{});
+    s.set_state(u);
+    return s.observables();
+}
+
+inline std::array<State, 3> eval_phi(const GridModel& model, const Mb4Scheme& scheme, const State& u0,
+                                     const std::array<State, 3>& stages, double h) {
+    std::array<State, 3> phi;
+    for (auto& p : phi) p.resize(u0.size());
+    DeviceSession s(model, scheme, NewtonConfig{});
+    auto d = [](const State& x) { return reinterpret_cast<const double*>(x.data()); };
+    auto m = [](State& x) { return reinterpret_cast<double*>(x.data()); };
+    s.check(mb4cu_eval_phi(s.handle(), d(u0), d(stages[0]), d(stages[1]), d(stages[2]), h, m(phi[0]),
+                           m(phi[1]), m(phi[2])));
+    return phi;
+}
+
+/// One MB4 step (mb4_integrator.hpp:103-110): host vectors in and out.
+inline State mb4_step(const GridModel& model, const Mb4Scheme& scheme, const State& u0, double h,
+                      const NewtonConfig& cfg, WorkerPool* = nullptr, StepStats* stats = nullptr,
+                      SolverKind = SolverKind::Direct, const std::vector<int>* = nullptr) {
+    cfg.validate();
+    if (!(h > 0.0)) throw std::invalid_argument("mb4_step: h must be positive");
+    DeviceSession s(model, scheme, cfg);
+    s.set_state(u0);
+    s.step(h, stats);
+    return s.get_state();
+}
+
+enum class MethodId { Rk4, Gauss2, Gauss4, Avf2, Avf4, Mb4 };
+
+/// integrators.hpp:46-66, MB4 branch.  Keeps one device session per driver.
+class StepDriver {
+public:
+    StepDriver(const GridModel& model, MethodId method, NewtonConfig cfg,
+               SolverKind = SolverKind::Direct, WorkerPool* = nullptr)
+        : cfg_(cfg) {
+        cfg_.validate();
+        if (method != MethodId::Mb4)
+            throw std::invalid_argument("StepDriver: only MethodId::Mb4 runs on the GPU path");
+        session_ = std::make_unique<DeviceSession>(model, scheme_, cfg_);
+    }
+    State advance(const State& u0, double h, StepStats* stats = nullptr) {
+        if (!(h > 0.0)) throw std::invalid_argument("mb4_step: h must be positive");
+        session_->set_state(u0);
+        session_->step(h, stats);
+        return session_->get_state();
+    }
+    const Mb4Scheme& scheme() const { return scheme_; }
+    DeviceSession& session() { return *session_; }
+
+private:
+    NewtonConfig cfg_;
+    Mb4Scheme scheme_;
+    std::unique_ptr<DeviceSession> session_;
+};
+
+}  // namespace nls2d
