@@ -80,6 +80,11 @@ typedef struct {
     int neumann_terms;        /* m in 0..3: preconditioner sum_{k<=m} (h lam J)^k; -1 = default */
     int device;               /* CUDA device ordinal                                    */
     int kernel;               /* 0 = default (fastest), 1 = tiled reference kernel      */
+    int ghost;                /* 0: one periodic domain.  > 0: this context is a sub-domain
+                                 of a decomposed lattice (multi-GPU): arrays carry `ghost`
+                                 halo layers (>= neumann_terms + 1) filled by the caller via
+                                 mb4cu_halo_pack / _unpack, and steps are driven sweep by
+                                 sweep (mb4cu_sweep / mb4cu_commit_step).                 */
 } mb4cu_problem;
 
 typedef struct {
@@ -125,6 +130,29 @@ int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out);
 /* Bind the context to an external CUDA stream (e.g. torch's current stream);
  * NULL restores the context's own stream. */
 int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
+
+/* ---- Sub-domain (multi-GPU) stepping, ghost > 0 ---------------------------------
+ * The caller owns the decomposition and the exchange (paper_2003_04345_b200/dist.py
+ * does it over torch.distributed / NCCL).  One MB4 step is:
+ *   exchange u0 halos;  for s = 0, 1, ...: (s > 0: exchange halos of stage set
+ *   (s-1) & 1);  mb4cu_sweep(ctx, h, s, &r, sums);  r = allreduce_max(r);
+ *   stop when r <= eps;  mb4cu_commit_step(ctx, s + 1).
+ * Fields: 0 = u0, 1 = V, 2 = stage set 0 (U1..U3), 3 = stage set 1.
+ * Sides: 0 = west (x low), 1 = east, 2 = south (y low), 3 = north.  Pack reads the
+ * ghost-wide strip of owned sites adjacent to the side; unpack writes the ghost strip
+ * on that side.  x sides cover the owned rows; y sides the full padded width, so an
+ * x exchange followed by a y exchange also fills the corners.  Counts are in doubles. */
+size_t mb4cu_halo_count(const mb4cu_ctx* ctx, int field, int side);
+int mb4cu_halo_pack(mb4cu_ctx* ctx, int field, int side, double* dev_buf);
+int mb4cu_halo_unpack(mb4cu_ctx* ctx, int field, int side, const double* dev_buf);
+/* One stage sweep (sweep index s; s == 0 starts from U = (u0,u0,u0) and also returns
+ * the local energy sums of u0: Re u^H K u, Im u^H K u, sum|u|^2, sum|u|^4, sum V|u|^2).
+ * *local_rmax = max over owned sites of the split-real update. */
+int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* local_sums5);
+/* Accept the iterate after `sweeps` sweeps as the step result (u0 <- U3). */
+int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
+/* Local energy sums of the resident state (ghosts of u0 must be current). */
+int mb4cu_observables_sums(mb4cu_ctx* ctx, double* local_sums5);
 
 /* ---- Lattice operators on caller-supplied host arrays (device-computed) -------
  * Used by the parity tests for the vector-field evaluator rows of SURVEY 8a. */

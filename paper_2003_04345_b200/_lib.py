@@ -53,6 +53,7 @@ class Problem(C.Structure):
         ("neumann_terms", I),
         ("device", I),
         ("kernel", I),
+        ("ghost", I),
     ]
 
 
@@ -137,6 +138,12 @@ def lib() -> C.CDLL:
         "mb4cu_profile_enable": (I, [P, I]),
         "mb4cu_profile_reset": (I, [P]),
         "mb4cu_profile_get": (I, [P, C.POINTER(Profile)]),
+        "mb4cu_halo_count": (C.c_size_t, [P, I, I]),
+        "mb4cu_halo_pack": (I, [P, I, I, P]),
+        "mb4cu_halo_unpack": (I, [P, I, I, P]),
+        "mb4cu_sweep": (I, [P, D, I, DP, DP]),
+        "mb4cu_commit_step": (I, [P, I]),
+        "mb4cu_observables_sums": (I, [P, DP]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -158,5 +165,6 @@ EXPORTED = [
     "mb4cu_get_state_device", "mb4cu_step", "mb4cu_run", "mb4cu_observables",
     "mb4cu_set_stream", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
     "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
-    "mb4cu_profile_reset", "mb4cu_profile_get",
+    "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",
+    "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_commit_step", "mb4cu_observables_sums",
 ]

@@ -1,0 +1,141 @@
+// Sub-domain (multi-GPU) support kernels: halo pack / unpack between padded
+// local arrays and contiguous exchange buffers, and the energy monitor on a
+// padded sub-domain.  The exchange itself (NCCL send/recv between the 4 torus
+// neighbours, x phase then y phase so corners propagate) is driven by the host
+// (paper_2003_04345_b200/dist.py); see DESIGN.md section 8.
+#include <cuda_runtime.h>
+
+#include "mb4cu_internal.hpp"
+
+namespace mb4cu {
+namespace {
+
+template <typename T>
+__global__ void halo_copy_kernel(T* const* arrays, int narr, int pitch, int ghost, int x0, int y0, int w,
+                                 int h, T* buf, bool pack) {
+    const size_t per = static_cast<size_t>(w) * h;
+    const size_t total = per * narr;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int a = static_cast<int>(e / per);
+        const size_t r = e - static_cast<size_t>(a) * per;
+        const int y = static_cast<int>(r / w), x = static_cast<int>(r - static_cast<size_t>(y) * w);
+        const size_t g = static_cast<size_t>(y0 + y + ghost) * pitch + (x0 + x + ghost);
+        if (pack)
+            buf[e] = arrays[a][g];
+        else
+            arrays[a][g] = buf[e];
+    }
+}
+
+struct Ptrs2 {
+    double2* p[3];
+};
+
+__global__ void halo_copy2_kernel(Ptrs2 arrays, int narr, int pitch, int ghost, int x0, int y0, int w, int h,
+                                  double2* buf, bool pack) {
+    const size_t per = static_cast<size_t>(w) * h;
+    const size_t total = per * narr;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int a = static_cast<int>(e / per);
+        const size_t r = e - static_cast<size_t>(a) * per;
+        const int y = static_cast<int>(r / w), x = static_cast<int>(r - static_cast<size_t>(y) * w);
+        const size_t g = static_cast<size_t>(y0 + y + ghost) * pitch + (x0 + x + ghost);
+        if (pack)
+            buf[e] = arrays.p[a][g];
+        else
+            arrays.p[a][g] = buf[e];
+    }
+}
+
+__global__ void halo_copy1_kernel(double* array, int pitch, int ghost, int x0, int y0, int w, int h,
+                                  double* buf, bool pack) {
+    const size_t total = static_cast<size_t>(w) * h;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(e / w), x = static_cast<int>(e - static_cast<size_t>(y) * w);
+        const size_t g = static_cast<size_t>(y0 + y + ghost) * pitch + (x0 + x + ghost);
+        if (pack)
+            buf[e] = array[g];
+        else
+            array[g] = buf[e];
+    }
+}
+
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(kThreads)
+observables_ghost_kernel(const ObsArgs a, int ghost, int pitch) {
+    double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const size_t n = static_cast<size_t>(a.nx) * a.ny;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(k / a.nx), i = static_cast<int>(k - static_cast<size_t>(j) * a.nx);
+        const size_t g = static_cast<size_t>(j + ghost) * pitch + (i + ghost);
+        const double2 u = a.u[g], l = a.u[g - 1], r = a.u[g + 1], d = a.u[g - pitch], up = a.u[g + pitch];
+        const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
+        const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
+        acc[0] += fma(u.x, kx, u.y * ky);
+        acc[1] += fma(u.x, ky, -u.y * kx);
+        const double n2 = fma(u.x, u.x, u.y * u.y);
+        acc[2] += n2;
+        acc[3] += n2 * n2;
+        acc[4] += a.V[g] * n2;
+    }
+    __shared__ double red[kObsFields][kThreads / 32];
+#pragma unroll
+    for (int f = 0; f < kObsFields; ++f) {
+        double v = acc[f];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kObsFields) {
+        double v = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
+        a.partial[blockIdx.x * kObsFields + threadIdx.x] = v;
+    }
+}
+
+__global__ void observables_ghost_finalize(const double* partial, int nblocks, double* out) {
+    if (threadIdx.x < kObsFields) {
+        double v = 0.0;
+        for (int b = 0; b < nblocks; ++b) v += partial[b * kObsFields + threadIdx.x];
+        out[threadIdx.x] = v;
+    }
+}
+
+int blocks_for(size_t n) {
+    const size_t b = (n + kThreads - 1) / kThreads;
+    return static_cast<int>(b < 148 * 8 ? (b ? b : 1) : 148 * 8);
+}
+
+}  // namespace
+
+cudaError_t launch_halo_copy2(double2* const* arrays, int narr, int pitch, int ghost, int x0, int y0,
+                              int w, int h, double2* buf, bool pack, cudaStream_t s) {
+    Ptrs2 p{};
+    for (int i = 0; i < narr && i < 3; ++i) p.p[i] = arrays[i];
+    halo_copy2_kernel<<<blocks_for(static_cast<size_t>(w) * h * narr), kThreads, 0, s>>>(
+        p, narr, pitch, ghost, x0, y0, w, h, buf, pack);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_copy1(double* array, int pitch, int ghost, int x0, int y0, int w, int h,
+                              double* buf, bool pack, cudaStream_t s) {
+    halo_copy1_kernel<<<blocks_for(static_cast<size_t>(w) * h), kThreads, 0, s>>>(array, pitch, ghost, x0, y0,
+                                                                                  w, h, buf, pack);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_observables_ghost(const ObsArgs& a, int ghost, int pitch, double* out5, cudaStream_t s) {
+    // a.partial must hold obs_blocks(nx, ny) * kObsFields doubles
+    const int nb = obs_blocks(a.nx, a.ny);
+    observables_ghost_kernel<<<nb, kThreads, 0, s>>>(a, ghost, pitch);
+    observables_ghost_finalize<<<1, 32, 0, s>>>(a.partial, nb, out5);
+    return cudaGetLastError();
+}
+
+}  // namespace mb4cu

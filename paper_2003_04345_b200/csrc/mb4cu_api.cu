@@ -25,6 +25,8 @@ struct mb4cu_ctx {
     size_t n = 0;
     double cx = 0, cy = 0, gamma = 0, eps = 0;
     int max_iters = 0, max_halvings = 0, m = 2, kernel = 0;
+    int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
+    size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
     mb4cu_scheme scheme{};
     double2* u0 = nullptr;
     double* V = nullptr;
@@ -127,7 +129,7 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
                                                 ctx->max_iters, ctx->eps, 1, c, ctx->device,
-                                                ctx->stream));
+                                                ctx->stream, 0, 0));
     } else {
         MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
@@ -284,6 +286,14 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->max_halvings = p->max_step_halvings;
     ctx->m = m;
     ctx->kernel = p->kernel;
+    ctx->ghost = p->ghost;
+    if (p->ghost < 0 || (p->ghost > 0 && (p->ghost < m + 1 || m > 2 || p->kernel != 0))) {
+        g_create_error = "mb4cu_create: sub-domain mode needs ghost >= neumann_terms + 1, m <= 2, kernel 0";
+        delete ctx;
+        return MB4CU_INVALID;
+    }
+    ctx->pitch = p->nx + 2 * p->ghost;
+    ctx->alloc_n = static_cast<size_t>(ctx->pitch) * (p->ny + 2 * p->ghost);
     ctx->scheme = *scheme;
 
     auto bail = [&](cudaError_t e, const char* where) {
@@ -297,9 +307,9 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if ((e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(e, "cudaStreamCreate");
     ctx->stream = ctx->own_stream;
-    const size_t sb = ctx->n * sizeof(double2);
+    const size_t sb = ctx->alloc_n * sizeof(double2);
     if ((e = cudaMalloc(&ctx->u0, sb)) != cudaSuccess) return bail(e, "cudaMalloc(u0)");
-    if ((e = cudaMalloc(&ctx->V, ctx->n * sizeof(double))) != cudaSuccess) return bail(e, "cudaMalloc(V)");
+    if ((e = cudaMalloc(&ctx->V, ctx->alloc_n * sizeof(double))) != cudaSuccess) return bail(e, "cudaMalloc(V)");
     for (int b = 0; b < 2; ++b)
         for (int i = 0; i < 3; ++i)
             if ((e = cudaMalloc(&ctx->U[b][i], sb)) != cudaSuccess) return bail(e, "cudaMalloc(U)");
@@ -327,7 +337,18 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     }
     if ((e = cudaEventCreate(&ctx->pev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&ctx->pev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
-    if ((e = cudaMemcpy(ctx->V, p->V, ctx->n * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
+    if (ctx->ghost > 0) {
+        for (auto& set : ctx->U)
+            for (auto* q : set)
+                if ((e = cudaMemset(q, 0, sb)) != cudaSuccess) return bail(e, "cudaMemset(U)");
+        if ((e = cudaMemset(ctx->V, 0, ctx->alloc_n * sizeof(double))) != cudaSuccess) return bail(e, "cudaMemset(V)");
+        e = cudaMemcpy2D(ctx->V + static_cast<size_t>(ctx->ghost) * ctx->pitch + ctx->ghost,
+                         sizeof(double) * ctx->pitch, p->V, sizeof(double) * ctx->nx, sizeof(double) * ctx->nx,
+                         ctx->ny, cudaMemcpyHostToDevice);
+    } else {
+        e = cudaMemcpy(ctx->V, p->V, ctx->n * sizeof(double), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess)
         return bail(e, "cudaMemcpy(V)");
     if ((e = cudaMemset(ctx->u0, 0, sb)) != cudaSuccess) return bail(e, "cudaMemset(u0)");
     *out = ctx;
@@ -369,37 +390,51 @@ int mb4cu_set_stream(mb4cu_ctx* ctx, void* s) {
     return MB4CU_OK;
 }
 
+// Copy between a contiguous nx*ny state and the (possibly padded) device u0.
+static cudaError_t copy_state(mb4cu_ctx* ctx, void* dst, const void* src, bool to_device, cudaMemcpyKind kind) {
+    if (ctx->ghost == 0) return cudaMemcpyAsync(dst, src, ctx->n * sizeof(double2), kind, ctx->stream);
+    const size_t off = static_cast<size_t>(ctx->ghost) * ctx->pitch + ctx->ghost;
+    const size_t row = sizeof(double2) * ctx->nx, dpitch = sizeof(double2) * ctx->pitch;
+    if (to_device)
+        return cudaMemcpy2DAsync(static_cast<double2*>(dst) + off, dpitch, src, row, row, ctx->ny, kind, ctx->stream);
+    return cudaMemcpy2DAsync(dst, row, static_cast<const double2*>(src) + off, dpitch, row, ctx->ny, kind, ctx->stream);
+}
+
 int mb4cu_set_state(mb4cu_ctx* ctx, const double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
-    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, u, ctx->n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyHostToDevice));
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->obs_cached = false;
     return MB4CU_OK;
 }
 
 int mb4cu_get_state(mb4cu_ctx* ctx, double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "get_state: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
-    MB4_CUDA(ctx, cudaMemcpyAsync(u, ctx->u0, ctx->n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, copy_state(ctx, u, ctx->u0, false, cudaMemcpyDeviceToHost));
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MB4CU_OK;
 }
 
 int mb4cu_set_state_device(mb4cu_ctx* ctx, const double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state_device: null argument");
-    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, u, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyDeviceToDevice));
+    ctx->obs_cached = false;
     return MB4CU_OK;
 }
 
 int mb4cu_get_state_device(mb4cu_ctx* ctx, double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "get_state_device: null argument");
-    MB4_CUDA(ctx, cudaMemcpyAsync(u, ctx->u0, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    MB4_CUDA(ctx, copy_state(ctx, u, ctx->u0, false, cudaMemcpyDeviceToDevice));
     return MB4CU_OK;
 }
 
 int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats) {
     if (!ctx) return MB4CU_INVALID;
     if (!(h > 0.0)) return fail(ctx, MB4CU_INVALID, "mb4_step: h must be positive");
+    if (ctx->ghost > 0)
+        return fail(ctx, MB4CU_INVALID, "mb4_step: sub-domain contexts step through mb4cu_sweep");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     MB4_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     double last = 0.0;
@@ -507,7 +542,10 @@ int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out) {
     a.u = ctx->u0;
     a.V = ctx->V;
     a.partial = ctx->d_obs_partial;
-    MB4_CUDA(ctx, mb4cu::launch_observables(a, ctx->d_obs5, ctx->stream));
+    if (ctx->ghost > 0)
+        MB4_CUDA(ctx, mb4cu::launch_observables_ghost(a, ctx->ghost, ctx->pitch, ctx->d_obs5, ctx->stream));
+    else
+        MB4_CUDA(ctx, mb4cu::launch_observables(a, ctx->d_obs5, ctx->stream));
     ctx->prof.other_launches += 2;
     MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_obs5, ctx->d_obs5, sizeof(double) * mb4cu::kObsFields,
                                   cudaMemcpyDeviceToHost, ctx->stream));
@@ -561,6 +599,105 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
         put_obs(obs_series + 7 * nsteps, o);
     }
     return MB4CU_OK;
+}
+
+// ---- sub-domain (multi-GPU) stepping ------------------------------------------
+
+namespace {
+
+// rectangle (x0, y0, w, h) of a halo side; pack == owned strip, unpack == ghost strip
+void halo_rect(const mb4cu_ctx* ctx, int side, bool pack, int* x0, int* y0, int* w, int* h) {
+    const int g = ctx->ghost, nx = ctx->nx, ny = ctx->ny;
+    switch (side) {
+        case 0: *x0 = pack ? 0 : -g; *y0 = 0; *w = g; *h = ny; break;            // west
+        case 1: *x0 = pack ? nx - g : nx; *y0 = 0; *w = g; *h = ny; break;       // east
+        case 2: *x0 = -g; *y0 = pack ? 0 : -g; *w = nx + 2 * g; *h = g; break;   // south
+        default: *x0 = -g; *y0 = pack ? ny - g : ny; *w = nx + 2 * g; *h = g; break;  // north
+    }
+}
+
+int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
+    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3 || !buf)
+        return fail(ctx, MB4CU_INVALID, "halo: bad context / field / side / buffer");
+    int x0, y0, w, h;
+    halo_rect(ctx, side, pack, &x0, &y0, &w, &h);
+    if (field == 1) {
+        MB4_CUDA(ctx, mb4cu::launch_halo_copy1(ctx->V, ctx->pitch, ctx->ghost, x0, y0, w, h, buf, pack, ctx->stream));
+    } else {
+        double2* arr[3];
+        int narr = 1;
+        if (field == 0) {
+            arr[0] = ctx->u0;
+        } else {
+            narr = 3;
+            for (int q = 0; q < 3; ++q) arr[q] = ctx->U[field - 2][q];
+        }
+        MB4_CUDA(ctx, mb4cu::launch_halo_copy2(arr, narr, ctx->pitch, ctx->ghost, x0, y0, w, h,
+                                               reinterpret_cast<double2*>(buf), pack, ctx->stream));
+    }
+    return MB4CU_OK;
+}
+
+}  // namespace
+
+size_t mb4cu_halo_count(const mb4cu_ctx* ctx, int field, int side) {
+    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3) return 0;
+    int x0, y0, w, h;
+    halo_rect(ctx, side, true, &x0, &y0, &w, &h);
+    const size_t sites = static_cast<size_t>(w) * h;
+    return field == 1 ? sites : (field == 0 ? 2 * sites : 6 * sites);
+}
+
+int mb4cu_halo_pack(mb4cu_ctx* ctx, int field, int side, double* dev_buf) {
+    return halo_xfer(ctx, field, side, dev_buf, true);
+}
+
+int mb4cu_halo_unpack(mb4cu_ctx* ctx, int field, int side, const double* dev_buf) {
+    return halo_xfer(ctx, field, side, const_cast<double*>(dev_buf), false);
+}
+
+int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* local_sums5) {
+    if (!ctx || ctx->ghost <= 0) return fail(ctx, MB4CU_INVALID, "sweep: sub-domain contexts only");
+    if (!(h > 0.0) || s < 0) return fail(ctx, MB4CU_INVALID, "sweep: h must be positive, s >= 0");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    const SweepConsts c = make_consts(ctx, h);
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
+    if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
+    MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
+                                            ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
+                                            ctx->device, ctx->stream, ctx->ghost, s));
+    if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(mb4cu::StepStatus), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->profiling) {
+        float ms = 0.f;
+        MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->pev0, ctx->pev1));
+        ctx->prof.kernel_ms += ms;
+        ctx->prof.launches += 1;
+        ctx->prof.sweeps += 1;
+        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : 120.0);
+    }
+    if (local_rmax) *local_rmax = ctx->h_status->rlast;
+    if (local_sums5 && s == 0)
+        for (int f = 0; f < mb4cu::kObsFields; ++f) local_sums5[f] = ctx->h_status->obs[f];
+    return MB4CU_OK;
+}
+
+int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps) {
+    if (!ctx || sweeps < 1) return fail(ctx, MB4CU_INVALID, "commit_step: sweeps must be >= 1");
+    std::swap(ctx->u0, ctx->U[(sweeps - 1) & 1][2]);
+    ctx->obs_cached = false;
+    return MB4CU_OK;
+}
+
+int mb4cu_observables_sums(mb4cu_ctx* ctx, double* sums) {
+    if (!ctx || !sums) return fail(ctx, MB4CU_INVALID, "observables_sums: null argument");
+    mb4cu_obs tmp{};
+    const int rc = mb4cu_observables(ctx, &tmp);
+    // the raw sums are left in h_obs5 by mb4cu_observables (also on health-check failure)
+    for (int f = 0; f < mb4cu::kObsFields; ++f) sums[f] = ctx->h_obs5[f];
+    return rc == MB4CU_NUMERIC ? MB4CU_OK : rc;
 }
 
 // ---- parity entry points on host arrays -------------------------------------

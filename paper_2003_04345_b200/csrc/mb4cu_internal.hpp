@@ -87,6 +87,13 @@ struct StepArgs {
     int max_iters;
     double eps;
     int want_obs;
+    // Sub-domain mode (multi-GPU): arrays are padded with `ghost` layers on every
+    // side (row pitch = nx + 2*ghost) that the host fills by halo exchange; the
+    // kernel then reads ghosts instead of wrapping periodically.  ghost == 0:
+    // single periodic domain, plain nx-pitched arrays.
+    int ghost;
+    int pitch;
+    int sweep0;                 // global index of the first sweep of this launch
 };
 
 // Launchers (sweep_tiled.cu, sweep_march.cu).
@@ -98,8 +105,19 @@ int march_grid_size(int m, int device);
 cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const double* V,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
-                               int want_obs, const SweepConsts& c, int device, cudaStream_t s);
+                               int want_obs, const SweepConsts& c, int device, cudaStream_t s,
+                               int ghost, int sweep0);
 int march2_grid_size(int m, int device);
+
+// Halo transfer between a padded sub-domain array set and a contiguous buffer
+// (halo.cu).  Rectangle [x0, x0+w) x [y0, y0+h) in local coordinates (ghosts
+// negative / >= n); buffer layout [array][row][col].
+cudaError_t launch_halo_copy2(double2* const* arrays, int narr, int pitch, int ghost, int x0, int y0,
+                              int w, int h, double2* buf, bool pack, cudaStream_t s);
+cudaError_t launch_halo_copy1(double* array, int pitch, int ghost, int x0, int y0, int w, int h,
+                              double* buf, bool pack, cudaStream_t s);
+// Energy sums of a padded sub-domain state (ghosts of u must be current).
+cudaError_t launch_observables_ghost(const ObsArgs& a, int ghost, int pitch, double* out5, cudaStream_t s);
 size_t tiled_smem_bytes(int m, bool first);
 cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
                                cudaStream_t s);

@@ -87,9 +87,14 @@ struct Coef {
     }
 };
 
-template <int M, int NT, bool FIRST, bool ISO>
+template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
 struct March3 {
     using G = Geom3<M, NT>;
+    // element offset of local site (x, y) (both may lie in the halo)
+    __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
+        if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
+        return static_cast<size_t>(y) * a.nx + x;
+    }
     double2* zu0;  // [S][ZW]
     double* zv;    // [S][ZW]
     double2* zU;   // [S][3][ZW]
@@ -117,7 +122,8 @@ struct March3 {
     __device__ __forceinline__ void issue_row(const StepArgs& a, const double2* const uin[3],
                                               const Seg& s, int k, int slot) {
         if (k < s.nzrows) {
-            const size_t rowoff = static_cast<size_t>(wrap_index(s.yz0 + k, a.ny)) * a.nx;
+            const size_t rowoff = GHOST ? static_cast<size_t>(s.yz0 + k + a.ghost) * a.pitch
+                                        : static_cast<size_t>(wrap_index(s.yz0 + k, a.ny)) * a.nx;
             const int t = threadIdx.x;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -208,7 +214,7 @@ struct March3 {
                 const double2 f = make_double2(gy, -gx);
                 if (M == 0) {
                     if (out_ok) {
-                        const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+                        const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                         for (int q = 0; q < 3; ++q) {
                             const double2 r = make_double2(cf.fc(q) * f.x, cf.fc(q) * f.y);
@@ -276,7 +282,7 @@ struct March3 {
                 }
                 if (M == 0) {
                     if (out_ok) {
-                        const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+                        const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                         for (int q = 0; q < 3; ++q) {
                             uout[q][gi] = make_double2(z[q + 1].x - phi[q].x, z[q + 1].y - phi[q].y);
@@ -314,7 +320,7 @@ struct March3 {
 #pragma unroll
                 for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b1[k].x, -b1[k].y);
                 from_eigen(c, rb, r);
-                const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+                const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const double2 uo = FIRST ? zw[S_DN][0] : zw[S_DN][q + 1];
@@ -342,7 +348,7 @@ struct March3 {
 #pragma unroll
             for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b2[k].x, -b2[k].y);
             from_eigen(c, rb, r);
-            const size_t gi = static_cast<size_t>(s.Y0 + yrel) * a.nx + xout;
+            const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZW + cc];
@@ -365,8 +371,17 @@ struct March3 {
         s.yz0 = Y0 - M - 1;
         s.nzrows = R + 2 * M + 2;
         const int xz0 = s.X0 - M - 1;
-        s.gxa = wrap_index(xz0 + static_cast<int>(threadIdx.x), a.nx);
-        s.gxb = wrap_index(xz0 + static_cast<int>(threadIdx.x) + NT, a.nx);
+        if (GHOST) {
+            // padded columns; columns past the right halo only feed masked outputs
+            const int last = a.pitch - 1;
+            const int ca = xz0 + static_cast<int>(threadIdx.x) + a.ghost;
+            const int cb = ca + NT;
+            s.gxa = ca < last ? ca : last;
+            s.gxb = cb < last ? cb : last;
+        } else {
+            s.gxa = wrap_index(xz0 + static_cast<int>(threadIdx.x), a.nx);
+            s.gxb = wrap_index(xz0 + static_cast<int>(threadIdx.x) + NT, a.nx);
+        }
 #pragma unroll
         for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k, k);
         const int jend = R + 2 * M + 2;
@@ -381,11 +396,11 @@ struct March3 {
     }
 };
 
-template <int M, int NT, bool FIRST, bool ISO>
+template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
                            unsigned long long& rmax, double acc[kObsFields]) {
-    March3<M, NT, FIRST, ISO> m(smem);
+    March3<M, NT, FIRST, ISO, GHOST> m(smem);
     const long long G = gridDim.x;
     const long long b0 = a.total * blockIdx.x / G;
     const long long b1 = a.total * (blockIdx.x + 1) / G;
@@ -400,7 +415,7 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
     }
 }
 
-template <int M, int NT, bool ISO>
+template <int M, int NT, bool ISO, bool GHOST>
 __global__ void __launch_bounds__(NT, Geom3<M, NT>::MINB)
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -409,12 +424,13 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     int sweeps = 0, set = 0, converged = 0;
     double rlast = 0.0;
     for (int s = 0; s < a.max_iters; ++s) {
-        const int out = s & 1;
+        const int sg = s + a.sweep0;  // global sweep index within the (sub)step
+        const int out = sg & 1;
         double2* const uout[3] = {a.U[out][0], a.U[out][1], a.U[out][2]};
         unsigned long long rmax = 0ull;
-        if (s == 0) {
+        if (sg == 0) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all3<M, NT, true, ISO>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, true, ISO, GHOST>(a, c, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -434,13 +450,13 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         } else {
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            sweep_all3<M, NT, false, ISO>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, false, ISO, GHOST>(a, c, smem, uin, uout, rmax, acc);
         }
         block_max_to(rmax, &a.rmax[s]);
         grid.sync();
         const unsigned long long bits = __ldcg(&a.rmax[s]);
         rlast = __longlong_as_double(static_cast<long long>(bits));
-        sweeps = s + 1;
+        sweeps = sg + 1;
         set = out;
         if (!isfinite(rlast)) break;
         if (rlast <= a.eps) {
@@ -461,16 +477,16 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     }
 }
 
-template <int M, int NT, bool ISO>
+template <int M, int NT, bool ISO, bool GHOST>
 struct Launcher3 {
     static int grid_size(int device) {
         static int cached[64] = {0};
         if (device >= 0 && device < 64 && cached[device]) return cached[device];
         const size_t smem = Geom3<M, NT>::bytes;
-        cudaFuncSetAttribute(mb4_step3_kernel<M, NT, ISO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(mb4_step3_kernel<M, NT, ISO, GHOST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<M, NT, ISO>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<M, NT, ISO, GHOST>, NT, smem);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
@@ -484,17 +500,37 @@ struct Launcher3 {
         a.nbands = (a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX;
         a.total = static_cast<long long>(a.nbands) * a.ny;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<M, NT, ISO>),
+        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<M, NT, ISO, GHOST>),
                                            dim3(grid), dim3(NT), params, Geom3<M, NT>::bytes, s);
     }
 };
+
+template <int M>
+cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
+    if (a.ghost > 0) {
+        return c.iso ? Launcher3<M, 128, true, true>::launch(a, c, device, s)
+                     : Launcher3<M, 128, false, true>::launch(a, c, device, s);
+    }
+    return c.iso ? Launcher3<M, 128, true, false>::launch(a, c, device, s)
+                 : Launcher3<M, 128, false, false>::launch(a, c, device, s);
+}
+
+template <int M>
+int grid3(int device) {
+    int g = 0;
+    const int v[4] = {Launcher3<M, 128, true, false>::grid_size(device), Launcher3<M, 128, false, false>::grid_size(device),
+                      Launcher3<M, 128, true, true>::grid_size(device), Launcher3<M, 128, false, true>::grid_size(device)};
+    for (int x : v) g = x > g ? x : g;
+    return g;
+}
 
 }  // namespace
 
 cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const double* V,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
-                               int want_obs, const SweepConsts& c, int device, cudaStream_t s) {
+                               int want_obs, const SweepConsts& c, int device, cudaStream_t s,
+                               int ghost, int sweep0) {
     StepArgs a{};
     a.nx = nx;
     a.ny = ny;
@@ -508,30 +544,24 @@ cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const d
     a.max_iters = max_iters;
     a.eps = eps;
     a.want_obs = want_obs;
-    if (c.iso) {
-        switch (m) {
-            case 0: return Launcher3<0, 128, true>::launch(a, c, device, s);
-            case 1: return Launcher3<1, 128, true>::launch(a, c, device, s);
-            case 2: return Launcher3<2, 128, true>::launch(a, c, device, s);
-        }
-    } else {
-        switch (m) {
-            case 0: return Launcher3<0, 128, false>::launch(a, c, device, s);
-            case 1: return Launcher3<1, 128, false>::launch(a, c, device, s);
-            case 2: return Launcher3<2, 128, false>::launch(a, c, device, s);
-        }
+    a.ghost = ghost;
+    a.pitch = nx + 2 * ghost;
+    a.sweep0 = sweep0;
+    switch (m) {
+        case 0: return dispatch3<0>(a, c, device, s);
+        case 1: return dispatch3<1>(a, c, device, s);
+        case 2: return dispatch3<2>(a, c, device, s);
     }
     return cudaErrorInvalidValue;
 }
 
 int march2_grid_size(int m, int device) {
-    int g = 0;
     switch (m) {
-        case 0: g = Launcher3<0, 128, true>::grid_size(device); g = g > Launcher3<0, 128, false>::grid_size(device) ? g : Launcher3<0, 128, false>::grid_size(device); break;
-        case 1: g = Launcher3<1, 128, true>::grid_size(device); g = g > Launcher3<1, 128, false>::grid_size(device) ? g : Launcher3<1, 128, false>::grid_size(device); break;
-        case 2: g = Launcher3<2, 128, true>::grid_size(device); g = g > Launcher3<2, 128, false>::grid_size(device) ? g : Launcher3<2, 128, false>::grid_size(device); break;
+        case 0: return grid3<0>(device);
+        case 1: return grid3<1>(device);
+        case 2: return grid3<2>(device);
     }
-    return g;
+    return 0;
 }
 
 }  // namespace mb4cu

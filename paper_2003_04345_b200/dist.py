@@ -1,0 +1,340 @@
+"""Multi-GPU MB4 stepping: 2-D block decomposition of the periodic lattice.
+
+One process per GPU (torchrun); torch.distributed is the plumbing (NCCL on the
+GPU, gloo for the CPU tests).  Each rank owns a block of the global lattice in
+a ghost-padded libmb4cu sub-domain context (mb4cu_problem.ghost = m + 1).  One
+MB4 step:
+
+    exchange u0 halos (x phase, then y phase: corners propagate)
+    for s = 0, 1, ...:
+        s > 0: exchange halos of the stage set written by sweep s-1
+        local sweep s  (one launch of the production kernel in sub-domain mode)
+        r = allreduce_max(local ||r||_inf);  s == 0: allreduce_sum(energy sums of u0)
+        r <= eps -> commit (u0 <- U3); non-finite / max_iters -> halve (reference policy)
+
+The convergence test, the halving policy (mb4_integrator.cpp:287-315) and the
+energy monitor (lattice.cpp:106-137) are the single-domain ones; only the
+reductions become collectives.  The exchange and reduction logic is covered on
+the CPU by tests/test_dist_gloo.py (world sizes 2 and 4) with a numpy backend.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+
+WEST, EAST, SOUTH, NORTH = 0, 1, 2, 3
+F_U0, F_V, F_SET0, F_SET1 = 0, 1, 2, 3
+
+
+def choose_grid(n: int, gnx: int, gny: int) -> Tuple[int, int]:
+    """px * py = n minimising the halo perimeter per rank (ties: squarest blocks)."""
+    best = None
+    for px in range(1, n + 1):
+        if n % px:
+            continue
+        py = n // px
+        if gnx % px or gny % py:
+            continue
+        lnx, lny = gnx // px, gny // py
+        cost = (lny if px > 1 else 0) + (lnx if py > 1 else 0)
+        key = (cost, abs(lnx - lny), px)
+        if best is None or key < best[0]:
+            best = (key, (px, py))
+    if best is None:
+        raise ValueError(f"cannot split {gnx}x{gny} over {n} ranks evenly")
+    return best[1]
+
+
+@dataclass
+class Decomposition:
+    gnx: int
+    gny: int
+    px: int
+    py: int
+    rank: int
+
+    def __post_init__(self):
+        if self.gnx % self.px or self.gny % self.py:
+            raise ValueError("lattice must split evenly over the process grid")
+        if not 0 <= self.rank < self.px * self.py:
+            raise ValueError("rank out of range")
+
+    @property
+    def rx(self) -> int:
+        return self.rank % self.px
+
+    @property
+    def ry(self) -> int:
+        return self.rank // self.px
+
+    @property
+    def lnx(self) -> int:
+        return self.gnx // self.px
+
+    @property
+    def lny(self) -> int:
+        return self.gny // self.py
+
+    @property
+    def x0(self) -> int:
+        return self.rx * self.lnx
+
+    @property
+    def y0(self) -> int:
+        return self.ry * self.lny
+
+    def rank_of(self, rx: int, ry: int) -> int:
+        return (ry % self.py) * self.px + (rx % self.px)
+
+    def neighbor(self, side: int) -> int:
+        dx, dy = {WEST: (-1, 0), EAST: (1, 0), SOUTH: (0, -1), NORTH: (0, 1)}[side]
+        return self.rank_of(self.rx + dx, self.ry + dy)
+
+    def block(self, global_array: np.ndarray) -> np.ndarray:
+        a = global_array.reshape(self.gny, self.gnx)
+        return np.ascontiguousarray(a[self.y0:self.y0 + self.lny, self.x0:self.x0 + self.lnx]).reshape(-1)
+
+
+class Comm:
+    """torch.distributed transport for halos and scalar reductions."""
+
+    def __init__(self, device: str):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.dist = dist
+        self.device = device
+
+    def allreduce_max(self, x: float) -> float:
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allreduce_sum(self, xs) -> np.ndarray:
+        t = self.torch.tensor(np.asarray(xs, dtype=np.float64), device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t.cpu().numpy()
+
+    def exchange(self, pairs):
+        """pairs: list of (send_tensor, dst, recv_tensor, src); all posted at once."""
+        ops = []
+        for send, dst, _, _ in pairs:
+            ops.append(self.dist.P2POp(self.dist.isend, send, dst))
+        for _, _, recv, src in pairs:
+            ops.append(self.dist.P2POp(self.dist.irecv, recv, src))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+class HaloExchange:
+    """Two-phase (x then y) halo exchange of one field on the process torus."""
+
+    def __init__(self, dec: Decomposition, backend, comm: Comm):
+        self.dec, self.b, self.comm = dec, backend, comm
+        self.bufs = {}
+
+    def _buf(self, key, n):
+        t = self.bufs.get(key)
+        if t is None or t.numel() != n:
+            t = self.b.new_buffer(n)
+            self.bufs[key] = t
+        return t
+
+    def exchange(self, field: int):
+        d = self.dec
+        for lo, hi, extent in ((WEST, EAST, d.px), (SOUTH, NORTH, d.py)):
+            n = self.b.halo_count(field, lo)
+            s_lo, s_hi = self._buf((field, lo, "s"), n), self._buf((field, hi, "s"), n)
+            self.b.pack(field, lo, s_lo)
+            self.b.pack(field, hi, s_hi)
+            if extent == 1:
+                # periodic wrap onto this rank: my low strip is my high ghost and vice versa
+                self.b.unpack(field, hi, s_lo)
+                self.b.unpack(field, lo, s_hi)
+                continue
+            r_hi, r_lo = self._buf((field, hi, "r"), n), self._buf((field, lo, "r"), n)
+            # order matters for extent == 2 (both neighbours are the same rank):
+            # sends [low strip -> low neighbour, high strip -> high neighbour],
+            # recvs [high ghost <- high neighbour's low strip, low ghost <- low neighbour's high strip]
+            self.b.sync()
+            self.comm.exchange([(s_lo, d.neighbor(lo), r_hi, d.neighbor(hi)),
+                                (s_hi, d.neighbor(hi), r_lo, d.neighbor(lo))])
+            self.b.unpack(field, hi, r_hi)
+            self.b.unpack(field, lo, r_lo)
+
+
+class NonConvergence(RuntimeError):
+    def __init__(self, what: str, residual: float):
+        super().__init__(what)
+        self.last_residual = residual
+
+
+class DistributedSession:
+    """MB4 stepping on one rank's block, collectives over torch.distributed."""
+
+    def __init__(self, dec: Decomposition, backend, comm: Comm, gamma: float, cx: float, cy: float,
+                 epsilon: float, max_iters: int = 50, max_step_halvings: int = 4):
+        self.dec, self.b, self.comm = dec, backend, comm
+        self.gamma, self.cx, self.cy = gamma, cx, cy
+        self.eps, self.max_iters, self.max_halvings = epsilon, max_iters, max_step_halvings
+        self.halo = HaloExchange(dec, backend, comm)
+        self.halo.exchange(F_V)
+        self.last_sweeps = 0
+        self.entry_sums: Optional[np.ndarray] = None
+
+    # -- energy monitor: global sums -> Observables (lattice.cpp:113-137)
+    def finish(self, sums) -> np.ndarray:
+        qr, qi, prob, quart, ext = sums
+        imag_scale = max(abs(qr), (4 * self.cx + 4 * self.cy) * prob)
+        if abs(qi) > 1e-12 * imag_scale and imag_scale > 0.0:
+            raise RuntimeError("observables: non-real kinetic quadratic form")
+        uk, ui = qr, -0.5 * self.gamma * quart
+        return np.array([uk, ui, ext, uk + ui + ext, prob, quart / (prob * prob) if prob > 0 else 0.0, quart])
+
+    def observables(self) -> np.ndarray:
+        self.halo.exchange(F_U0)
+        return self.finish(self.comm.allreduce_sum(self.b.obs_sums()))
+
+    def _substep(self, h: float) -> Tuple[int, float]:
+        self.halo.exchange(F_U0)
+        r = float("nan")
+        for s in range(self.max_iters):
+            if s > 0:
+                self.halo.exchange(F_SET0 + ((s - 1) & 1))
+            r_loc, sums = self.b.sweep(h, s)
+            r = self.comm.allreduce_max(r_loc)
+            if s == 0 and self.entry_sums is None:
+                self.entry_sums = self.comm.allreduce_sum(sums)
+            if not math.isfinite(r):
+                raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
+            if r <= self.eps:
+                self.b.commit(s + 1)
+                return s + 1, r
+        raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
+
+    def step(self, h: float) -> Tuple[int, int]:
+        """One MB4 step with the reference halving policy; returns (sweeps, halvings)."""
+        self.entry_sums = None
+        last = 0.0
+        for hv in range(self.max_halvings + 1):
+            sub = 1 << hv
+            if hv == 1:
+                self.b.save()
+            elif hv > 1:
+                self.b.restore()
+            try:
+                total = 0
+                for _ in range(sub):
+                    n, _ = self._substep(h / sub)
+                    total += n
+                self.last_sweeps = total
+                return total, hv
+            except NonConvergence as e:
+                last = e.last_residual
+        if self.max_halvings >= 1:
+            self.b.restore()
+        raise NonConvergence(f"mb4_step: no convergence after {self.max_halvings} step halvings", last)
+
+    def run(self, h: float, nsteps: int):
+        """nsteps steps; returns (obs[(nsteps+1),7], sweeps[nsteps]) with the fused energy record."""
+        rows, sweeps = [], []
+        for _ in range(nsteps):
+            n, _ = self.step(h)
+            sweeps.append(n)
+            rows.append(self.finish(self.entry_sums))
+        rows.append(self.observables())
+        return np.array(rows), np.array(sweeps)
+
+
+class CudaBackend:
+    """libmb4cu sub-domain context on this rank's GPU (ghost mode)."""
+
+    def __init__(self, dec: Decomposition, V_block: np.ndarray, scheme, gamma: float, cx: float, cy: float,
+                 epsilon: float, max_iters: int, neumann_terms: int, device: int):
+        import torch
+
+        self.torch = torch
+        self.L = _lib.lib()
+        self.dev = torch.device("cuda", device)
+        p = _lib.Problem()
+        p.nx, p.ny = dec.lnx, dec.lny
+        p.cx, p.cy, p.gamma = cx, cy, gamma
+        self._v = np.ascontiguousarray(V_block, dtype=np.float64)
+        p.V = _lib.dptr(self._v)
+        p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, 0
+        p.neumann_terms = neumann_terms
+        p.device = device
+        p.kernel = 0
+        p.ghost = neumann_terms + 1
+        self.ctx = C.c_void_p()
+        rc = self.L.mb4cu_create(C.byref(p), C.byref(scheme.raw), C.byref(self.ctx))
+        if rc:
+            raise RuntimeError(self.L.mb4cu_create_error().decode())
+        # run on torch's stream so NCCL and our kernels are ordered
+        self.L.mb4cu_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream))
+        self.n = dec.lnx * dec.lny
+        self._saved = None
+
+    def _chk(self, rc):
+        if rc:
+            raise RuntimeError(f"mb4cu status {rc}: {self.L.mb4cu_last_error(self.ctx).decode()}")
+
+    def new_buffer(self, n):
+        return self.torch.empty(n, dtype=self.torch.float64, device=self.dev)
+
+    def sync(self):
+        pass  # same stream as torch.distributed
+
+    def halo_count(self, field, side):
+        return int(self.L.mb4cu_halo_count(self.ctx, field, side))
+
+    def pack(self, field, side, buf):
+        self._chk(self.L.mb4cu_halo_pack(self.ctx, field, side, C.c_void_p(buf.data_ptr())))
+
+    def unpack(self, field, side, buf):
+        self._chk(self.L.mb4cu_halo_unpack(self.ctx, field, side, C.c_void_p(buf.data_ptr())))
+
+    def sweep(self, h, s):
+        r = C.c_double(0.0)
+        sums = np.zeros(5)
+        self._chk(self.L.mb4cu_sweep(self.ctx, h, s, C.byref(r), _lib.dptr(sums)))
+        return r.value, sums
+
+    def commit(self, sweeps):
+        self._chk(self.L.mb4cu_commit_step(self.ctx, sweeps))
+
+    def obs_sums(self):
+        sums = np.zeros(5)
+        self._chk(self.L.mb4cu_observables_sums(self.ctx, _lib.dptr(sums)))
+        return sums
+
+    def set_state(self, u_block):
+        u = np.ascontiguousarray(u_block, dtype=np.complex128)
+        self._chk(self.L.mb4cu_set_state(self.ctx, _lib.dptr(u)))
+
+    def get_state(self):
+        out = np.empty(self.n, dtype=np.complex128)
+        self._chk(self.L.mb4cu_get_state(self.ctx, _lib.dptr(out)))
+        return out
+
+    def save(self):
+        self._saved = self.get_state()
+
+    def restore(self):
+        self.set_state(self._saved)
+
+    def profile(self, on=True):
+        self.L.mb4cu_profile_enable(self.ctx, int(on))
+
+    def close(self):
+        if self.ctx:
+            self.L.mb4cu_destroy(self.ctx)
+            self.ctx = None

@@ -1,0 +1,198 @@
+"""Multi-process CPU tests (gloo) of the multi-GPU decomposition logic.
+
+dist.DistributedSession (halo exchange order incl. the 2-rank torus, corner
+propagation, convergence / energy collectives, commit, halving) is driven with a
+numpy backend that has exactly the libmb4cu sub-domain semantics (padded arrays,
+halo rectangles, sweep s / commit).  World sizes 2 and 4 must reproduce the
+single-domain matrix-free iteration bit for bit, and the reference oracle within
+the parity bound.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import sweep_model as SM
+from paper_2003_04345_b200 import configs, dist as D, nls2d
+
+
+class NumpyBackend:
+    """Numpy stand-in for dist.CudaBackend (test infrastructure)."""
+
+    def __init__(self, dec, V_block, scheme, gamma, cx, cy, m):
+        self.dec, self.scheme, self.gamma, self.cx, self.cy, self.m = dec, scheme, gamma, cx, cy, m
+        self.g = m + 1
+        self.P = (dec.lny + 2 * self.g, dec.lnx + 2 * self.g)
+        z = lambda: np.zeros(self.P, dtype=np.complex128)  # noqa: E731
+        self.u0 = z()
+        self.V = np.zeros(self.P)
+        self.U = [[z(), z(), z()], [z(), z(), z()]]
+        self._in(self.V)[:] = V_block.reshape(dec.lny, dec.lnx)
+        self._saved = None
+
+    def _in(self, a):
+        g = self.g
+        return a[g:g + self.dec.lny, g:g + self.dec.lnx]
+
+    def _rect(self, side, pack):
+        g, nx, ny = self.g, self.dec.lnx, self.dec.lny
+        if side == D.WEST:
+            x0, y0, w, h = (0 if pack else -g), 0, g, ny
+        elif side == D.EAST:
+            x0, y0, w, h = (nx - g if pack else nx), 0, g, ny
+        elif side == D.SOUTH:
+            x0, y0, w, h = -g, (0 if pack else -g), nx + 2 * g, g
+        else:
+            x0, y0, w, h = -g, (ny - g if pack else ny), nx + 2 * g, g
+        return (slice(y0 + g, y0 + g + h), slice(x0 + g, x0 + g + w))
+
+    def _arrays(self, field):
+        return [self.u0] if field == D.F_U0 else [self.V] if field == D.F_V else self.U[field - D.F_SET0]
+
+    def new_buffer(self, n):
+        return torch.zeros(n, dtype=torch.float64)
+
+    def sync(self):
+        pass
+
+    def halo_count(self, field, side):
+        sy, sx = self._rect(side, True)
+        sites = (sy.stop - sy.start) * (sx.stop - sx.start)
+        return sites * (1 if field == D.F_V else 2 * len(self._arrays(field)))
+
+    def pack(self, field, side, buf):
+        sl = self._rect(side, True)
+        parts = [a[sl].reshape(-1) for a in self._arrays(field)]
+        flat = np.concatenate(parts)
+        buf.numpy()[:] = flat.view(np.float64) if flat.dtype == np.complex128 else flat
+
+    def unpack(self, field, side, buf):
+        sl = self._rect(side, False)
+        arrs = self._arrays(field)
+        b = buf.numpy()
+        if field == D.F_V:
+            arrs[0][sl] = b.reshape(arrs[0][sl].shape)
+            return
+        c = b.view(np.complex128)
+        n = c.size // len(arrs)
+        for k, a in enumerate(arrs):
+            a[sl] = c[k * n:(k + 1) * n].reshape(a[sl].shape)
+
+    def sweep(self, h, s):
+        PY, PX = self.P
+        flat = lambda a: a.reshape(-1)  # noqa: E731
+        U_in = None if s == 0 else [flat(u) for u in self.U[(s - 1) & 1]]
+        Un, _ = SM.sweep(flat(self.u0), U_in, flat(self.V), self.gamma, h, self.scheme, self.m, PX, PY,
+                         self.cx, self.cy)
+        src = [self.u0] * 3 if s == 0 else self.U[(s - 1) & 1]
+        out = self.U[s & 1]
+        r = 0.0
+        for q in range(3):
+            new = Un[q].reshape(self.P)
+            d = self._in(new) - self._in(src[q])
+            r = max(r, np.abs(d.real).max(), np.abs(d.imag).max())
+            out[q][...] = new
+        sums = self.obs_sums() if s == 0 else np.zeros(5)
+        return r, sums
+
+    def commit(self, sweeps):
+        k = (sweeps - 1) & 1
+        self.u0, self.U[k][2] = self.U[k][2], self.u0
+
+    def obs_sums(self):
+        PY, PX = self.P
+        ku = SM.kv(self.u0.reshape(-1), np.zeros(PX * PY), PX, PY, self.cx, self.cy).reshape(self.P)
+        u, k, v = self._in(self.u0), self._in(ku), self._in(self.V)
+        q = np.sum(np.conj(u) * k)
+        n2 = np.abs(u) ** 2
+        return np.array([q.real, q.imag, n2.sum(), (n2 * n2).sum(), (v * n2).sum()])
+
+    def set_state(self, u_block):
+        self._in(self.u0)[:] = u_block.reshape(self.dec.lny, self.dec.lnx)
+
+    def get_state(self):
+        return self._in(self.u0).reshape(-1).copy()
+
+    def save(self):
+        self._saved = self.get_state()
+
+    def restore(self):
+        self.set_state(self._saved)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, px, py, m, nsteps, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = configs.CONFIGS["cfg1"]
+        V, psi = configs.make_inputs(cfg)
+        dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
+        scheme = nls2d.Mb4Scheme()
+        be = NumpyBackend(dec, dec.block(V), scheme, cfg.gamma, 1.0, 1.0, m)
+        be.set_state(dec.block(psi))
+        sess = D.DistributedSession(dec, be, D.Comm("cpu"), cfg.gamma, 1.0, 1.0, cfg.epsilon)
+        obs, sweeps = sess.run(cfg.dt, nsteps)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), u=be.get_state(), obs=obs, sweeps=sweeps)
+    finally:
+        dist.destroy_process_group()
+
+
+def _reference(m, nsteps):
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    scheme = nls2d.Mb4Scheme()
+    u, its = psi, []
+    for _ in range(nsteps):
+        u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon)
+        its.append(it)
+    return u, its
+
+
+@pytest.mark.parametrize("px,py,m", [(2, 1, 1), (1, 2, 2), (2, 2, 1)])
+def test_decomposed_run_reproduces_single_domain(tmp_path, px, py, m):
+    world, nsteps = px * py, 3
+    mp.spawn(_worker, args=(world, _free_port(), px, py, m, nsteps, str(tmp_path)), nprocs=world, join=True)
+    cfg = configs.CONFIGS["cfg1"]
+    u_ref, its_ref = _reference(m, nsteps)
+    glob = np.zeros((cfg.ny, cfg.nx), dtype=np.complex128)
+    obs0 = None
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        dec = D.Decomposition(cfg.nx, cfg.ny, px, py, r)
+        glob[dec.y0:dec.y0 + dec.lny, dec.x0:dec.x0 + dec.lnx] = d["u"].reshape(dec.lny, dec.lnx)
+        assert list(d["sweeps"]) == its_ref
+        if obs0 is None:
+            obs0 = d["obs"]
+        else:
+            assert np.array_equal(d["obs"], obs0)  # every rank sees the same global record
+    assert np.array_equal(glob.reshape(-1), u_ref)  # bit-identical to the single domain
+    H = obs0[:, 3]
+    assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
+    V, psi = configs.make_inputs(cfg)
+    from oracle import oracle as O
+
+    o = O.Oracle(cfg.nx, cfg.ny, cfg.gamma, V).observables(psi)
+    assert abs(obs0[0, 3] - o.total_energy) <= 1e-13 * abs(o.total_energy)
+
+
+def test_choose_grid_and_neighbours():
+    assert D.choose_grid(1, 8192, 8192) == (1, 1)
+    assert D.choose_grid(2, 16384, 8192) == (2, 1)
+    assert D.choose_grid(4, 16384, 16384) == (2, 2)
+    assert D.choose_grid(8, 16384, 32768) == (2, 4)
+    dec = D.Decomposition(16384, 32768, 2, 4, 5)
+    assert (dec.rx, dec.ry, dec.lnx, dec.lny) == (1, 2, 8192, 8192)
+    assert dec.neighbor(D.EAST) == 4 and dec.neighbor(D.WEST) == 4
+    assert dec.neighbor(D.NORTH) == 7 and dec.neighbor(D.SOUTH) == 3

@@ -1,0 +1,123 @@
+"""GPU tests of the sub-domain (multi-GPU) path on ONE GPU.
+
+Ranks are emulated by threads in one process, each owning a libmb4cu sub-domain
+context (ghost mode) on cuda:0; a host-side loopback transport stands in for
+NCCL.  Kernels never wait on each other (the exchange is host-mediated between
+launches), so this is safe on a single GPU.  The decomposed run must reproduce
+the single-domain production kernel bit for bit.
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2003_04345_b200 import configs, dist as D, nls2d
+
+pytestmark = pytest.mark.gpu
+
+
+class Hub:
+    def __init__(self, world):
+        self.world = world
+        self.bar = threading.Barrier(world)
+        self.vals = [None] * world
+        self.mail = {}
+        self.lock = threading.Lock()
+
+
+class LoopbackComm:
+    def __init__(self, hub, rank):
+        self.h, self.rank = hub, rank
+
+    def _gather(self, x):
+        self.h.vals[self.rank] = x
+        self.h.bar.wait()
+        v = list(self.h.vals)
+        self.h.bar.wait()
+        return v
+
+    def allreduce_max(self, x):
+        return float(max(self._gather(x)))
+
+    def allreduce_sum(self, xs):
+        vals = self._gather(np.asarray(xs, dtype=np.float64))
+        acc = np.zeros_like(vals[0])
+        for v in vals:  # fixed rank order
+            acc = acc + v
+        return acc
+
+    def exchange(self, pairs):
+        torch.cuda.synchronize()
+        counts = {}
+        with self.h.lock:
+            for send, dst, _, _ in pairs:
+                k = counts.get(dst, 0)
+                counts[dst] = k + 1
+                self.h.mail[(self.rank, dst, k)] = send.clone()
+        torch.cuda.synchronize()
+        self.h.bar.wait()
+        counts = {}
+        for _, _, recv, src in pairs:
+            k = counts.get(src, 0)
+            counts[src] = k + 1
+            recv.copy_(self.h.mail[(src, self.rank, k)])
+        torch.cuda.synchronize()
+        self.h.bar.wait()
+        with self.h.lock:
+            self.h.mail.clear()
+        self.h.bar.wait()
+
+
+def _run_decomposed(name, px, py, m, nsteps):
+    cfg = configs.CONFIGS[name]
+    V, psi = configs.make_inputs(cfg)
+    world = px * py
+    hub = Hub(world)
+    out = [None] * world
+    errs = []
+
+    def work(rank):
+        try:
+            torch.cuda.set_device(0)
+            dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
+            be = D.CudaBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon,
+                               cfg.max_iters, m, 0)
+            be.set_state(dec.block(psi))
+            sess = D.DistributedSession(dec, be, LoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon)
+            obs, sweeps = sess.run(cfg.dt, nsteps)
+            out[rank] = (dec, be.get_state(), obs, sweeps)
+            be.close()
+        except Exception as exc:  # surface thread failures
+            errs.append(exc)
+            hub.bar.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    glob = np.zeros((cfg.ny, cfg.nx), dtype=np.complex128)
+    for dec, u, _, _ in out:
+        glob[dec.y0:dec.y0 + dec.lny, dec.x0:dec.x0 + dec.lnx] = u.reshape(dec.lny, dec.lnx)
+    return glob.reshape(-1), out[0][2], out[0][3]
+
+
+@pytest.mark.parametrize("px,py,m", [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1), (2, 2, 2)])
+def test_subdomain_path_matches_single_domain(px, py, m):
+    name, nsteps = "cfg2", 4
+    cfg = configs.CONFIGS[name]
+    u_dec, obs_dec, sweeps_dec = _run_decomposed(name, px, py, m, nsteps)
+    V, psi = configs.make_inputs(cfg)
+    with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg),
+                       neumann_terms=m) as s:
+        s.set_state(psi)
+        obs, sweeps = s.run(cfg.dt, nsteps)
+        u = s.get_state()
+    assert list(sweeps_dec) == list(sweeps)
+    assert np.array_equal(u_dec, u), np.abs(u_dec - u).max()
+    H = obs_dec[:, 3]
+    assert np.abs(H - obs[:, 3]).max() <= 1e-14 * abs(H[0])
+    assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
