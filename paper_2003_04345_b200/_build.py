@@ -26,8 +26,9 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
-    target = os.path.join(HERE, "libmb4cu.so")
+def build_lib(force: bool = False, verbose: bool = False, defines=(), name: str = "libmb4cu.so") -> str:
+    """Build libmb4cu.so (or an experiment variant with extra -D defines)."""
+    target = os.path.join(HERE, name)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "mb4cu.h")]
     if not force and not _stale(target, deps):
         return target
@@ -35,8 +36,8 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
     procs = []
     for src in _sources():
-        obj = os.path.join(ROOT, "build", src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        obj = os.path.join(ROOT, "build", name + "." + src + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmb4cu.so")
+LIB_PATH = os.environ.get("MB4CU_LIB") or os.path.join(HERE, "libmb4cu.so")
 
 MB4CU_OK = 0
 MB4CU_INVALID = 1

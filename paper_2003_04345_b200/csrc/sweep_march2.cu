@@ -30,6 +30,13 @@
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
 
+#ifndef MB4_CONSTS_IN_SMEM
+#define MB4_CONSTS_IN_SMEM 1
+#endif
+#ifndef MB4_MINB_M1
+#define MB4_MINB_M1 2
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace mb4cu {
@@ -48,7 +55,8 @@ struct Geom3 {
     static constexpr size_t zU_bytes = sizeof(double2) * S * 3 * ZW;
     static constexpr size_t pub_bytes = sizeof(double2) * 2 * 3 * ZW;  // one level, 2 parities
     static constexpr size_t bytes = zu0_bytes + zv_bytes + zU_bytes + M * pub_bytes;
-    static constexpr int MINB = 2;  // CTAs per SM (register / smem budget)
+    // CTAs per SM: M <= 1 fits 3 (<= 168 registers, ~70 KB smem), M = 2 fits 2
+    static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
 };
 
 // Coefficient views: isotropic (unit stencil, pre-scaled constants) or general.
@@ -116,14 +124,25 @@ struct March3 {
 
     struct Seg {
         int X0, Y0, R, yz0, nzrows;
-        int gxa, gxb;  // global columns of smem columns t and t + NT (t < 2)
+        int gxa, gxb;    // global columns of smem columns t and t + NT (t < 2)
+        int next_row;    // global (periodic) row of the next z row to issue
+        size_t next_off; // its element offset
     };
 
+    // Issue z row k (rows are issued in order, so the row offset advances by one
+    // pitch per call and wraps periodically without a division).
     __device__ __forceinline__ void issue_row(const StepArgs& a, const double2* const uin[3],
-                                              const Seg& s, int k, int slot) {
+                                              Seg& s, int k, int slot) {
         if (k < s.nzrows) {
-            const size_t rowoff = GHOST ? static_cast<size_t>(s.yz0 + k + a.ghost) * a.pitch
-                                        : static_cast<size_t>(wrap_index(s.yz0 + k, a.ny)) * a.nx;
+            const size_t rowoff = s.next_off;
+            if (GHOST) {
+                s.next_off += a.pitch;
+            } else if (++s.next_row == a.ny) {
+                s.next_row = 0;
+                s.next_off = 0;
+            } else {
+                s.next_off += a.nx;
+            }
             const int t = threadIdx.x;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -141,17 +160,21 @@ struct March3 {
         cp_async_commit();
     }
 
-    __device__ __forceinline__ static void track(unsigned long long& rmax, double2 r) {
-        const unsigned long long bx = abs_bits(r.x), by = abs_bits(r.y);
-        rmax = bx > rmax ? bx : rmax;
-        rmax = by > rmax ? by : rmax;
+    // ||r||_inf on the high 32 bits of |r| (sign cleared): monotone, NaN/Inf above
+    // every finite value.  The block result is widened to the largest double with
+    // that high word, an upper bound within a factor 1 + 2^-20 of the true max, so
+    // the convergence test can only be stricter than the reference's.
+    __device__ __forceinline__ static void track(unsigned& rmax, double2 r) {
+        const unsigned hx = static_cast<unsigned>(__double2hiint(r.x)) & 0x7FFFFFFFu;
+        const unsigned hy = static_cast<unsigned>(__double2hiint(r.y)) & 0x7FFFFFFFu;
+        rmax = max(rmax, max(hx, hy));
     }
 
     // Iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); h3 = 3 * ((j / 3) & 1).
     template <int PH>
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf,
                                          const double2* const uin[3], double2* const uout[3],
-                                         const Seg& s, int j, int h3, unsigned long long& rmax,
+                                         Seg& s, int j, int h3, unsigned& rmax,
                                          double acc[kObsFields]) {
         constexpr int S_NEW = PH;            // z row j      (own column, newly loaded)
         constexpr int S_CEN = (PH + 2) % 3;  // z row j - 1  (level-0 centre row)
@@ -316,16 +339,15 @@ struct March3 {
 
         if (M == 1) {
             if (out_ok) {
-                double2 rb[3], r[3];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b1[k].x, -b1[k].y);
-                from_eigen(c, rb, r);
+                // r = T rbar = -T b1
+                double2 tb[3];
+                from_eigen(c, b1, tb);
                 const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const double2 uo = FIRST ? zw[S_DN][0] : zw[S_DN][q + 1];
-                    uout[q][gi] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
-                    track(rmax, r[q]);
+                    uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
+                    track(rmax, tb[q]);
                 }
             }
             return;
@@ -344,16 +366,14 @@ struct March3 {
                 const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], b1_m3[k], b1[k]);
                 b2[k] = cf.horner(k, pb_m2[k], tc, ak, u0m);
             }
-            double2 rb[3], r[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) rb[k] = make_double2(-b2[k].x, -b2[k].y);
-            from_eigen(c, rb, r);
+            double2 tb[3];
+            from_eigen(c, b2, tb);  // r = -T b2
             const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZW + cc];
-                uout[q][gi] = make_double2(uo.x + r[q].x, uo.y + r[q].y);
-                track(rmax, r[q]);
+                uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
+                track(rmax, tb[q]);
             }
         }
 #pragma unroll
@@ -361,7 +381,7 @@ struct March3 {
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
-                        double2* const uout[3], int band, int Y0, int R, unsigned long long& rmax,
+                        double2* const uout[3], int band, int Y0, int R, unsigned& rmax,
                         double acc[kObsFields]) {
         const Coef<ISO> cf{c};
         Seg s;
@@ -370,6 +390,12 @@ struct March3 {
         s.R = R;
         s.yz0 = Y0 - M - 1;
         s.nzrows = R + 2 * M + 2;
+        if (GHOST) {
+            s.next_off = static_cast<size_t>(s.yz0 + a.ghost) * a.pitch;
+        } else {
+            s.next_row = wrap_index(s.yz0, a.ny);
+            s.next_off = static_cast<size_t>(s.next_row) * a.nx;
+        }
         const int xz0 = s.X0 - M - 1;
         if (GHOST) {
             // padded columns; columns past the right halo only feed masked outputs
@@ -399,7 +425,7 @@ struct March3 {
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
-                           unsigned long long& rmax, double acc[kObsFields]) {
+                           unsigned& rmax, double acc[kObsFields]) {
     March3<M, NT, FIRST, ISO, GHOST> m(smem);
     const long long G = gridDim.x;
     const long long b0 = a.total * blockIdx.x / G;
@@ -421,16 +447,32 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#if MB4_CONSTS_IN_SMEM
+    // M = 2: scheme / step constants as a shared-memory broadcast table (LDS)
+    // instead of the constant bank (LDCU + uniform-register shuffling), which
+    // relieves the register pressure of the two-level kernel (measured: +2 %);
+    // for M <= 1 the constant bank is faster (measured: +18 %).
+    __shared__ __align__(16) SweepConsts csm;
+    if (M == 2) {
+        const double* src = reinterpret_cast<const double*>(&c);
+        double* dst = reinterpret_cast<double*>(&csm);
+        for (int q = threadIdx.x; q < static_cast<int>(sizeof(SweepConsts) / sizeof(double)); q += NT) dst[q] = src[q];
+        __syncthreads();
+    }
+    const SweepConsts& cc = M == 2 ? csm : c;
+#else
+    const SweepConsts& cc = c;
+#endif
     int sweeps = 0, set = 0, converged = 0;
     double rlast = 0.0;
     for (int s = 0; s < a.max_iters; ++s) {
         const int sg = s + a.sweep0;  // global sweep index within the (sub)step
         const int out = sg & 1;
         double2* const uout[3] = {a.U[out][0], a.U[out][1], a.U[out][2]};
-        unsigned long long rmax = 0ull;
+        unsigned rmax = 0u;
         if (sg == 0) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all3<M, NT, true, ISO, GHOST>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, true, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -450,9 +492,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         } else {
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            sweep_all3<M, NT, false, ISO, GHOST>(a, c, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, false, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
         }
-        block_max_to(rmax, &a.rmax[s]);
+        block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[s]);
         grid.sync();
         const unsigned long long bits = __ldcg(&a.rmax[s]);
         rlast = __longlong_as_double(static_cast<long long>(bits));

@@ -1,0 +1,9 @@
+#!/bin/bash
+# usage: tools/variants.sh "<bench args>" lib1.so lib2.so ...  (run on the GPU box)
+ARGS="$1"; shift
+for lib in "$@"; do
+  MB4CU_LIB=$PWD/paper_2003_04345_b200/$lib python bench.py $ARGS --no-cpu-baseline --no-e2e 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read())
+print('$lib', d['config']['workload'][:5], 'm=%s'%d['config']['neumann_terms'], '%.3e'%d['value'], d['sweeps_per_step'], 'frac=%.3f'%d['roofline']['frac'], 'ms/launch=%.3f'%d['roofline']['kernel_ms_per_launch'], d['clocks'])"
+done
