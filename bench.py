@@ -164,6 +164,16 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- helpers
 
 
+def measured_traffic(cfg_name: str, m: int):
+    """DRAM bytes per step-kernel launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(f"{cfg_name}_m{m}")
+        return None if t is None else float(t["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -342,7 +352,8 @@ def run_ours(args, d: Dist):
             "peak": peak,
             "unit": "GB/s",
             "frac": achieved / peak,
-            "traffic": None,
+            "traffic": measured_traffic(cfg.name, args.neumann if args.neumann >= 0 else 1),
+            "traffic_source": "ncu --set full, dram__bytes_read+write per launch (profiles/traffic.json)",
             "peak_kind": peak_kind,
             "kernel": "stage sweep",
             "alg_bytes_per_step": step_alg_bytes,
