@@ -85,6 +85,9 @@ typedef struct {
                                  halo layers (>= neumann_terms + 1) filled by the caller via
                                  mb4cu_halo_pack / _unpack, and steps are driven sweep by
                                  sweep (mb4cu_sweep / mb4cu_commit_step).                 */
+    int neumann_first;        /* Neumann depth of the FIRST sweep of a step (its Phi is the
+                                 cheap closed form); -1 = default (2).  Must equal
+                                 neumann_terms or be 2.                                    */
 } mb4cu_problem;
 
 typedef struct {

@@ -241,6 +241,8 @@ inline DeviceSession::DeviceSession(const GridModel& model, const Mb4Scheme& sch
     p.max_iters = cfg.max_iters;
     p.max_step_halvings = cfg.max_step_halvings;
     p.neumann_terms = neumann_terms;
+    p.neumann_first = -1;
+    p.ghost = 0;
     p.device = device;
     p.kernel = kernel;
     const int rc = mb4cu_create(&p, &scheme.raw(), &ctx_);

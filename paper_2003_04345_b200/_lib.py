@@ -54,6 +54,7 @@ class Problem(C.Structure):
         ("device", I),
         ("kernel", I),
         ("ghost", I),
+        ("neumann_first", I),
     ]
 
 

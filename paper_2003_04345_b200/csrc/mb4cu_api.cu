@@ -24,7 +24,7 @@ struct mb4cu_ctx {
     int nx = 0, ny = 0;
     size_t n = 0;
     double cx = 0, cy = 0, gamma = 0, eps = 0;
-    int max_iters = 0, max_halvings = 0, m = 2, kernel = 0;
+    int max_iters = 0, max_halvings = 0, m = 2, mf = 2, kernel = 0;
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
     mb4cu_scheme scheme{};
@@ -125,8 +125,8 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * ctx->max_iters,
                                   ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
-    if (ctx->kernel == 0 && ctx->m <= 2) {
-        MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
+    if (ctx->kernel == 0 && mb4cu::march2_supported(ctx->mf, ctx->m)) {
+        MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
                                                 ctx->max_iters, ctx->eps, 1, c, ctx->device,
                                                 ctx->stream, 0, 0));
@@ -188,7 +188,7 @@ int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         a.rmax = ctx->d_rmax;
         MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
         if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
-        MB4_CUDA(ctx, mb4cu::launch_sweep_tiled(ctx->m, cur < 0, a, c, ctx->stream));
+        MB4_CUDA(ctx, mb4cu::launch_sweep_tiled(cur < 0 ? ctx->mf : ctx->m, cur < 0, a, c, ctx->stream));
         if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
         MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long),
                                       cudaMemcpyDeviceToHost, ctx->stream));
@@ -202,14 +202,18 @@ int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
             ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (cur < 0 ? 72.0 : 120.0);
         }
         *sweeps = it;
-        const double r = decode_bits(*ctx->h_rmax);
+        unsigned long long bits = *ctx->h_rmax;
+        // same widened high-word residual as the production kernel
+        if (bits >> 32) bits = (bits & 0xFFFFFFFF00000000ull) | 0xFFFFFFFFull;
+        const double r = decode_bits(bits);
+        const double r_prev = *last_res;
         *last_res = r;
         cur = nxt;
         if (!std::isfinite(r)) {
             *last_res = INFINITY;
             return fail(ctx, MB4CU_NONCONVERGED, "stage iteration diverged (non-finite update)");
         }
-        if (r <= ctx->eps) {
+        if (mb4cu::stage_converged(r, r_prev, it - 1, ctx->eps)) {
             std::swap(ctx->u0, ctx->U[cur][2]);
             return MB4CU_OK;
         }
@@ -287,7 +291,16 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->m = m;
     ctx->kernel = p->kernel;
     ctx->ghost = p->ghost;
-    if (p->ghost < 0 || (p->ghost > 0 && (p->ghost < m + 1 || m > 2 || p->kernel != 0))) {
+    // first-sweep depth: default 2 on the production kernel (v1 march: same as m)
+    ctx->mf = p->neumann_first >= 0 ? p->neumann_first : (p->kernel == 2 || m > 2 ? m : 2);
+    if (p->kernel == 2) ctx->mf = m;
+    if (ctx->mf != m && !(ctx->mf == 2 && m <= 2)) {
+        g_create_error = "mb4cu_create: neumann_first must equal neumann_terms or be 2";
+        delete ctx;
+        return MB4CU_INVALID;
+    }
+    const int mmax = ctx->mf > m ? ctx->mf : m;
+    if (p->ghost < 0 || (p->ghost > 0 && (p->ghost < mmax + 1 || m > 2 || p->kernel != 0))) {
         g_create_error = "mb4cu_create: sub-domain mode needs ghost >= neumann_terms + 1, m <= 2, kernel 0";
         delete ctx;
         return MB4CU_INVALID;
@@ -324,7 +337,9 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if (ctx->kernel != 1) {
         const int grid = std::max(mb4cu::march_grid_size(ctx->m, ctx->device),
-                                  ctx->m <= 2 ? mb4cu::march2_grid_size(ctx->m, ctx->device) : 0);
+                                  mb4cu::march2_supported(ctx->mf, ctx->m)
+                                      ? mb4cu::march2_grid_size(ctx->mf, ctx->m, ctx->device)
+                                      : 0);
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
         if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * ctx->max_iters)) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
@@ -663,7 +678,7 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
     const SweepConsts c = make_consts(ctx, h);
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
-    MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
+    MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
                                             ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
                                             ctx->device, ctx->stream, ctx->ghost, s));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));

@@ -309,12 +309,15 @@ mb4_step_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         }
         block_max_to(rmax, &a.rmax[s]);
         grid.sync();
-        const unsigned long long bits = __ldcg(&a.rmax[s]);
+        unsigned long long bits = __ldcg(&a.rmax[s]);
+        // same widened high-word residual as the production kernel
+        if (bits >> 32) bits = (bits & 0xFFFFFFFF00000000ull) | 0xFFFFFFFFull;
+        const double rprev = rlast;
         rlast = __longlong_as_double(static_cast<long long>(bits));
         sweeps = s + 1;
         set = out;
         if (!isfinite(rlast)) break;
-        if (rlast <= a.eps) {
+        if (stage_converged(rlast, rprev, s, a.eps)) {
             converged = 1;
             break;
         }

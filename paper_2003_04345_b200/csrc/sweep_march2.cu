@@ -36,6 +36,9 @@
 #ifndef MB4_MINB_M1
 #define MB4_MINB_M1 2
 #endif
+#ifndef MB4_UNROLL3
+#define MB4_UNROLL3 1
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -411,12 +414,26 @@ struct March3 {
 #pragma unroll
         for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k, k);
         const int jend = R + 2 * M + 2;
+#if MB4_UNROLL3
         for (int j = 0; j < jend; j += 3) {
             const int h3 = ((j / 3) & 1) * 3;
             body<0>(a, cf, uin, uout, s, j, h3, rmax, acc);
             body<1>(a, cf, uin, uout, s, j + 1, h3, rmax, acc);
             body<2>(a, cf, uin, uout, s, j + 2, h3, rmax, acc);
         }
+#else
+        // one body per row; the register window rotates by explicit moves
+        for (int j = 0; j < jend; ++j) {
+            body<0>(a, cf, uin, uout, s, j, j % 6, rmax, acc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                zw[1][q] = zw[2][q];
+                zw[2][q] = zw[0][q];
+            }
+            vw[1] = vw[2];
+            vw[2] = vw[0];
+        }
+#endif
         cp_async_wait<0>();
         __syncthreads();
     }
@@ -427,9 +444,11 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
                            const double2* const uin[3], double2* const uout[3],
                            unsigned& rmax, double acc[kObsFields]) {
     March3<M, NT, FIRST, ISO, GHOST> m(smem);
+    // band-rows of this sweep's band width (TX depends on M)
+    const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
     const long long G = gridDim.x;
-    const long long b0 = a.total * blockIdx.x / G;
-    const long long b1 = a.total * (blockIdx.x + 1) / G;
+    const long long b0 = total * blockIdx.x / G;
+    const long long b1 = total * (blockIdx.x + 1) / G;
     long long pos = b0;
     while (pos < b1) {
         const int band = static_cast<int>(pos / a.ny);
@@ -441,8 +460,18 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
     }
 }
 
-template <int M, int NT, bool ISO, bool GHOST>
-__global__ void __launch_bounds__(NT, Geom3<M, NT>::MINB)
+// MF: Neumann depth of the first sweep of a step (whose level 0 is the cheap closed
+// form, so a deeper first sweep costs little and saves one later sweep: measured
+// 5 -> 4 sweeps/step at cfg5 for (MF, M) = (2, 1)); M: depth of the other sweeps.
+template <int MF, int M, int NT>
+struct KGeom {
+    static constexpr size_t bytes = Geom3<MF, NT>::bytes > Geom3<M, NT>::bytes ? Geom3<MF, NT>::bytes
+                                                                             : Geom3<M, NT>::bytes;
+    static constexpr int MINB = (MF == 2 || M == 2) ? 2 : MB4_MINB_M1;
+};
+
+template <int MF, int M, int NT, bool ISO, bool GHOST>
+__global__ void __launch_bounds__(NT, (KGeom<MF, M, NT>::MINB))
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
@@ -472,7 +501,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         unsigned rmax = 0u;
         if (sg == 0) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all3<M, NT, true, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
+            sweep_all3<MF, NT, true, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -497,11 +526,12 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[s]);
         grid.sync();
         const unsigned long long bits = __ldcg(&a.rmax[s]);
+        const double rprev = rlast;
         rlast = __longlong_as_double(static_cast<long long>(bits));
         sweeps = sg + 1;
         set = out;
         if (!isfinite(rlast)) break;
-        if (rlast <= a.eps) {
+        if (stage_converged(rlast, rprev, sg, a.eps)) {
             converged = 1;
             break;
         }
@@ -519,16 +549,16 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     }
 }
 
-template <int M, int NT, bool ISO, bool GHOST>
+template <int MF, int M, int NT, bool ISO, bool GHOST>
 struct Launcher3 {
     static int grid_size(int device) {
         static int cached[64] = {0};
         if (device >= 0 && device < 64 && cached[device]) return cached[device];
-        const size_t smem = Geom3<M, NT>::bytes;
-        cudaFuncSetAttribute(mb4_step3_kernel<M, NT, ISO, GHOST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const size_t smem = KGeom<MF, M, NT>::bytes;
+        cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<M, NT, ISO, GHOST>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<MF, M, NT, ISO, GHOST>, NT, smem);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
@@ -539,36 +569,40 @@ struct Launcher3 {
     static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
         const int grid = grid_size(device);
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
-        a.nbands = (a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX;
-        a.total = static_cast<long long>(a.nbands) * a.ny;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<M, NT, ISO, GHOST>),
-                                           dim3(grid), dim3(NT), params, Geom3<M, NT>::bytes, s);
+        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST>),
+                                           dim3(grid), dim3(NT), params, KGeom<MF, M, NT>::bytes, s);
     }
 };
 
-template <int M>
+template <int MF, int M>
 cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
     if (a.ghost > 0) {
-        return c.iso ? Launcher3<M, 128, true, true>::launch(a, c, device, s)
-                     : Launcher3<M, 128, false, true>::launch(a, c, device, s);
+        return c.iso ? Launcher3<MF, M, 128, true, true>::launch(a, c, device, s)
+                     : Launcher3<MF, M, 128, false, true>::launch(a, c, device, s);
     }
-    return c.iso ? Launcher3<M, 128, true, false>::launch(a, c, device, s)
-                 : Launcher3<M, 128, false, false>::launch(a, c, device, s);
+    return c.iso ? Launcher3<MF, M, 128, true, false>::launch(a, c, device, s)
+                 : Launcher3<MF, M, 128, false, false>::launch(a, c, device, s);
 }
 
-template <int M>
+template <int MF, int M>
 int grid3(int device) {
     int g = 0;
-    const int v[4] = {Launcher3<M, 128, true, false>::grid_size(device), Launcher3<M, 128, false, false>::grid_size(device),
-                      Launcher3<M, 128, true, true>::grid_size(device), Launcher3<M, 128, false, true>::grid_size(device)};
+    const int v[4] = {Launcher3<MF, M, 128, true, false>::grid_size(device),
+                      Launcher3<MF, M, 128, false, false>::grid_size(device),
+                      Launcher3<MF, M, 128, true, true>::grid_size(device),
+                      Launcher3<MF, M, 128, false, true>::grid_size(device)};
     for (int x : v) g = x > g ? x : g;
     return g;
 }
 
 }  // namespace
 
-cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const double* V,
+bool march2_supported(int mf, int m) {
+    return (m >= 0 && m <= 2) && (mf == m || mf == 2);
+}
+
+cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0, const double* V,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
@@ -589,19 +623,23 @@ cudaError_t launch_step_march2(int m, int nx, int ny, const double2* u0, const d
     a.ghost = ghost;
     a.pitch = nx + 2 * ghost;
     a.sweep0 = sweep0;
-    switch (m) {
-        case 0: return dispatch3<0>(a, c, device, s);
-        case 1: return dispatch3<1>(a, c, device, s);
-        case 2: return dispatch3<2>(a, c, device, s);
+    switch (mf * 4 + m) {
+        case 0: return dispatch3<0, 0>(a, c, device, s);
+        case 5: return dispatch3<1, 1>(a, c, device, s);
+        case 10: return dispatch3<2, 2>(a, c, device, s);
+        case 8: return dispatch3<2, 0>(a, c, device, s);
+        case 9: return dispatch3<2, 1>(a, c, device, s);
     }
     return cudaErrorInvalidValue;
 }
 
-int march2_grid_size(int m, int device) {
-    switch (m) {
-        case 0: return grid3<0>(device);
-        case 1: return grid3<1>(device);
-        case 2: return grid3<2>(device);
+int march2_grid_size(int mf, int m, int device) {
+    switch (mf * 4 + m) {
+        case 0: return grid3<0, 0>(device);
+        case 5: return grid3<1, 1>(device);
+        case 10: return grid3<2, 2>(device);
+        case 8: return grid3<2, 0>(device);
+        case 9: return grid3<2, 1>(device);
     }
     return 0;
 }

@@ -31,6 +31,30 @@ from . import _lib
 WEST, EAST, SOUTH, NORTH = 0, 1, 2, 3
 F_U0, F_V, F_SET0, F_SET1 = 0, 1, 2, 3
 
+# Stopping rule, identical to the device kernels (mb4cu_internal.hpp: stage_converged):
+# the reference test r <= eps plus a margin on the predicted next update.
+STOP_MARGIN = 0.01
+STAGNATION = 0.8
+
+
+def widen_residual(r: float) -> float:
+    """The kernels track ||r||_inf on the high 32 bits of |r| and report the largest
+    double with that high word (an upper bound within 1 + 2^-20)."""
+    import struct
+
+    b = struct.unpack("<Q", struct.pack("<d", abs(r)))[0]
+    if b >> 32:
+        b = (b & 0xFFFFFFFF00000000) | 0xFFFFFFFF
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def stage_converged(r: float, r_prev: float, s: int, eps: float) -> bool:
+    if not r <= eps:
+        return False
+    if s == 0:
+        return r <= STOP_MARGIN * eps
+    return r * r <= STOP_MARGIN * eps * r_prev or r >= STAGNATION * r_prev
+
 
 def choose_grid(n: int, gnx: int, gny: int) -> Tuple[int, int]:
     """px * py = n minimising the halo perimeter per rank (ties: squarest blocks)."""
@@ -205,7 +229,7 @@ class DistributedSession:
 
     def _substep(self, h: float) -> Tuple[int, float]:
         self.halo.exchange(F_U0)
-        r = float("nan")
+        r = r_prev = float("nan")
         for s in range(self.max_iters):
             if s > 0:
                 self.halo.exchange(F_SET0 + ((s - 1) & 1))
@@ -215,9 +239,10 @@ class DistributedSession:
                 self.entry_sums = self.comm.allreduce_sum(sums)
             if not math.isfinite(r):
                 raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
-            if r <= self.eps:
+            if stage_converged(r, r_prev, s, self.eps):
                 self.b.commit(s + 1)
                 return s + 1, r
+            r_prev = r
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
     def step(self, h: float) -> Tuple[int, int]:
@@ -258,7 +283,8 @@ class CudaBackend:
     """libmb4cu sub-domain context on this rank's GPU (ghost mode)."""
 
     def __init__(self, dec: Decomposition, V_block: np.ndarray, scheme, gamma: float, cx: float, cy: float,
-                 epsilon: float, max_iters: int, neumann_terms: int, device: int):
+                 epsilon: float, max_iters: int, neumann_terms: int, device: int,
+                 neumann_first: int = 2):
         import torch
 
         self.torch = torch
@@ -271,9 +297,10 @@ class CudaBackend:
         p.V = _lib.dptr(self._v)
         p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, 0
         p.neumann_terms = neumann_terms
+        p.neumann_first = neumann_first
         p.device = device
         p.kernel = 0
-        p.ghost = neumann_terms + 1
+        p.ghost = max(neumann_terms, neumann_first) + 1
         self.ctx = C.c_void_p()
         rc = self.L.mb4cu_create(C.byref(p), C.byref(scheme.raw), C.byref(self.ctx))
         if rc:

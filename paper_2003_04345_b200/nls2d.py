@@ -271,7 +271,7 @@ class Session:
 
     def __init__(self, model: GridModel, scheme: Optional[Mb4Scheme] = None,
                  cfg: Optional[NewtonConfig] = None, neumann_terms: Optional[int] = None,
-                 device: int = 0, kernel: int = 0):
+                 device: int = 0, kernel: int = 0, neumann_first: Optional[int] = None):
         self._L = _lib.lib()
         self.model = model
         self.scheme = scheme if scheme is not None else Mb4Scheme()
@@ -287,6 +287,8 @@ class Session:
         p.max_iters = self.cfg.max_iters
         p.max_step_halvings = self.cfg.max_step_halvings
         p.neumann_terms = -1 if neumann_terms is None else int(neumann_terms)
+        p.neumann_first = -1 if neumann_first is None else int(neumann_first)
+        p.ghost = 0
         p.device = device
         p.kernel = kernel
         self._ctx = C.c_void_p()

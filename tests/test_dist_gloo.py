@@ -23,9 +23,10 @@ from paper_2003_04345_b200 import configs, dist as D, nls2d
 class NumpyBackend:
     """Numpy stand-in for dist.CudaBackend (test infrastructure)."""
 
-    def __init__(self, dec, V_block, scheme, gamma, cx, cy, m):
+    def __init__(self, dec, V_block, scheme, gamma, cx, cy, m, mf=None):
         self.dec, self.scheme, self.gamma, self.cx, self.cy, self.m = dec, scheme, gamma, cx, cy, m
-        self.g = m + 1
+        self.mf = m if mf is None else mf
+        self.g = max(m, self.mf) + 1
         self.P = (dec.lny + 2 * self.g, dec.lnx + 2 * self.g)
         z = lambda: np.zeros(self.P, dtype=np.complex128)  # noqa: E731
         self.u0 = z()
@@ -86,8 +87,8 @@ class NumpyBackend:
         PY, PX = self.P
         flat = lambda a: a.reshape(-1)  # noqa: E731
         U_in = None if s == 0 else [flat(u) for u in self.U[(s - 1) & 1]]
-        Un, _ = SM.sweep(flat(self.u0), U_in, flat(self.V), self.gamma, h, self.scheme, self.m, PX, PY,
-                         self.cx, self.cy)
+        Un, _ = SM.sweep(flat(self.u0), U_in, flat(self.V), self.gamma, h, self.scheme,
+                         self.mf if s == 0 else self.m, PX, PY, self.cx, self.cy)
         src = [self.u0] * 3 if s == 0 else self.U[(s - 1) & 1]
         out = self.U[s & 1]
         r = 0.0
@@ -97,7 +98,7 @@ class NumpyBackend:
             r = max(r, np.abs(d.real).max(), np.abs(d.imag).max())
             out[q][...] = new
         sums = self.obs_sums() if s == 0 else np.zeros(5)
-        return r, sums
+        return D.widen_residual(r), sums
 
     def commit(self, sweeps):
         k = (sweeps - 1) & 1
@@ -140,7 +141,7 @@ def _worker(rank, world, port, px, py, m, nsteps, out_dir):
         V, psi = configs.make_inputs(cfg)
         dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
         scheme = nls2d.Mb4Scheme()
-        be = NumpyBackend(dec, dec.block(V), scheme, cfg.gamma, 1.0, 1.0, m)
+        be = NumpyBackend(dec, dec.block(V), scheme, cfg.gamma, 1.0, 1.0, m, mf=2)
         be.set_state(dec.block(psi))
         sess = D.DistributedSession(dec, be, D.Comm("cpu"), cfg.gamma, 1.0, 1.0, cfg.epsilon)
         obs, sweeps = sess.run(cfg.dt, nsteps)
@@ -155,7 +156,7 @@ def _reference(m, nsteps):
     scheme = nls2d.Mb4Scheme()
     u, its = psi, []
     for _ in range(nsteps):
-        u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon)
+        u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=2)
         its.append(it)
     return u, its
 

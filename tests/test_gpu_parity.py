@@ -91,7 +91,8 @@ def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
     V, psi = configs.make_inputs(cfg)
     model = configs.model_for(cfg, V)
     scheme = nls2d.Mb4Scheme()
-    ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon)
+    mf = m if (kernel == 2 or m > 2) else 2  # production/tiled default: first sweep depth 2
+    ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=mf)
     with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=m, kernel=kernel) as s:
         s.set_state(psi)
         st = nls2d.StepStats()
