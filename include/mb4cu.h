@@ -203,6 +203,9 @@ typedef struct {
     long long sweeps;         /* stage sweeps executed                                */
     double alg_bytes;         /* algorithmic bytes of those sweeps                    */
     long long other_launches; /* energy-monitor / helper kernels                      */
+    double sweep_ms[8];       /* device time by sweep index within a step (0 = first),
+                                 persistent kernel only (%globaltimer at grid barriers) */
+    long long sweep_n[8];     /* samples accumulated in sweep_ms                      */
 } mb4cu_profile;
 
 int mb4cu_profile_enable(mb4cu_ctx* ctx, int on);

@@ -80,6 +80,8 @@ class Profile(C.Structure):
         ("sweeps", C.c_longlong),
         ("alg_bytes", D),
         ("other_launches", C.c_longlong),
+        ("sweep_ms", D * 8),
+        ("sweep_n", C.c_longlong * 8),
     ]
 
 

@@ -109,6 +109,12 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         c.first_ss[k] = cc * c.first_s[k];
         c.first_cs[k] = cc * c.first_c[k];
     }
+    for (int i = 0; i < 3; ++i)
+        for (int n = 0; n < 4; ++n) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += s.T[i][k] * c.first_s[k] * std::pow(c.hlam[k], n);
+            c.fco[i][n] = -acc * (c.iso ? std::pow(cc, n + 1) : 1.0);
+        }
     return c;
 }
 
@@ -148,6 +154,12 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         ctx->prof.launches += 1;
         ctx->prof.sweeps += st.sweeps;
         ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (st.sweeps - 1));
+        if (ctx->kernel == 0 && mb4cu::march2_supported(ctx->mf, ctx->m)) {
+            for (int k = 0; k < st.sweeps && k < 8; ++k) {
+                ctx->prof.sweep_ms[k] += 1e-6 * static_cast<double>(st.t[k + 1] - st.t[k]);
+                ctx->prof.sweep_n[k] += 1;
+            }
+        }
     }
     // the first sweep evaluated the energy sums of the entry state
     for (int f = 0; f < mb4cu::kObsFields; ++f) ctx->obs_cache[f] = st.obs[f];

@@ -37,6 +37,12 @@ struct SweepConsts {
     double hls[3];      // c * h * lambda_k
     double first_ss[3]; // c * first_s
     double first_cs[3]; // c * first_c
+    // First sweep at Neumann depth MF from U = (u0,u0,u0): every phibar_k is a
+    // multiple of f(u0), so the recursion needs only g_n = J^n f (n <= MF) once,
+    // not per stage:  U_i = u0 + sum_n fco[i][n] g_n  with
+    //   fco[i][n] = -sum_k T[i][k] first_s[k] (h lam_k)^n
+    // (in isotropic units -- f and J evaluated with the unit stencil -- times c^(n+1)).
+    double fco[3][4];
     double h;
     double gamma;
     double cx, cy, diag;  // stencil: diag = 2cx + 2cy
@@ -91,7 +97,17 @@ struct StepStatus {
     int pad;
     double rlast;      // ||r||_inf of the last sweep
     double obs[kObsFields];  // energy sums of u0 (first sweep)
+    // %globaltimer (ns) at kernel start and after each sweep's grid barrier
+    // (block 0), for per-sweep timing; entries past `sweeps` are stale.
+    static constexpr int kMaxTimed = 16;
+    unsigned long long t[kMaxTimed + 1];
 };
+
+__device__ __forceinline__ unsigned long long global_timer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Arguments of one persistent step launch (sweep_march*.cu).
 struct StepArgs {

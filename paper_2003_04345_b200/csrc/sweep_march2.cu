@@ -96,6 +96,14 @@ struct Coef {
         const double jy = fma(g(), nlx, -a.x);
         return make_double2(fma(hl(k), jx, base.x), fma(hl(k), jy, base.y));
     }
+    // J t (isotropic: J t / c) from a = kv(...) of t and u0
+    __device__ __forceinline__ double2 jt(double2 t, double2 a, double2 u0) const {
+        const double pp = u0.x * u0.x, qq = u0.y * u0.y;
+        const double al = fma(3.0, pp, qq), be = 2.0 * u0.x * u0.y, de = fma(3.0, qq, pp);
+        const double nlx = fma(al, t.x, be * t.y);
+        const double nly = fma(be, t.x, de * t.y);
+        return make_double2(fma(-g(), nly, a.y), fma(g(), nlx, -a.x));
+    }
 };
 
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
@@ -439,10 +447,209 @@ struct March3 {
     }
 };
 
+// First sweep of a step at Neumann depth MF >= 1, specialised.  From U = (u0,u0,u0)
+// every phibar_k = first_s[k] f(u0), so the M-term recursion of all three stages
+// reduces to the chain g_0 = f, g_n = J g_{n-1} (one complex per site and level
+// instead of three) and U_i = u0 + sum_n fco[i][n] g_n.  Same band march, ring
+// and publish-row scheme as March3 (level n at row i - n, one barrier per row).
+template <int MF, int NT, bool ISO, bool GHOST>
+struct MarchFirst {
+    static_assert(MF >= 1 && MF <= 2, "first-sweep depth 1..2");
+    using G = Geom3<MF, NT>;
+    static constexpr int ZW = G::ZW;
+    static constexpr int S = 12;  // light rows: prefetch deeper (P = 8 / 10 rows) to cover HBM latency
+    static constexpr int BACK = MF == 2 ? 3 : 1;
+    static constexpr int P = S - 1 - BACK;
+    static constexpr size_t zu0_bytes = sizeof(double2) * S * ZW;
+    static constexpr size_t zv_bytes = ((sizeof(double) * S * ZW + 15) / 16) * 16;
+    static constexpr size_t bytes = zu0_bytes + zv_bytes + sizeof(double2) * MF * 2 * ZW;
+    static_assert(bytes <= Geom3<MF, NT>::bytes, "fits the kernel's dynamic smem");
+
+    double2* zu0;
+    double* zv;
+    double2* pub;  // [MF][2][ZW]
+    double2 zw[3];
+    double vw[3];
+
+    __device__ MarchFirst(unsigned char* smem) {
+        zu0 = reinterpret_cast<double2*>(smem);
+        zv = reinterpret_cast<double*>(smem + zu0_bytes);
+        pub = reinterpret_cast<double2*>(smem + zu0_bytes + zv_bytes);
+    }
+    __device__ __forceinline__ double2* pub_row(int level, int parity) { return pub + (level * 2 + parity) * ZW; }
+    __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
+        if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
+        return static_cast<size_t>(y) * a.nx + x;
+    }
+
+    struct Seg {
+        int X0, Y0, R, nzrows, gxa, gxb, next_row;
+        size_t next_off;
+    };
+
+    __device__ __forceinline__ void issue_row(const StepArgs& a, Seg& s, int k, int slot) {
+        if (k < s.nzrows) {
+            const size_t rowoff = s.next_off;
+            if (GHOST) {
+                s.next_off += a.pitch;
+            } else if (++s.next_row == a.ny) {
+                s.next_row = 0;
+                s.next_off = 0;
+            } else {
+                s.next_off += a.nx;
+            }
+            const int t = threadIdx.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && t >= 2) break;
+                const int col = t + h * NT;
+                const size_t g = rowoff + (h ? s.gxb : s.gxa);
+                cp_async16(&zu0[slot * ZW + col], a.u0 + g);
+                cp_async8(&zv[slot * ZW + col], a.V + g);
+            }
+        }
+        cp_async_commit();
+    }
+
+    __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3],
+                                         Seg& s, int j, unsigned& rmax, double acc[kObsFields]) {
+        const SweepConsts& c = cf.c;
+        const int t = threadIdx.x, cc = t + 1, i = j - 2;
+        auto ring = [&](int k) { return ((j - k) % S + S) % S; };
+        const int slot_new = ring(0), slot_cen = ring(1);
+        cp_async_wait<P - 1>();
+        __syncthreads();
+        issue_row(a, s, j + P, ring(-P));
+
+        const int yrel = i - 2 * MF;
+        const int xout = s.X0 - MF + t;
+        const bool out_ok = yrel >= 0 && yrel < s.R && t >= MF && t < NT - MF && xout < a.nx;
+        const int par = j & 1, ppar = par ^ 1;
+
+        zw[0] = zu0[slot_new * ZW + cc];  // window: [0] new (z row j), [1] centre, [2] down
+        vw[0] = zv[slot_new * ZW + cc];
+
+        // own-column history, read before this iteration republishes the rows
+        const double2 f_m2 = MF == 2 ? pub_row(0, par)[cc] : make_double2(0.0, 0.0);   // f(i-2)
+        const double2 g1_m3 = MF == 2 ? pub_row(1, par)[cc] : make_double2(0.0, 0.0);  // g1(i-3)
+
+        // ---- level 0 at row i: f(u0) and the energy monitor --------------------
+        const double v = vw[1];
+        const double2 u0c = zw[1];
+        const double2 w0 = cf.kv(cf.dv(v), u0c, zu0[slot_cen * ZW + cc - 1], zu0[slot_cen * ZW + cc + 1],
+                                 zw[2], zw[0]);
+        const double n2 = fma(u0c.x, u0c.x, u0c.y * u0c.y);
+        const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
+        const double gy = fma(-cf.g() * n2, u0c.y, w0.y);
+        const double2 f = make_double2(gy, -gx);
+        if (i >= MF && i < MF + s.R && t >= MF && t < NT - MF && xout < a.nx) {
+            const double vn = v * n2;
+            const double sc = ISO ? c.cx : 1.0;
+            acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
+            acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
+            acc[2] += n2;
+            acc[3] += n2 * n2;
+            acc[4] += vn;
+        }
+
+        // ---- level 1 at row i-1: g1 = J f ---------------------------------------
+        const double2* f_row = pub_row(0, ppar);  // f(i-1), published last iteration
+        const double2 f_c = f_row[cc];
+        const double2 f_dn = MF == 2 ? f_m2 : pub_row(0, par)[cc];  // f(i-2)
+        const double2 u0m = zw[2];                                   // u0(i-1)
+        const double2 a1 = cf.kv(cf.dv(vw[2]), f_c, f_row[cc - 1], f_row[cc + 1], f_dn, f);
+        const double2 g1 = cf.jt(f_c, a1, u0m);
+        pub_row(0, par)[cc] = f;  // publish f(i)
+
+        if (MF == 1) {
+            if (out_ok) {
+                const size_t gi = at(a, xout, s.Y0 + yrel);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double2 r = make_double2(fma(c.fco[q][0], f_c.x, c.fco[q][1] * g1.x),
+                                                   fma(c.fco[q][0], f_c.y, c.fco[q][1] * g1.y));
+                    uout[q][gi] = make_double2(u0m.x + r.x, u0m.y + r.y);
+                    March3<MF, NT, true, ISO, GHOST>::track(rmax, r);
+                }
+            }
+        } else {
+            // ---- level 2 at row i-2: g2 = J g1; output -------------------------
+            if (out_ok) {
+                const double2* g_row = pub_row(1, ppar);  // g1(i-2)
+                const double2 g_c = g_row[cc];
+                const int slot_m3 = ring(3);              // z row j-3 == row i-2
+                const double2 u0o = zu0[slot_m3 * ZW + cc];
+                const double2 a2 = cf.kv(cf.dv(zv[slot_m3 * ZW + cc]), g_c, g_row[cc - 1], g_row[cc + 1], g1_m3, g1);
+                const double2 g2 = cf.jt(g_c, a2, u0o);
+                const size_t gi = at(a, xout, s.Y0 + yrel);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double2 r = make_double2(
+                        fma(c.fco[q][0], f_m2.x, fma(c.fco[q][1], g_c.x, c.fco[q][2] * g2.x)),
+                        fma(c.fco[q][0], f_m2.y, fma(c.fco[q][1], g_c.y, c.fco[q][2] * g2.y)));
+                    uout[q][gi] = make_double2(u0o.x + r.x, u0o.y + r.y);
+                    March3<MF, NT, true, ISO, GHOST>::track(rmax, r);
+                }
+            }
+            pub_row(1, par)[cc] = g1;  // publish g1(i-1)
+        }
+        // rotate the window: down <- centre <- new
+        zw[2] = zw[1];
+        zw[1] = zw[0];
+        vw[2] = vw[1];
+        vw[1] = vw[0];
+    }
+
+    __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int band, int Y0,
+                        int R, unsigned& rmax, double acc[kObsFields]) {
+        const Coef<ISO> cf{c};
+        Seg s;
+        s.X0 = band * G::TX;
+        s.Y0 = Y0;
+        s.R = R;
+        s.nzrows = R + 2 * MF + 2;
+        const int yz0 = Y0 - MF - 1, xz0 = s.X0 - MF - 1;
+        if (GHOST) {
+            s.next_off = static_cast<size_t>(yz0 + a.ghost) * a.pitch;
+            const int last = a.pitch - 1;
+            const int ca = xz0 + static_cast<int>(threadIdx.x) + a.ghost, cb = ca + NT;
+            s.gxa = ca < last ? ca : last;
+            s.gxb = cb < last ? cb : last;
+        } else {
+            s.next_row = wrap_index(yz0, a.ny);
+            s.next_off = static_cast<size_t>(s.next_row) * a.nx;
+            s.gxa = wrap_index(xz0 + static_cast<int>(threadIdx.x), a.nx);
+            s.gxb = wrap_index(xz0 + static_cast<int>(threadIdx.x) + NT, a.nx);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) issue_row(a, s, k, k);
+        const int jend = R + 2 * MF + 2;
+        for (int j = 0; j < jend; ++j) body(a, cf, uout, s, j, rmax, acc);
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+};
+
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
                            unsigned& rmax, double acc[kObsFields]) {
+    if constexpr (FIRST && M >= 1) {
+        MarchFirst<M, NT, ISO, GHOST> mf(smem);
+        const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
+        const long long G = gridDim.x;
+        const long long b0 = total * blockIdx.x / G;
+        const long long b1 = total * (blockIdx.x + 1) / G;
+        for (long long pos = b0; pos < b1;) {
+            const int band = static_cast<int>(pos / a.ny);
+            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
+            const long long band_end = static_cast<long long>(band + 1) * a.ny;
+            const long long seg_end = band_end < b1 ? band_end : b1;
+            mf.run(a, c, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
+            pos = seg_end;
+        }
+        return;
+    }
     March3<M, NT, FIRST, ISO, GHOST> m(smem);
     // band-rows of this sweep's band width (TX depends on M)
     const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
@@ -493,6 +700,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     const SweepConsts& cc = c;
 #endif
     int sweeps = 0, set = 0, converged = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
     double rlast = 0.0;
     for (int s = 0; s < a.max_iters; ++s) {
         const int sg = s + a.sweep0;  // global sweep index within the (sub)step
@@ -525,6 +733,8 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         }
         block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[s]);
         grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0 && s < StepStatus::kMaxTimed)
+            a.status->t[s + 1] = global_timer_ns();
         const unsigned long long bits = __ldcg(&a.rmax[s]);
         const double rprev = rlast;
         rlast = __longlong_as_double(static_cast<long long>(bits));

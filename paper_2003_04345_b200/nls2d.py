@@ -375,7 +375,11 @@ class Session:
     def profile(self) -> dict:
         p = _lib.Profile()
         self._check(self._L.mb4cu_profile_get(self._ctx, C.byref(p)))
-        return {f: getattr(p, f) for f, _ in _lib.Profile._fields_}
+        out = {}
+        for f, _ in _lib.Profile._fields_:
+            v = getattr(p, f)
+            out[f] = list(v) if hasattr(v, "__len__") else v
+        return out
 
     def observables(self) -> Observables:
         o = _lib.Obs()
