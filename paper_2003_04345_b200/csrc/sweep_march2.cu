@@ -672,9 +672,11 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
 // 5 -> 4 sweeps/step at cfg5 for (MF, M) = (2, 1)); M: depth of the other sweeps.
 template <int MF, int M, int NT>
 struct KGeom {
-    static constexpr size_t bytes = Geom3<MF, NT>::bytes > Geom3<M, NT>::bytes ? Geom3<MF, NT>::bytes
-                                                                             : Geom3<M, NT>::bytes;
-    static constexpr int MINB = (MF == 2 || M == 2) ? 2 : MB4_MINB_M1;
+    // the first sweep runs MarchFirst (MF >= 1) or March3<0>; later sweeps March3<M>
+    static constexpr size_t first_bytes = MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
+                                                  : Geom3<0, NT>::bytes;
+    static constexpr size_t bytes = first_bytes > Geom3<M, NT>::bytes ? first_bytes : Geom3<M, NT>::bytes;
+    static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
 };
 
 template <int MF, int M, int NT, bool ISO, bool GHOST>

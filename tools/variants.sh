@@ -5,5 +5,6 @@ for lib in "$@"; do
   MB4CU_LIB=$PWD/paper_2003_04345_b200/$lib python bench.py $ARGS --no-cpu-baseline --no-e2e 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
-print('$lib', d['config']['workload'][:5], 'm=%s'%d['config']['neumann_terms'], '%.3e'%d['value'], d['sweeps_per_step'], 'frac=%.3f'%d['roofline']['frac'], 'ms/launch=%.3f'%d['roofline']['kernel_ms_per_launch'], d['clocks'])"
+r=d['roofline']
+print('$lib', d['config']['workload'][:5], 'm=%s'%d['config']['neumann_terms'], '%.3e'%d['value'], d['sweeps_per_step'], 'frac=%.3f'%r['frac'], 'ms/launch=%.3f'%r['kernel_ms_per_launch'], r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
 done
