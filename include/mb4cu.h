@@ -79,7 +79,10 @@ typedef struct {
     int max_step_halvings;    /* halving-on-failure policy (mb4_integrator.cpp:287-315) */
     int neumann_terms;        /* m in 0..3: preconditioner sum_{k<=m} (h lam J)^k; -1 = default */
     int device;               /* CUDA device ordinal                                    */
-    int kernel;               /* 0 = default (fastest), 1 = tiled reference kernel      */
+    int kernel;               /* stage solver: 0 = default (persistent matrix-free sweeps),
+                                 1 = tiled sweep kernel, 2 = march v1, 3 = Newton-Krylov
+                                 (the reference's simplified Newton with matrix-free
+                                 GMRES stage solves, for stiff h*lambda*rho(J) >~ 1)    */
     int ghost;                /* 0: one periodic domain.  > 0: this context is a sub-domain
                                  of a decomposed lattice (multi-GPU): arrays carry `ghost`
                                  halo layers (>= neumann_terms + 1) filled by the caller via

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "mb4cu.h"
 #include "mb4cu_internal.hpp"
@@ -47,6 +48,18 @@ struct mb4cu_ctx {
     bool obs_cached = false;                   // energy sums of the current u0 known
     double obs_cache[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
     double entry_obs[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
+    // Newton-Krylov path (kernel = 3), allocated on first use
+    struct {
+        int m = 0;                  // GMRES restart length
+        int nblk = 0;
+        double2* mem = nullptr;     // basis (m+1) + b[3] + x[3] + w + y vectors
+        double2** v_dev = nullptr;  // device array of basis pointers
+        double* partial = nullptr;  // [m+1][nblk]
+        double* h_partial = nullptr;  // pinned copy
+        double* coef = nullptr;     // device coefficients [m+1]
+        double* h_coef = nullptr;   // pinned
+        long long gmres_iters = 0;  // total inner iterations (stats)
+    } kr;
     bool profiling = false;
     mb4cu_profile prof{};
     std::string err;
@@ -179,9 +192,182 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
                 "stage iteration: no convergence after " + std::to_string(ctx->max_iters) + " sweeps");
 }
 
+// ---- Newton-Krylov stage solver (kernel = 3) --------------------------------
+// The reference's simplified Newton iteration (mb4_integrator.cpp:194-255) with
+// matrix-free GMRES(m) stage solves (restating iterative.cpp:68-153 without the
+// ILU(0) preconditioner); O(N) work on the device, Hessenberg on the host.
+
+constexpr int kKrylovRestart = 50;
+constexpr int kKrylovMaxIters = 2000;
+constexpr double kKrylovTol = 1e-13;
+
+int kr_alloc(mb4cu_ctx* ctx) {
+    auto& k = ctx->kr;
+    if (k.mem) return MB4CU_OK;
+    k.m = kKrylovRestart;
+    k.nblk = mb4cu::krylov_blocks(ctx->n);
+    const size_t nvec = static_cast<size_t>(k.m + 1) + 3 + 3 + 2;
+    MB4_CUDA(ctx, cudaMalloc(&k.mem, nvec * ctx->n * sizeof(double2)));
+    MB4_CUDA(ctx, cudaMalloc(&k.v_dev, sizeof(double2*) * (k.m + 1)));
+    std::vector<double2*> ptrs(k.m + 1);
+    for (int i = 0; i <= k.m; ++i) ptrs[i] = k.mem + static_cast<size_t>(i) * ctx->n;
+    MB4_CUDA(ctx, cudaMemcpy(k.v_dev, ptrs.data(), sizeof(double2*) * (k.m + 1), cudaMemcpyHostToDevice));
+    MB4_CUDA(ctx, cudaMalloc(&k.partial, sizeof(double) * (k.m + 1) * k.nblk));
+    MB4_CUDA(ctx, cudaMallocHost(&k.h_partial, sizeof(double) * (k.m + 1) * k.nblk));
+    MB4_CUDA(ctx, cudaMalloc(&k.coef, sizeof(double) * (k.m + 1)));
+    MB4_CUDA(ctx, cudaMallocHost(&k.h_coef, sizeof(double) * (k.m + 1)));
+    return MB4CU_OK;
+}
+
+double2* kr_vec(mb4cu_ctx* ctx, size_t idx) { return ctx->kr.mem + idx * ctx->n; }
+
+// fixed-order host sum of nv rows of block partials
+int kr_fetch(mb4cu_ctx* ctx, int nv, double* out) {
+    auto& k = ctx->kr;
+    MB4_CUDA(ctx, cudaMemcpyAsync(k.h_partial, k.partial, sizeof(double) * nv * k.nblk, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < nv; ++i) {
+        double s = 0.0;
+        for (int b = 0; b < k.nblk; ++b) s += k.h_partial[static_cast<size_t>(i) * k.nblk + b];
+        out[i] = s;
+    }
+    return MB4CU_OK;
+}
+
+// Solve (I - hl J(u0)) x = b, x initialised to zero.
+int kr_gmres(mb4cu_ctx* ctx, const SweepConsts& c, double hl, const double2* b, double2* x) {
+    auto& k = ctx->kr;
+    const size_t n = ctx->n;
+    const int m = k.m;
+    double2* w = kr_vec(ctx, m + 1 + 6);
+    double2* y = kr_vec(ctx, m + 1 + 7);
+    std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0),
+        yv(m, 0.0), tmp(m + 1, 0.0);
+    auto Hat = [&](int i, int j) -> double& { return H[static_cast<size_t>(i) * m + j]; };
+    MB4_CUDA(ctx, cudaMemsetAsync(x, 0, n * sizeof(double2), ctx->stream));
+    // v_0 <- b and ||b||^2 (residual of x = 0)
+    MB4_CUDA(ctx, cudaMemsetAsync(y, 0, n * sizeof(double2), ctx->stream));
+    MB4_CUDA(ctx, mb4cu::kr_residual(b, y, kr_vec(ctx, 0), n, k.partial, ctx->stream));
+    double bn2 = 0.0;
+    if (int rc = kr_fetch(ctx, 1, &bn2)) return rc;
+    const double bnorm = std::sqrt(bn2);
+    if (bnorm == 0.0) return MB4CU_OK;
+    bool first = true;
+    for (int iter = 0; iter < kKrylovMaxIters;) {
+        double beta;
+        if (first) {
+            beta = bnorm;  // r = b already in v_0 (unscaled)
+            first = false;
+        } else {
+            MB4_CUDA(ctx, mb4cu::kr_matvec(x, y, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream));
+            MB4_CUDA(ctx, mb4cu::kr_residual(b, y, kr_vec(ctx, 0), n, k.partial, ctx->stream));
+            double r2 = 0.0;
+            if (int rc = kr_fetch(ctx, 1, &r2)) return rc;
+            beta = std::sqrt(r2);
+        }
+        if (beta / bnorm <= kKrylovTol) return MB4CU_OK;
+        MB4_CUDA(ctx, mb4cu::kr_scale(kr_vec(ctx, 0), kr_vec(ctx, 0), 1.0 / beta, n, ctx->stream));
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int j = 0;
+        bool done = false;
+        for (; j < m && iter < kKrylovMaxIters; ++j, ++iter) {
+            MB4_CUDA(ctx, mb4cu::kr_matvec(kr_vec(ctx, j), w, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream));
+            for (int i = 0; i <= j; ++i) Hat(i, j) = 0.0;
+            double wn2 = 0.0;
+            for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, twice
+                MB4_CUDA(ctx, mb4cu::kr_dots(w, k.v_dev, j + 1, n, k.partial, ctx->stream));
+                if (int rc = kr_fetch(ctx, j + 1, tmp.data())) return rc;
+                for (int i = 0; i <= j; ++i) {
+                    Hat(i, j) += tmp[i];
+                    k.h_coef[i] = tmp[i];
+                }
+                MB4_CUDA(ctx, cudaMemcpyAsync(k.coef, k.h_coef, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                                              ctx->stream));
+                MB4_CUDA(ctx, mb4cu::kr_axpy_norm(w, k.v_dev, k.coef, j + 1, n, k.partial, ctx->stream));
+                if (int rc = kr_fetch(ctx, 1, &wn2)) return rc;
+            }
+            const double hn = std::sqrt(wn2);
+            Hat(j + 1, j) = hn;
+            if (hn > 0.0) MB4_CUDA(ctx, mb4cu::kr_scale(w, kr_vec(ctx, j + 1), 1.0 / hn, n, ctx->stream));
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);
+                Hat(i + 1, j) = -sn[i] * Hat(i, j) + cs[i] * Hat(i + 1, j);
+                Hat(i, j) = t;
+            }
+            const double den = std::hypot(Hat(j, j), Hat(j + 1, j));
+            if (den == 0.0) return fail(ctx, MB4CU_NONCONVERGED, "gmres: breakdown");
+            cs[j] = Hat(j, j) / den;
+            sn[j] = Hat(j + 1, j) / den;
+            Hat(j, j) = den;
+            Hat(j + 1, j) = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            if (std::fabs(g[j + 1]) / bnorm <= kKrylovTol || hn == 0.0) {
+                ++j;
+                ++iter;
+                done = true;
+                break;
+            }
+        }
+        k.gmres_iters += j;
+        for (int i = j - 1; i >= 0; --i) {
+            double s = g[i];
+            for (int q = i + 1; q < j; ++q) s -= Hat(i, q) * yv[q];
+            yv[i] = s / Hat(i, i);
+        }
+        for (int i = 0; i < j; ++i) k.h_coef[i] = yv[i];
+        MB4_CUDA(ctx, cudaMemcpyAsync(k.coef, k.h_coef, sizeof(double) * j, cudaMemcpyHostToDevice, ctx->stream));
+        MB4_CUDA(ctx, mb4cu::kr_combine(x, k.v_dev, k.coef, j, n, ctx->stream));
+        if (done) return MB4CU_OK;
+    }
+    return MB4CU_OK;  // best effort after the iteration cap, as the reference (iterative.cpp:152)
+}
+
+int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
+    if (int rc = kr_alloc(ctx)) return rc;
+    const SweepConsts c = make_consts(ctx, h);
+    const size_t sb = ctx->n * sizeof(double2);
+    double2* st[3] = {ctx->U[0][0], ctx->U[0][1], ctx->U[0][2]};
+    for (int i = 0; i < 3; ++i)
+        MB4_CUDA(ctx, cudaMemcpyAsync(st[i], ctx->u0, sb, cudaMemcpyDeviceToDevice, ctx->stream));
+    const int m = ctx->kr.m;
+    // vectors 0..m: Krylov basis; m+1..m+3: b; m+4..m+6: x; m+7, m+8: work (kr_gmres)
+    double2* b[3] = {kr_vec(ctx, m + 1), kr_vec(ctx, m + 2), kr_vec(ctx, m + 3)};
+    double2* x[3] = {kr_vec(ctx, m + 4), kr_vec(ctx, m + 5), kr_vec(ctx, m + 6)};
+    *iters = 0;
+    for (int it = 1; it <= ctx->max_iters; ++it) {
+        const double2* cst[3] = {st[0], st[1], st[2]};
+        MB4_CUDA(ctx, mb4cu::kr_phibar(ctx->nx, ctx->ny, ctx->u0, cst, ctx->V, b, c, ctx->stream));
+        for (int k = 0; k < 3; ++k)
+            if (int rc = kr_gmres(ctx, c, c.hlam[k], b[k], x[k])) return rc;
+        MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
+        const double2* cx[3] = {x[0], x[1], x[2]};
+        MB4_CUDA(ctx, mb4cu::kr_update(st, cx, ctx->n, ctx->d_rmax, c, ctx->stream));
+        MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        *iters = it;
+        const double r = decode_bits(*ctx->h_rmax);
+        *last_res = r;
+        if (!std::isfinite(r)) {
+            *last_res = INFINITY;
+            return fail(ctx, MB4CU_NONCONVERGED, "newton_solve: iteration diverged (non-finite update)");
+        }
+        if (r <= ctx->eps) {  // the reference test (:250); Newton's remaining error is << eps
+            std::swap(ctx->u0, ctx->U[0][2]);
+            return MB4CU_OK;
+        }
+    }
+    return fail(ctx, MB4CU_NONCONVERGED,
+                "newton_solve: no convergence after " + std::to_string(ctx->max_iters) + " iterations");
+}
+
 // One MB4 sub-step of size h on ctx->u0: sweeps until ||r||_inf <= eps
 // (newton_solve, mb4_integrator.cpp:194-255).  On success u0 <- U3 (c3 = 1).
 int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
+    if (ctx->kernel == 3) return substep_krylov(ctx, h, sweeps, last_res);
     if (ctx->kernel != 1) return substep_march(ctx, h, sweeps, last_res);
     const SweepConsts c = make_consts(ctx, h);
     int cur = -1;
@@ -303,6 +489,11 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->m = m;
     ctx->kernel = p->kernel;
     ctx->ghost = p->ghost;
+    if (p->kernel < 0 || p->kernel > 3) {
+        g_create_error = "mb4cu_create: kernel must be 0 (default), 1 (tiled), 2 (march v1) or 3 (Newton-Krylov)";
+        delete ctx;
+        return MB4CU_INVALID;
+    }
     // first-sweep depth: default 2 on the production kernel (v1 march: same as m)
     ctx->mf = p->neumann_first >= 0 ? p->neumann_first : (p->kernel == 2 || m > 2 ? m : 2);
     if (p->kernel == 2) ctx->mf = m;
@@ -400,6 +591,12 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs_march);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
+    cudaFree(ctx->kr.mem);
+    cudaFree(ctx->kr.v_dev);
+    cudaFree(ctx->kr.partial);
+    cudaFreeHost(ctx->kr.h_partial);
+    cudaFree(ctx->kr.coef);
+    cudaFreeHost(ctx->kr.h_coef);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->pev0) cudaEventDestroy(ctx->pev0);
@@ -597,7 +794,7 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     mb4cu_obs o{};
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
-    const bool fused = ctx->kernel != 1;
+    const bool fused = ctx->kernel == 0 || ctx->kernel == 2;
     for (int s = 1; s <= nsteps; ++s) {
         if (obs_series && !fused) {
             const int rc0 = mb4cu_observables(ctx, &o);

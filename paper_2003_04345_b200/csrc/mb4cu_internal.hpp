@@ -155,6 +155,20 @@ cudaError_t launch_halo_copy1(double* array, int pitch, int ghost, int x0, int y
                               double* buf, bool pack, cudaStream_t s);
 // Energy sums of a padded sub-domain state (ghosts of u must be current).
 cudaError_t launch_observables_ghost(const ObsArgs& a, int ghost, int pitch, double* out5, cudaStream_t s);
+// Newton-Krylov stage solver kernels (krylov.cu).
+int krylov_blocks(size_t n);
+cudaError_t kr_phibar(int nx, int ny, const double2* u0, const double2* const st[3], const double* V,
+                      double2* const b[3], const SweepConsts& c, cudaStream_t s);
+cudaError_t kr_matvec(const double2* x, double2* y, const double2* u0, const double* V, int nx, int ny, double hl,
+                      const SweepConsts& c, cudaStream_t s);
+cudaError_t kr_dots(const double2* w, double2* const* v_dev, int nv, size_t n, double* partial, cudaStream_t s);
+cudaError_t kr_axpy_norm(double2* w, double2* const* v_dev, const double* h_dev, int nv, size_t n, double* partial,
+                         cudaStream_t s);
+cudaError_t kr_scale(const double2* x, double2* y, double alpha, size_t n, cudaStream_t s);
+cudaError_t kr_combine(double2* x, double2* const* v_dev, const double* coef_dev, int nv, size_t n, cudaStream_t s);
+cudaError_t kr_residual(const double2* b, const double2* y, double2* r, size_t n, double* partial, cudaStream_t s);
+cudaError_t kr_update(double2* const st[3], const double2* const x[3], size_t n, unsigned long long* rmax,
+                      const SweepConsts& c, cudaStream_t s);
 size_t tiled_smem_bytes(int m, bool first);
 cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const SweepConsts& c,
                                cudaStream_t s);
