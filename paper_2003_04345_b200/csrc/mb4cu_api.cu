@@ -25,6 +25,8 @@ struct mb4cu_ctx {
     int nx = 0, ny = 0;
     size_t n = 0;
     double cx = 0, cy = 0, gamma = 0, eps = 0;
+    double vmax = 0;    // max |V| (host, at create)
+    double amax2 = 0;   // max |u|^2 of the last host-set state (stiffness estimate)
     int max_iters = 0, max_halvings = 0, m = 2, mf = 2, kernel = 0;
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
@@ -190,6 +192,18 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     }
     return fail(ctx, MB4CU_NONCONVERGED,
                 "stage iteration: no convergence after " + std::to_string(ctx->max_iters) + " sweeps");
+}
+
+// Stiffness of a (sub)step: kappa = h max|lambda| rho(J(u0)) with the Gershgorin
+// bound rho(J) <= 4cx + 4cy + max|V| + 3|gamma| max|u0|^2.  The m-term Neumann
+// sweep contracts by ~kappa^(m+1) and is the fast path only well below kappa = 1.
+constexpr double kStiffKappa = 0.5;
+
+bool stiff_step(const mb4cu_ctx* ctx, double h) {
+    const double lam = std::max({std::fabs(ctx->scheme.lam[0]), std::fabs(ctx->scheme.lam[1]),
+                                 std::fabs(ctx->scheme.lam[2])});
+    const double rho = 4.0 * ctx->cx + 4.0 * ctx->cy + ctx->vmax + 3.0 * std::fabs(ctx->gamma) * ctx->amax2;
+    return h * lam * rho > kStiffKappa;
 }
 
 // ---- Newton-Krylov stage solver (kernel = 3) --------------------------------
@@ -368,6 +382,22 @@ int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
 // (newton_solve, mb4_integrator.cpp:194-255).  On success u0 <- U3 (c3 = 1).
 int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     if (ctx->kernel == 3) return substep_krylov(ctx, h, sweeps, last_res);
+    if (ctx->kernel == 0) {
+        // default policy: matrix-free sweeps unless the step is stiff; a sweep
+        // iteration that fails falls back to Newton-Krylov at the same step size
+        // (the reference would not halve there), then the halving policy applies.
+        if (stiff_step(ctx, h)) return substep_krylov(ctx, h, sweeps, last_res);
+        int sw = 0;
+        const int rc = substep_march(ctx, h, &sw, last_res);
+        if (rc != MB4CU_NONCONVERGED) {
+            *sweeps = sw;
+            return rc;
+        }
+        int it = 0;
+        const int rc2 = substep_krylov(ctx, h, &it, last_res);
+        *sweeps = sw + it;
+        return rc2;
+    }
     if (ctx->kernel != 1) return substep_march(ctx, h, sweeps, last_res);
     const SweepConsts c = make_consts(ctx, h);
     int cur = -1;
@@ -511,6 +541,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->pitch = p->nx + 2 * p->ghost;
     ctx->alloc_n = static_cast<size_t>(ctx->pitch) * (p->ny + 2 * p->ghost);
     ctx->scheme = *scheme;
+    for (size_t k = 0; k < ctx->n; ++k) ctx->vmax = std::max(ctx->vmax, std::fabs(p->V[k]));
 
     auto bail = [&](cudaError_t e, const char* where) {
         g_create_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -628,6 +659,9 @@ int mb4cu_set_state(mb4cu_ctx* ctx, const double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyHostToDevice));
+    double a2 = 0.0;  // amplitude for the stiffness estimate, while the copy runs
+    for (size_t k = 0; k < ctx->n; ++k) a2 = std::max(a2, u[2 * k] * u[2 * k] + u[2 * k + 1] * u[2 * k + 1]);
+    ctx->amax2 = a2;
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->obs_cached = false;
     return MB4CU_OK;
@@ -794,7 +828,7 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     mb4cu_obs o{};
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
-    const bool fused = ctx->kernel == 0 || ctx->kernel == 2;
+    const bool fused = (ctx->kernel == 0 && !stiff_step(ctx, h)) || ctx->kernel == 2;
     for (int s = 1; s <= nsteps; ++s) {
         if (obs_series && !fused) {
             const int rc0 = mb4cu_observables(ctx, &o);

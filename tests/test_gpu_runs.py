@@ -139,7 +139,11 @@ def test_halving_path_is_deterministic_and_matches_oracle():
     out = []
     for _ in range(2):
         st = nls2d.StepStats()
-        out.append(nls2d.mb4_step(model, nls2d.Mb4Scheme(), u0, 0.05, cfg, stats=st))
+        # sweep-only solver (kernel 1): too stiff for 12 sweeps at h = 0.05 -> halves
+        with nls2d.Session(model, nls2d.Mb4Scheme(), cfg, kernel=1) as s:
+            s.set_state(u0)
+            s.step(0.05, st)
+            out.append(s.get_state())
     assert np.array_equal(out[0], out[1])
     assert st.halvings >= 1
     o = O.Oracle(6, 6, 0.1, np.zeros(36), cx=model.cx, cy=model.cy)
@@ -148,6 +152,14 @@ def test_halving_path_is_deterministic_and_matches_oracle():
         rc, u, _, _, _ = o.step(u, 0.05 / 2 ** st.halvings, eps=1e-13, max_halvings=0)
         assert rc == 0
     assert rel(out[0], u) <= 1e-10
+    # the default policy detects the stiff step and solves it at full size, like the
+    # reference (Newton-Krylov), without halving
+    st = nls2d.StepStats()
+    u1 = nls2d.mb4_step(model, nls2d.Mb4Scheme(), u0, 0.05, cfg, stats=st)
+    assert st.halvings == 0
+    rc, uref, _, hv, _ = o.step(u0, 0.05, eps=1e-13)
+    assert rc == 0 and hv == 0
+    assert rel(u1, uref) <= 1e-10
 
 
 def test_single_mode_phase_rotation_fifth_order():
