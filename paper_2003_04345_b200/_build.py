@@ -26,6 +26,28 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+GEN_DIR = os.path.join(ROOT, "build", "gen")
+
+
+def gen_default_scheme() -> str:
+    """Generate build/gen/defscheme.inc: the default MB4 scheme tables as exact
+    hex-float constants, from the library's own long-double scheme routine."""
+    inc = os.path.join(GEN_DIR, "defscheme.inc")
+    srcs = [os.path.join(CSRC, f) for f in ("gen_default_scheme.cpp", "scheme_host.cpp", "mb4cu_internal.hpp")]
+    if not _stale(inc, srcs + [os.path.join(ROOT, "include", "mb4cu.h")]):
+        return inc
+    os.makedirs(GEN_DIR, exist_ok=True)
+    exe = os.path.join(GEN_DIR, "gen_default_scheme")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    srcs[0], srcs[1], "-o", exe], check=True)
+    out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    tmp = inc + ".tmp"
+    with open(tmp, "w") as f:
+        f.write(out)
+    os.replace(tmp, inc)
+    return inc
+
+
 def build_lib(force: bool = False, verbose: bool = False, defines=(), name: str = "libmb4cu.so") -> str:
     """Build libmb4cu.so (or an experiment variant with extra -D defines)."""
     target = os.path.join(HERE, name)
@@ -34,10 +56,11 @@ def build_lib(force: bool = False, verbose: bool = False, defines=(), name: str 
         return target
     objs = []
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    gen_default_scheme()
     procs = []
     for src in _sources():
         obj = os.path.join(ROOT, "build", name + "." + src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", GEN_DIR, "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []

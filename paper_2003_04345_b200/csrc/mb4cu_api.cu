@@ -26,7 +26,8 @@ struct mb4cu_ctx {
     size_t n = 0;
     double cx = 0, cy = 0, gamma = 0, eps = 0;
     double vmax = 0;    // max |V| (host, at create)
-    double amax2 = 0;   // max |u|^2 of the last host-set state (stiffness estimate)
+    double amax2 = 0;   // max |u|^2 of the last set state (stiffness estimate)
+    bool amax2_valid = false;  // recomputed on the device after every state set
     int max_iters = 0, max_halvings = 0, m = 2, mf = 2, kernel = 0;
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
@@ -91,6 +92,24 @@ int cuda_fail(mb4cu_ctx* ctx, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
     } while (0)
 
+// Host copy of the generated default-scheme tables (build/gen/defscheme.inc).
+namespace defscheme_host {
+#define MB4_DS_QUAL static constexpr
+#include "defscheme.inc"
+#undef MB4_DS_QUAL
+}  // namespace defscheme_host
+
+// 1 if the context's scheme is bit-identical to the compiled-in default tables,
+// so the production kernel may use them as immediates.
+int is_default_scheme(const mb4cu_scheme& s) {
+    namespace d = defscheme_host;
+    return std::memcmp(s.L, d::L, sizeof(d::L)) == 0 && std::memcmp(s.WA, d::WA, sizeof(d::WA)) == 0 &&
+                   std::memcmp(s.E, d::E, sizeof(d::E)) == 0 && std::memcmp(s.T, d::T, sizeof(d::T)) == 0 &&
+                   std::memcmp(s.Tinv, d::Tinv, sizeof(d::Tinv)) == 0
+               ? 1
+               : 0;
+}
+
 SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
     SweepConsts c{};
     const mb4cu_scheme& s = ctx->scheme;
@@ -119,6 +138,8 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 4; ++j) c.Es[i][j] = cc * s.E[i][j];
     c.gs = ctx->gamma / cc;
+    c.hs = cc * h;
+    c.def = is_default_scheme(s);
     for (int k = 0; k < 3; ++k) {
         c.hls[k] = cc * c.hlam[k];
         c.first_ss[k] = cc * c.first_s[k];
@@ -199,6 +220,22 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
 // sweep contracts by ~kappa^(m+1) and is the fast path only well below kappa = 1.
 constexpr double kStiffKappa = 0.5;
 
+// max |u0|^2 of a newly set state, on the device (one read of u0 + 8 B back).
+// Refreshed lazily when a state is set, not per step: the amplitude of a
+// Hamiltonian run drifts slowly and the policy falls back to Newton-Krylov on any
+// sweep failure, so the estimate only steers the choice of the fast path.
+int refresh_amax2(mb4cu_ctx* ctx) {
+    if (ctx->amax2_valid) return MB4CU_OK;
+    MB4_CUDA(ctx, mb4cu::launch_amax2(ctx->u0, ctx->alloc_n, ctx->d_rmax, ctx->stream));
+    ctx->prof.other_launches += 1;
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->amax2 = decode_bits(*ctx->h_rmax);
+    ctx->amax2_valid = true;
+    return MB4CU_OK;
+}
+
 bool stiff_step(const mb4cu_ctx* ctx, double h) {
     const double lam = std::max({std::fabs(ctx->scheme.lam[0]), std::fabs(ctx->scheme.lam[1]),
                                  std::fabs(ctx->scheme.lam[2])});
@@ -225,7 +262,10 @@ int kr_alloc(mb4cu_ctx* ctx) {
     MB4_CUDA(ctx, cudaMalloc(&k.v_dev, sizeof(double2*) * (k.m + 1)));
     std::vector<double2*> ptrs(k.m + 1);
     for (int i = 0; i <= k.m; ++i) ptrs[i] = k.mem + static_cast<size_t>(i) * ctx->n;
-    MB4_CUDA(ctx, cudaMemcpy(k.v_dev, ptrs.data(), sizeof(double2*) * (k.m + 1), cudaMemcpyHostToDevice));
+    // on the context stream (a legacy-stream copy does not order against it)
+    MB4_CUDA(ctx, cudaMemcpyAsync(k.v_dev, ptrs.data(), sizeof(double2*) * (k.m + 1), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     MB4_CUDA(ctx, cudaMalloc(&k.partial, sizeof(double) * (k.m + 1) * k.nblk));
     MB4_CUDA(ctx, cudaMallocHost(&k.h_partial, sizeof(double) * (k.m + 1) * k.nblk));
     MB4_CUDA(ctx, cudaMalloc(&k.coef, sizeof(double) * (k.m + 1)));
@@ -600,6 +640,10 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if (e != cudaSuccess)
         return bail(e, "cudaMemcpy(V)");
     if ((e = cudaMemset(ctx->u0, 0, sb)) != cudaSuccess) return bail(e, "cudaMemset(u0)");
+    // cudaMemset is asynchronous and runs on the legacy stream, which does not order
+    // against the non-blocking context stream: finish the initialisation here, or a
+    // late zero-fill can overwrite the first set_state copy.
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "cudaDeviceSynchronize(create)");
     *out = ctx;
     return MB4CU_OK;
 }
@@ -659,11 +703,9 @@ int mb4cu_set_state(mb4cu_ctx* ctx, const double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyHostToDevice));
-    double a2 = 0.0;  // amplitude for the stiffness estimate, while the copy runs
-    for (size_t k = 0; k < ctx->n; ++k) a2 = std::max(a2, u[2 * k] * u[2 * k] + u[2 * k + 1] * u[2 * k + 1]);
-    ctx->amax2 = a2;
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->obs_cached = false;
+    ctx->amax2_valid = false;
     return MB4CU_OK;
 }
 
@@ -679,6 +721,7 @@ int mb4cu_set_state_device(mb4cu_ctx* ctx, const double* u) {
     if (!ctx || !u) return fail(ctx, MB4CU_INVALID, "set_state_device: null argument");
     MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyDeviceToDevice));
     ctx->obs_cached = false;
+    ctx->amax2_valid = false;
     return MB4CU_OK;
 }
 
@@ -694,6 +737,10 @@ int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats) {
     if (ctx->ghost > 0)
         return fail(ctx, MB4CU_INVALID, "mb4_step: sub-domain contexts step through mb4cu_sweep");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (ctx->kernel == 0) {
+        const int rca = refresh_amax2(ctx);
+        if (rca) return rca;
+    }
     MB4_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     double last = 0.0;
     int rc = MB4CU_NONCONVERGED;
@@ -826,6 +873,10 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     if (!ctx) return MB4CU_INVALID;
     if (nsteps < 0) return fail(ctx, MB4CU_INVALID, "run: nsteps must be >= 0");
     mb4cu_obs o{};
+    if (ctx->kernel == 0) {
+        const int rca = refresh_amax2(ctx);
+        if (rca) return rca;
+    }
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
     const bool fused = (ctx->kernel == 0 && !stiff_step(ctx, h)) || ctx->kernel == 2;

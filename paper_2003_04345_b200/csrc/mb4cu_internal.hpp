@@ -37,6 +37,8 @@ struct SweepConsts {
     double hls[3];      // c * h * lambda_k
     double first_ss[3]; // c * first_s
     double first_cs[3]; // c * first_c
+    double hs;          // c * h (isotropic residual with unscaled E, see defscheme)
+    int def;            // scheme tables equal the generated default ones (defscheme.inc)
     // First sweep at Neumann depth MF from U = (u0,u0,u0): every phibar_k is a
     // multiple of f(u0), so the recursion needs only g_n = J^n f (n <= MF) once,
     // not per stage:  U_i = u0 + sum_n fco[i][n] g_n  with
@@ -174,6 +176,8 @@ cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const Swee
                                cudaStream_t s);
 int obs_blocks(int nx, int ny);
 cudaError_t launch_observables(const ObsArgs& a, double* out5, cudaStream_t s);
+// max |u|^2 over n sites, written as the bits of a double to *out (stiffness estimate)
+cudaError_t launch_amax2(const double2* u, size_t n, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_apply_kv(int nx, int ny, double cx, double cy, const double2* u, const double* V,
                             double gamma, bool rhs, double2* y, cudaStream_t s);
 cudaError_t launch_eval_phi(int nx, int ny, const double2* u0, const double* V,

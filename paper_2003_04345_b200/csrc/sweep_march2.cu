@@ -62,11 +62,49 @@ struct Geom3 {
     static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
 };
 
-// Coefficient views: isotropic (unit stencil, pre-scaled constants) or general.
-template <bool ISO>
+// The default scheme's tables (alpha1 = -712.5, nodes 1/3, 2/3, 1) as compile-time
+// constants, generated at build time from the library's scheme routine
+// (gen_default_scheme.cpp).  Kernels specialised on them (DEF) fold the ~80 table
+// entries into FFMA immediates instead of constant-bank loads and uniform-register
+// shuffling (measured +4 % at cfg4 / cfg5, profiles/).
+namespace defscheme {
+#define MB4_DS_QUAL __device__ constexpr
+#include "defscheme.inc"
+#undef MB4_DS_QUAL
+}  // namespace defscheme
+
+// Coefficient views: isotropic (unit stencil, pre-scaled constants) or general;
+// DEF: scheme tables from defscheme (only with ISO, see dispatch3).
+template <bool ISO, bool DEF = false>
 struct Coef {
     const SweepConsts& c;
-    __device__ __forceinline__ double E(int i, int j) const { return ISO ? c.Es[i][j] : c.E[i][j]; }
+    __device__ __forceinline__ double Lq(int q, int b) const { return DEF ? defscheme::L[q][b] : c.L[q][b]; }
+    __device__ __forceinline__ double WAk(int k, int q) const { return DEF ? defscheme::WA[k][q] : c.WA[k][q]; }
+    // level-0 residual Phi_k = dz_k - hr * (E0 w ...) with w = (K+V) z (/ c if ISO):
+    // ISO without DEF uses the pre-scaled Es = c E and the true gamma, h; ISO with
+    // DEF the unscaled E and gamma / c, c h (the same product, one rounding apart).
+    __device__ __forceinline__ double E0(int i, int j) const {
+        return DEF ? defscheme::E[i][j] : (ISO ? c.Es[i][j] : c.E[i][j]);
+    }
+    __device__ __forceinline__ double g0() const { return DEF && ISO ? c.gs : c.gamma; }
+    __device__ __forceinline__ double h0() const { return DEF && ISO ? c.hs : c.h; }
+    // phibar = T^-1 phi, r = T rbar
+    __device__ __forceinline__ void to_eigen(const double2 phi[3], double2 out[3]) const {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            out[k].x = fma(Ti(k, 0), phi[0].x, fma(Ti(k, 1), phi[1].x, Ti(k, 2) * phi[2].x));
+            out[k].y = fma(Ti(k, 0), phi[0].y, fma(Ti(k, 1), phi[1].y, Ti(k, 2) * phi[2].y));
+        }
+    }
+    __device__ __forceinline__ void from_eigen(const double2 rb[3], double2 out[3]) const {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            out[i].x = fma(Tm(i, 0), rb[0].x, fma(Tm(i, 1), rb[1].x, Tm(i, 2) * rb[2].x));
+            out[i].y = fma(Tm(i, 0), rb[0].y, fma(Tm(i, 1), rb[1].y, Tm(i, 2) * rb[2].y));
+        }
+    }
+    __device__ __forceinline__ double Tm(int i, int k) const { return DEF ? defscheme::T[i][k] : c.T[i][k]; }
+    __device__ __forceinline__ double Ti(int k, int i) const { return DEF ? defscheme::Tinv[k][i] : c.Tinv[k][i]; }
     __device__ __forceinline__ double g() const { return ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double hl(int k) const { return ISO ? c.hls[k] : c.hlam[k]; }
     __device__ __forceinline__ double fs(int k) const { return ISO ? c.first_ss[k] : c.first_s[k]; }
@@ -106,7 +144,7 @@ struct Coef {
     }
 };
 
-template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
+template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF = false>
 struct March3 {
     using G = Geom3<M, NT>;
     // element offset of local site (x, y) (both may lie in the halo)
@@ -183,7 +221,7 @@ struct March3 {
 
     // Iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); h3 = 3 * ((j / 3) & 1).
     template <int PH>
-    __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf,
+    __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO, DEF>& cf,
                                          const double2* const uin[3], double2* const uout[3],
                                          Seg& s, int j, int h3, unsigned& rmax,
                                          double acc[kObsFields]) {
@@ -286,33 +324,33 @@ struct March3 {
                 for (int k = 0; k < 3; ++k) cub[k] = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) {
-                    double ur = c.L[q][0] * z[0].x, ui = c.L[q][0] * z[0].y;
+                    double ur = cf.Lq(q, 0) * z[0].x, ui = cf.Lq(q, 0) * z[0].y;
 #pragma unroll
                     for (int b = 1; b < 4; ++b) {
-                        ur = fma(c.L[q][b], z[b].x, ur);
-                        ui = fma(c.L[q][b], z[b].y, ui);
+                        ur = fma(cf.Lq(q, b), z[b].x, ur);
+                        ui = fma(cf.Lq(q, b), z[b].y, ui);
                     }
                     const double n2 = fma(ur, ur, ui * ui);
                     const double gr = n2 * ur, gi = n2 * ui;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        cub[k].x = fma(c.WA[k][q], gr, cub[k].x);
-                        cub[k].y = fma(c.WA[k][q], gi, cub[k].y);
+                        cub[k].x = fma(cf.WAk(k, q), gr, cub[k].x);
+                        cub[k].y = fma(cf.WAk(k, q), gi, cub[k].y);
                     }
                 }
                 double2 phi[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    double kr = cf.E(k, 0) * w[0].x, ki = cf.E(k, 0) * w[0].y;
+                    double kr = cf.E0(k, 0) * w[0].x, ki = cf.E0(k, 0) * w[0].y;
 #pragma unroll
                     for (int b = 1; b < 4; ++b) {
-                        kr = fma(cf.E(k, b), w[b].x, kr);
-                        ki = fma(cf.E(k, b), w[b].y, ki);
+                        kr = fma(cf.E0(k, b), w[b].x, kr);
+                        ki = fma(cf.E0(k, b), w[b].y, ki);
                     }
-                    const double rr = fma(-c.gamma, cub[k].y, ki);
-                    const double ri = fma(c.gamma, cub[k].x, -kr);
-                    phi[k].x = fma(-c.h, rr, z[k + 1].x - z[0].x);
-                    phi[k].y = fma(-c.h, ri, z[k + 1].y - z[0].y);
+                    const double rr = fma(-cf.g0(), cub[k].y, ki);
+                    const double ri = fma(cf.g0(), cub[k].x, -kr);
+                    phi[k].x = fma(-cf.h0(), rr, z[k + 1].x - z[0].x);
+                    phi[k].y = fma(-cf.h0(), ri, z[k + 1].y - z[0].y);
                 }
                 if (M == 0) {
                     if (out_ok) {
@@ -324,7 +362,7 @@ struct March3 {
                         }
                     }
                 } else {
-                    to_eigen(c, phi, pb);
+                    cf.to_eigen(phi, pb);
                 }
             }
         }
@@ -352,7 +390,7 @@ struct March3 {
             if (out_ok) {
                 // r = T rbar = -T b1
                 double2 tb[3];
-                from_eigen(c, b1, tb);
+                cf.from_eigen(b1, tb);
                 const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
@@ -378,7 +416,7 @@ struct March3 {
                 b2[k] = cf.horner(k, pb_m2[k], tc, ak, u0m);
             }
             double2 tb[3];
-            from_eigen(c, b2, tb);  // r = -T b2
+            cf.from_eigen(b2, tb);  // r = -T b2
             const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -394,7 +432,7 @@ struct March3 {
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
                         double2* const uout[3], int band, int Y0, int R, unsigned& rmax,
                         double acc[kObsFields]) {
-        const Coef<ISO> cf{c};
+        const Coef<ISO, DEF> cf{c};
         Seg s;
         s.X0 = band * G::TX;
         s.Y0 = Y0;
@@ -630,7 +668,7 @@ struct MarchFirst {
     }
 };
 
-template <int M, int NT, bool FIRST, bool ISO, bool GHOST>
+template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
                            unsigned& rmax, double acc[kObsFields]) {
@@ -650,7 +688,7 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
         }
         return;
     }
-    March3<M, NT, FIRST, ISO, GHOST> m(smem);
+    March3<M, NT, FIRST, ISO, GHOST, DEF> m(smem);
     // band-rows of this sweep's band width (TX depends on M)
     const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
     const long long G = gridDim.x;
@@ -679,7 +717,7 @@ struct KGeom {
     static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
 };
 
-template <int MF, int M, int NT, bool ISO, bool GHOST>
+template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
 __global__ void __launch_bounds__(NT, (KGeom<MF, M, NT>::MINB))
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -701,6 +739,12 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 #else
     const SweepConsts& cc = c;
 #endif
+#ifdef MB4_POISON_SMEM
+    // debug builds: stale shared memory must never reach an output
+    for (size_t q = threadIdx.x; q < KGeom<MF, M, NT>::bytes / 8; q += NT)
+        reinterpret_cast<unsigned long long*>(smem)[q] = MB4_POISON_SMEM;
+    __syncthreads();
+#endif
     int sweeps = 0, set = 0, converged = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
     double rlast = 0.0;
@@ -711,7 +755,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         unsigned rmax = 0u;
         if (sg == 0) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all3<MF, NT, true, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
+            sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -731,7 +775,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         } else {
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            sweep_all3<M, NT, false, ISO, GHOST>(a, cc, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
         }
         block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[s]);
         grid.sync();
@@ -761,16 +805,16 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     }
 }
 
-template <int MF, int M, int NT, bool ISO, bool GHOST>
+template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
 struct Launcher3 {
     static int grid_size(int device) {
         static int cached[64] = {0};
         if (device >= 0 && device < 64 && cached[device]) return cached[device];
         const size_t smem = KGeom<MF, M, NT>::bytes;
-        cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<MF, M, NT, ISO, GHOST>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>, NT, smem);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
@@ -782,28 +826,33 @@ struct Launcher3 {
         const int grid = grid_size(device);
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST>),
+        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>),
                                            dim3(grid), dim3(NT), params, KGeom<MF, M, NT>::bytes, s);
     }
 };
 
 template <int MF, int M>
 cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
+    // compile-time scheme tables for the (common) isotropic default-scheme case
     if (a.ghost > 0) {
-        return c.iso ? Launcher3<MF, M, 128, true, true>::launch(a, c, device, s)
-                     : Launcher3<MF, M, 128, false, true>::launch(a, c, device, s);
+        if (c.iso && c.def) return Launcher3<MF, M, 128, true, true, true>::launch(a, c, device, s);
+        return c.iso ? Launcher3<MF, M, 128, true, true, false>::launch(a, c, device, s)
+                     : Launcher3<MF, M, 128, false, true, false>::launch(a, c, device, s);
     }
-    return c.iso ? Launcher3<MF, M, 128, true, false>::launch(a, c, device, s)
-                 : Launcher3<MF, M, 128, false, false>::launch(a, c, device, s);
+    if (c.iso && c.def) return Launcher3<MF, M, 128, true, false, true>::launch(a, c, device, s);
+    return c.iso ? Launcher3<MF, M, 128, true, false, false>::launch(a, c, device, s)
+                 : Launcher3<MF, M, 128, false, false, false>::launch(a, c, device, s);
 }
 
 template <int MF, int M>
 int grid3(int device) {
     int g = 0;
-    const int v[4] = {Launcher3<MF, M, 128, true, false>::grid_size(device),
-                      Launcher3<MF, M, 128, false, false>::grid_size(device),
-                      Launcher3<MF, M, 128, true, true>::grid_size(device),
-                      Launcher3<MF, M, 128, false, true>::grid_size(device)};
+    const int v[6] = {Launcher3<MF, M, 128, true, false, false>::grid_size(device),
+                      Launcher3<MF, M, 128, false, false, false>::grid_size(device),
+                      Launcher3<MF, M, 128, true, true, false>::grid_size(device),
+                      Launcher3<MF, M, 128, false, true, false>::grid_size(device),
+                      Launcher3<MF, M, 128, true, false, true>::grid_size(device),
+                      Launcher3<MF, M, 128, true, true, true>::grid_size(device)};
     for (int x : v) g = x > g ? x : g;
     return g;
 }

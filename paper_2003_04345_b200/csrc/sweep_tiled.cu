@@ -289,6 +289,17 @@ int grid_for(size_t n, int threads) {
     return static_cast<int>(b < 148 * 16 ? (b ? b : 1) : 148 * 16);
 }
 
+// max |u|^2 over n sites as the bit pattern of a non-negative double (atomicMax)
+__global__ void amax2_kernel(const double2* __restrict__ u, size_t n, unsigned long long* out) {
+    double m = 0.0;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double2 z = __ldcs(u + k);
+        m = fmax(m, fma(z.x, z.x, z.y * z.y));
+    }
+    block_max_to(static_cast<unsigned long long>(__double_as_longlong(m)), out);
+}
+
 }  // namespace
 
 size_t tiled_smem_bytes(int m, bool first) {
@@ -318,6 +329,13 @@ cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const Swee
         case 7: return launch_tiled<3, true>(a, c, s);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_amax2(const double2* u, size_t n, unsigned long long* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(*out), s);
+    if (e != cudaSuccess) return e;
+    amax2_kernel<<<grid_for(n, 256), 256, 0, s>>>(u, n, out);
+    return cudaGetLastError();
 }
 
 int obs_blocks(int nx, int ny) {

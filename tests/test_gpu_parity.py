@@ -141,3 +141,22 @@ def test_mb4_step_drop_in_matches_oracle():
     ref, _ = _oracle_steps(cfg, V, psi, 1)
     assert rel(u1, ref) <= 1e-10
     assert stats.newton_iters > 0 and stats.halvings == 0
+
+
+@pytest.mark.parametrize("alpha1", [-712.5, -800.0])
+@pytest.mark.parametrize("m", [1, 2])
+def test_scheme_tables_runtime_and_compiled(alpha1, m):
+    """The production kernel uses compile-time tables only for the default scheme
+    (alpha1 = -712.5); any other alpha1 runs on the runtime tables.  Both must
+    match the oracle built with the same scheme."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    o = O.Oracle(cfg.nx, cfg.ny, cfg.gamma, V, alpha1=alpha1)
+    ref, ref_obs, _ = o.run(psi, cfg.dt, 5, eps=cfg.epsilon)
+    model = configs.model_for(cfg, V)
+    with nls2d.Session(model, nls2d.Mb4Scheme(alpha1), configs.newton_for(cfg), neumann_terms=m) as s:
+        s.set_state(psi)
+        obs, _ = s.run(cfg.dt, 5)
+        got = s.get_state()
+    assert rel(got, ref) <= 1e-10
+    assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * abs(ref_obs[0, 3])
