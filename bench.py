@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--neumann", type=int, default=-1)
+    ap.add_argument("--neumann-first", type=int, default=-1)
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -256,6 +257,7 @@ def run_ours(args, d: Dist):
     model = configs.model_for(cfg, V)
     sess = nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg),
                          neumann_terms=None if args.neumann < 0 else args.neumann,
+                         neumann_first=None if args.neumann_first < 0 else args.neumann_first,
                          device=d.local, kernel=args.kernel)
     sess.set_state(psi)
     obs0 = sess.observables()

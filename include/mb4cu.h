@@ -77,7 +77,8 @@ typedef struct {
     double epsilon;           /* stop when ||r||_inf <= epsilon (split reals)          */
     int max_iters;            /* cap on stage sweeps per (sub)step                      */
     int max_step_halvings;    /* halving-on-failure policy (mb4_integrator.cpp:287-315) */
-    int neumann_terms;        /* m in 0..3: preconditioner sum_{k<=m} (h lam J)^k; -1 = default */
+    int neumann_terms;        /* m in 0..3: preconditioner sum_{k<=m} (h lam J)^k; -1 = default
+                                 (kernel 0: adaptive 1/2 from the sweep counts; else 1)    */
     int device;               /* CUDA device ordinal                                    */
     int kernel;               /* stage solver: 0 = default (persistent matrix-free sweeps),
                                  1 = tiled sweep kernel, 2 = march v1, 3 = Newton-Krylov
@@ -89,8 +90,10 @@ typedef struct {
                                  mb4cu_halo_pack / _unpack, and steps are driven sweep by
                                  sweep (mb4cu_sweep / mb4cu_commit_step).                 */
     int neumann_first;        /* Neumann depth of the FIRST sweep of a step (its Phi is the
-                                 cheap closed form); -1 = default (2).  Must equal
-                                 neumann_terms or be 2.                                    */
+                                 cheap closed form, so the recursion is one J-chain);
+                                 -1 = default (kernel 0: 6; sub-domain mode / tiled: 2).
+                                 Kernel 0 pairs (first, terms): (0,0) (1,1) (2,0..2)
+                                 (3,1) (4,1..2) (6,0..2); tiled: equal or (2, <=2).     */
 } mb4cu_problem;
 
 typedef struct {

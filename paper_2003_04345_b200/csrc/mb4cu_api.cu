@@ -29,6 +29,8 @@ struct mb4cu_ctx {
     double amax2 = 0;   // max |u|^2 of the last set state (stiffness estimate)
     bool amax2_valid = false;  // recomputed on the device after every state set
     int max_iters = 0, max_halvings = 0, m = 2, mf = 2, kernel = 0;
+    bool m_auto = false;  // neumann_terms = -1 on the production kernel: m adapts in {1, 2}
+    int auto_steps = 0;
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
     mb4cu_scheme scheme{};
@@ -71,8 +73,25 @@ struct mb4cu_ctx {
 namespace {
 
 // Default Neumann depth m of the stage preconditioner (fastest measured on B200 at
-// the BASELINE sizes, profiles/).
+// the BASELINE sizes, profiles/); on the production kernel m adapts between 1 and 2
+// (adapt_neumann), and the first sweep of a step runs at depth kDefaultFirst.
 constexpr int kDefaultNeumann = 1;
+constexpr int kDefaultFirst = 6;
+
+// Adaptive m (production kernel, neumann_terms = -1).  A later sweep at m = 2 costs
+// ~1.28x one at m = 1 and contracts ~1.5x as much (kappa^3 vs kappa^2), so m = 2
+// pays once a step needs >= 3 later sweeps at m = 1; it is re-probed every 64 steps.
+// The choice depends only on sweep counts: reruns stay bit-identical.
+void adapt_neumann(mb4cu_ctx* ctx, int sweeps) {
+    if (!ctx->m_auto) return;
+    if (ctx->m == 1 && sweeps >= 4) {
+        ctx->m = 2;
+        ctx->auto_steps = 0;
+    } else if (ctx->m == 2 && ++ctx->auto_steps >= 64) {
+        ctx->m = 1;
+        ctx->auto_steps = 0;
+    }
+}
 
 thread_local std::string g_create_error;
 
@@ -146,7 +165,7 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         c.first_cs[k] = cc * c.first_c[k];
     }
     for (int i = 0; i < 3; ++i)
-        for (int n = 0; n < 4; ++n) {
+        for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) {
             double acc = 0.0;
             for (int k = 0; k < 3; ++k) acc += s.T[i][k] * c.first_s[k] * std::pow(c.hlam[k], n);
             c.fco[i][n] = -acc * (c.iso ? std::pow(cc, n + 1) : 1.0);
@@ -209,6 +228,7 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     if (st.converged) {
         std::swap(ctx->u0, ctx->U[st.set][2]);
         ctx->obs_cached = false;
+        adapt_neumann(ctx, st.sweeps);
         return MB4CU_OK;
     }
     return fail(ctx, MB4CU_NONCONVERGED,
@@ -564,17 +584,28 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         delete ctx;
         return MB4CU_INVALID;
     }
-    // first-sweep depth: default 2 on the production kernel (v1 march: same as m)
-    ctx->mf = p->neumann_first >= 0 ? p->neumann_first : (p->kernel == 2 || m > 2 ? m : 2);
+    // first-sweep depth: default kDefaultFirst on the production kernel (2 in
+    // sub-domain mode, 2 on the tiled kernel; v1 march: same as m)
+    ctx->m_auto = p->neumann_terms < 0 && p->kernel == 0 && p->ghost == 0;
+    if (p->neumann_first >= 0)
+        ctx->mf = p->neumann_first;
+    else if (p->kernel == 0 && p->ghost == 0 && mb4cu::march2_supported(kDefaultFirst, m))
+        ctx->mf = kDefaultFirst;
+    else
+        ctx->mf = p->kernel == 2 || m > 2 ? m : 2;
     if (p->kernel == 2) ctx->mf = m;
-    if (ctx->mf != m && !(ctx->mf == 2 && m <= 2)) {
-        g_create_error = "mb4cu_create: neumann_first must equal neumann_terms or be 2";
+    if (ctx->m_auto && !mb4cu::march2_supported(ctx->mf, 2)) ctx->m_auto = false;
+    if (ctx->mf != m && !(p->kernel == 0 && mb4cu::march2_supported(ctx->mf, m)) &&
+        !(p->kernel != 2 && ctx->mf == 2 && m <= 2)) {
+        g_create_error = "mb4cu_create: unsupported (neumann_first, neumann_terms) pair for this kernel";
         delete ctx;
         return MB4CU_INVALID;
     }
     const int mmax = ctx->mf > m ? ctx->mf : m;
-    if (p->ghost < 0 || (p->ghost > 0 && (p->ghost < mmax + 1 || m > 2 || p->kernel != 0))) {
-        g_create_error = "mb4cu_create: sub-domain mode needs ghost >= neumann_terms + 1, m <= 2, kernel 0";
+    if (p->ghost < 0 || (p->ghost > 0 && (p->ghost < mmax + 1 || m > 2 || p->kernel != 0 ||
+                                          p->ghost > p->nx || p->ghost > p->ny))) {
+        g_create_error = "mb4cu_create: sub-domain mode needs neumann_first + 1 <= ghost <= block size, "
+                         "neumann_terms + 1 <= ghost, m <= 2, kernel 0";
         delete ctx;
         return MB4CU_INVALID;
     }
@@ -610,10 +641,11 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return bail(e, "cudaEventCreate");
     if (ctx->kernel != 1) {
-        const int grid = std::max(mb4cu::march_grid_size(ctx->m, ctx->device),
-                                  mb4cu::march2_supported(ctx->mf, ctx->m)
-                                      ? mb4cu::march2_grid_size(ctx->mf, ctx->m, ctx->device)
-                                      : 0);
+        int grid = std::max(mb4cu::march_grid_size(ctx->m, ctx->device),
+                            mb4cu::march2_supported(ctx->mf, ctx->m)
+                                ? mb4cu::march2_grid_size(ctx->mf, ctx->m, ctx->device)
+                                : 0);
+        if (ctx->m_auto) grid = std::max(grid, mb4cu::march2_grid_size(ctx->mf, 2, ctx->device));
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
         if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * ctx->max_iters)) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
@@ -914,9 +946,15 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
 
 namespace {
 
+// Halo width of a field: u0 and V feed the first sweep (depth mf -> mf + 1 layers);
+// the stage sets only the later sweeps (m + 1 layers).
+int halo_width(const mb4cu_ctx* ctx, int field) {
+    return field <= 1 ? ctx->ghost : std::min(ctx->ghost, ctx->m + 1);
+}
+
 // rectangle (x0, y0, w, h) of a halo side; pack == owned strip, unpack == ghost strip
-void halo_rect(const mb4cu_ctx* ctx, int side, bool pack, int* x0, int* y0, int* w, int* h) {
-    const int g = ctx->ghost, nx = ctx->nx, ny = ctx->ny;
+void halo_rect(const mb4cu_ctx* ctx, int field, int side, bool pack, int* x0, int* y0, int* w, int* h) {
+    const int g = halo_width(ctx, field), nx = ctx->nx, ny = ctx->ny;
     switch (side) {
         case 0: *x0 = pack ? 0 : -g; *y0 = 0; *w = g; *h = ny; break;            // west
         case 1: *x0 = pack ? nx - g : nx; *y0 = 0; *w = g; *h = ny; break;       // east
@@ -929,7 +967,7 @@ int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
     if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3 || !buf)
         return fail(ctx, MB4CU_INVALID, "halo: bad context / field / side / buffer");
     int x0, y0, w, h;
-    halo_rect(ctx, side, pack, &x0, &y0, &w, &h);
+    halo_rect(ctx, field, side, pack, &x0, &y0, &w, &h);
     if (field == 1) {
         MB4_CUDA(ctx, mb4cu::launch_halo_copy1(ctx->V, ctx->pitch, ctx->ghost, x0, y0, w, h, buf, pack, ctx->stream));
     } else {
@@ -952,7 +990,7 @@ int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
 size_t mb4cu_halo_count(const mb4cu_ctx* ctx, int field, int side) {
     if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3) return 0;
     int x0, y0, w, h;
-    halo_rect(ctx, side, true, &x0, &y0, &w, &h);
+    halo_rect(ctx, field, side, true, &x0, &y0, &w, &h);
     const size_t sites = static_cast<size_t>(w) * h;
     return field == 1 ? sites : (field == 0 ? 2 * sites : 6 * sites);
 }

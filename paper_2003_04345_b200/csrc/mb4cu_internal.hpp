@@ -19,6 +19,9 @@ int scale_state(double* psi, size_t nsites, double s, int threads);
 
 // Per-sweep constants, passed by value as a __grid_constant__ kernel parameter
 // (lives in the constant bank; no per-context __constant__ symbol juggling).
+// deepest first sweep of the production kernel (MarchFirst, sweep_march2.cu)
+constexpr int kMaxNeumannFirst = 6;
+
 struct SweepConsts {
     double E[3][4];     // combos c_i = sum_j E[i][j] z_j
     double L[6][4];     // U_q = sum_a L[q][a] z_a
@@ -44,7 +47,7 @@ struct SweepConsts {
     // not per stage:  U_i = u0 + sum_n fco[i][n] g_n  with
     //   fco[i][n] = -sum_k T[i][k] first_s[k] (h lam_k)^n
     // (in isotropic units -- f and J evaluated with the unit stencil -- times c^(n+1)).
-    double fco[3][4];
+    double fco[3][kMaxNeumannFirst + 1];
     double h;
     double gamma;
     double cx, cy, diag;  // stencil: diag = 2cx + 2cy

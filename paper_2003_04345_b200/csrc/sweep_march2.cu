@@ -486,35 +486,70 @@ struct March3 {
 };
 
 // First sweep of a step at Neumann depth MF >= 1, specialised.  From U = (u0,u0,u0)
-// every phibar_k = first_s[k] f(u0), so the M-term recursion of all three stages
-// reduces to the chain g_0 = f, g_n = J g_{n-1} (one complex per site and level
-// instead of three) and U_i = u0 + sum_n fco[i][n] g_n.  Same band march, ring
-// and publish-row scheme as March3 (level n at row i - n, one barrier per row).
+// every phibar_k = first_s[k] f(u0), so the MF-term recursion of all three stages
+// reduces to ONE chain g_0 = f, g_n = J g_{n-1} (one complex per site and level
+// instead of three) and U_i = u0 + sum_n fco[i][n] g_n.  The chain is cheap, so the
+// first sweep runs deep (default MF = 6): on the nearly linear stage systems of the
+// BASELINE configs it leaves only the nonlinear remainder for the later sweeps
+// (cfg5: 4 -> 2 sweeps per step, profiles/).
+//
+// Same band march as March3: level n works on row i - n at iteration j (i = j - 2),
+// one barrier per row.  Level n-1 publishes its row into a ring of own-column
+// history (depth D_n) from which level n reads the centre row's left/right
+// neighbours (previous iteration) and its own column two rows back; the output row
+// i - MF reads the older chain values g_n(i - MF), n <= MF - 3, from the same rings.
 template <int MF, int NT, bool ISO, bool GHOST>
 struct MarchFirst {
-    static_assert(MF >= 1 && MF <= 2, "first-sweep depth 1..2");
-    using G = Geom3<MF, NT>;
-    static constexpr int ZW = G::ZW;
-    static constexpr int S = 12;  // light rows: prefetch deeper (P = 8 / 10 rows) to cover HBM latency
-    static constexpr int BACK = MF == 2 ? 3 : 1;
-    static constexpr int P = S - 1 - BACK;
+    static_assert(MF >= 1 && MF <= kMaxNeumannFirst, "first-sweep depth");
+    static constexpr int TX = NT - 2 * MF;  // output columns per band
+    static constexpr int ZW = NT + 2;
+    // z rows kept behind the newest: levels n >= 2 read u0 / V of row i - n from the ring
+    static constexpr int BACK = MF >= 2 ? MF + 1 : 1;
+    // rows in flight: light rows, prefetch deep to cover HBM latency (smem-bounded)
+    static constexpr int P = MF <= 2 ? 10 - (MF == 2 ? 2 : 0) : 8;
+    static constexpr int S = P + 1 + BACK;
+    // history depth of level n: the output reads g_n(i - MF), written MF - n iterations ago
+    __host__ __device__ static constexpr int depth(int n) { return n >= MF - 2 ? 2 : MF - n + 1; }
+    __host__ __device__ static constexpr int base(int n) { return n == 0 ? 0 : base(n - 1) + depth(n - 1); }
+    static constexpr int HROWS = base(MF);
     static constexpr size_t zu0_bytes = sizeof(double2) * S * ZW;
     static constexpr size_t zv_bytes = ((sizeof(double) * S * ZW + 15) / 16) * 16;
-    static constexpr size_t bytes = zu0_bytes + zv_bytes + sizeof(double2) * MF * 2 * ZW;
-    static_assert(bytes <= Geom3<MF, NT>::bytes, "fits the kernel's dynamic smem");
+    static constexpr size_t bytes = zu0_bytes + zv_bytes + sizeof(double2) * HROWS * ZW;
 
     double2* zu0;
     double* zv;
-    double2* pub;  // [MF][2][ZW]
+    double2* hist;  // [HROWS][ZW]
     double2 zw[3];
     double vw[3];
+    // own-column g_n of the last two iterations, slot = iteration parity (static
+    // after the unroll by 2): the centre and down values of level n + 1 come from
+    // registers, only the left/right neighbours from shared memory
+    double2 gp[MF][2];
+    // ring positions of iteration j, advanced incrementally (no integer division):
+    // zs = j mod S, hs[n] = j mod depth(n) for the deep-history levels n <= MF - 3
+    int zs;
+    int hs[MF > 3 ? MF - 2 : 1];
+    __device__ __forceinline__ int zslot(int back) const {  // z ring slot of z row j - back
+        const int x = zs - back;
+        return x < 0 ? x + S : x;
+    }
 
     __device__ MarchFirst(unsigned char* smem) {
         zu0 = reinterpret_cast<double2*>(smem);
         zv = reinterpret_cast<double*>(smem + zu0_bytes);
-        pub = reinterpret_cast<double2*>(smem + zu0_bytes + zv_bytes);
+        hist = reinterpret_cast<double2*>(smem + zu0_bytes + zv_bytes);
     }
-    __device__ __forceinline__ double2* pub_row(int level, int parity) { return pub + (level * 2 + parity) * ZW; }
+    // own-column g_N(i - MF) for N <= MF - 3, written at iteration j - MF + N
+    template <int N>
+    __device__ __forceinline__ void gather(double2* gout) {
+        if constexpr (N + 3 <= MF) {
+            // slot (j - (MF - N)) mod D = (j + 1) mod D, as D = MF - N + 1
+            constexpr int D = depth(N);
+            const int sl = hs[N] + 1 == D ? 0 : hs[N] + 1;
+            gout[N] = hist[(base(N) + sl) * ZW + threadIdx.x + 1];
+            gather<N + 1>(gout);
+        }
+    }
     __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
         if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
         return static_cast<size_t>(y) * a.nx + x;
@@ -549,27 +584,59 @@ struct MarchFirst {
         cp_async_commit();
     }
 
+    struct Chain {
+        double2 up;   // g_{n-1}(i - n + 1), computed this iteration
+        double2 low;  // g_{MF-2}(i - MF)
+        double2 mid;  // g_{MF-1}(i - MF)
+    };
+
+    // level N (compile-time recursion: every ring offset and slot depth is static)
+    template <int N, int PAR>
+    __device__ __forceinline__ void levels(const Coef<ISO>& cf, int j, Chain& ch) {
+        if constexpr (N <= MF) {
+            constexpr int D = depth(N - 1);
+            const int cc = threadIdx.x + 1;
+            int s_own = PAR, s_prev = PAR ^ 1;  // depth 2: slot = iteration parity
+            if constexpr (D != 2) {
+                s_own = hs[N - 1];
+                s_prev = s_own == 0 ? D - 1 : s_own - 1;
+            }
+            const double2* crow = hist + (base(N - 1) + s_prev) * ZW;  // iteration j - 1
+            double2* own = hist + (base(N - 1) + s_own) * ZW;          // iteration j
+            const double2 gc = gp[N - 1][PAR ^ 1];                       // iteration j - 1
+            const double2 gd = gp[N - 1][PAR];                           // iteration j - 2
+            const int zrow = zslot(N + 1);                               // z row of i - N
+            const double2 u0n = N == 1 ? zw[2] : zu0[zrow * ZW + cc];
+            const double vn = N == 1 ? vw[2] : zv[zrow * ZW + cc];
+            const double2 an = cf.kv(cf.dv(vn), gc, crow[cc - 1], crow[cc + 1], gd, ch.up);
+            const double2 gn = cf.jt(gc, an, u0n);
+            own[cc] = ch.up;  // publish g_{N-1}(i - N + 1) for the neighbours / the output
+            gp[N - 1][PAR] = ch.up;
+            if (N == MF - 1) ch.low = gd;
+            if (N == MF) ch.mid = gc;
+            ch.up = gn;
+            levels<N + 1, PAR>(cf, j, ch);
+        }
+    }
+
+    // j >= 0; iterations before a level's first valid row compute on stale rows and
+    // are masked (out_ok / the monitor window), as in March3.
+    template <int PAR>  // = j & 1
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3],
                                          Seg& s, int j, unsigned& rmax, double acc[kObsFields]) {
         const SweepConsts& c = cf.c;
         const int t = threadIdx.x, cc = t + 1, i = j - 2;
-        auto ring = [&](int k) { return ((j - k) % S + S) % S; };
-        const int slot_new = ring(0), slot_cen = ring(1);
+        const int slot_new = zs, slot_cen = zslot(1);
         cp_async_wait<P - 1>();
         __syncthreads();
-        issue_row(a, s, j + P, ring(-P));
+        issue_row(a, s, j + P, zs + P >= S ? zs + P - S : zs + P);
 
         const int yrel = i - 2 * MF;
         const int xout = s.X0 - MF + t;
         const bool out_ok = yrel >= 0 && yrel < s.R && t >= MF && t < NT - MF && xout < a.nx;
-        const int par = j & 1, ppar = par ^ 1;
 
         zw[0] = zu0[slot_new * ZW + cc];  // window: [0] new (z row j), [1] centre, [2] down
         vw[0] = zv[slot_new * ZW + cc];
-
-        // own-column history, read before this iteration republishes the rows
-        const double2 f_m2 = MF == 2 ? pub_row(0, par)[cc] : make_double2(0.0, 0.0);   // f(i-2)
-        const double2 g1_m3 = MF == 2 ? pub_row(1, par)[cc] : make_double2(0.0, 0.0);  // g1(i-3)
 
         // ---- level 0 at row i: f(u0) and the energy monitor --------------------
         const double v = vw[1];
@@ -590,59 +657,49 @@ struct MarchFirst {
             acc[4] += vn;
         }
 
-        // ---- level 1 at row i-1: g1 = J f ---------------------------------------
-        const double2* f_row = pub_row(0, ppar);  // f(i-1), published last iteration
-        const double2 f_c = f_row[cc];
-        const double2 f_dn = MF == 2 ? f_m2 : pub_row(0, par)[cc];  // f(i-2)
-        const double2 u0m = zw[2];                                   // u0(i-1)
-        const double2 a1 = cf.kv(cf.dv(vw[2]), f_c, f_row[cc - 1], f_row[cc + 1], f_dn, f);
-        const double2 g1 = cf.jt(f_c, a1, u0m);
-        pub_row(0, par)[cc] = f;  // publish f(i)
+        // ---- levels 1..MF: g_n at row i - n from g_{n-1} rows i-n-1, i-n, i-n+1 ----
+        Chain ch{f, f, f};
+        levels<1, PAR>(cf, j, ch);
+        const double2 up = ch.up;
+        const double2 g_low = ch.low, g_mid = ch.mid;
 
-        if (MF == 1) {
-            if (out_ok) {
-                const size_t gi = at(a, xout, s.Y0 + yrel);
+        if (out_ok) {
+            // g_n(i - MF): n <= MF - 3 from the history rings, MF - 2 / MF - 1 / MF in registers
+            double2 gout[MF + 1];
+            gather<0>(gout);
+            if (MF >= 2) gout[MF - 2] = g_low;
+            gout[MF - 1] = g_mid;
+            gout[MF] = up;
+            const int slot_o = zslot(MF + 1);  // z row of output row i - MF
+            const double2 u0o = MF == 1 ? zw[2] : zu0[slot_o * ZW + cc];
+            const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const double2 r = make_double2(fma(c.fco[q][0], f_c.x, c.fco[q][1] * g1.x),
-                                                   fma(c.fco[q][0], f_c.y, c.fco[q][1] * g1.y));
-                    uout[q][gi] = make_double2(u0m.x + r.x, u0m.y + r.y);
-                    March3<MF, NT, true, ISO, GHOST>::track(rmax, r);
-                }
-            }
-        } else {
-            // ---- level 2 at row i-2: g2 = J g1; output -------------------------
-            if (out_ok) {
-                const double2* g_row = pub_row(1, ppar);  // g1(i-2)
-                const double2 g_c = g_row[cc];
-                const int slot_m3 = ring(3);              // z row j-3 == row i-2
-                const double2 u0o = zu0[slot_m3 * ZW + cc];
-                const double2 a2 = cf.kv(cf.dv(zv[slot_m3 * ZW + cc]), g_c, g_row[cc - 1], g_row[cc + 1], g1_m3, g1);
-                const double2 g2 = cf.jt(g_c, a2, u0o);
-                const size_t gi = at(a, xout, s.Y0 + yrel);
+            for (int q = 0; q < 3; ++q) {
+                double rx = c.fco[q][MF] * gout[MF].x, ry = c.fco[q][MF] * gout[MF].y;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const double2 r = make_double2(
-                        fma(c.fco[q][0], f_m2.x, fma(c.fco[q][1], g_c.x, c.fco[q][2] * g2.x)),
-                        fma(c.fco[q][0], f_m2.y, fma(c.fco[q][1], g_c.y, c.fco[q][2] * g2.y)));
-                    uout[q][gi] = make_double2(u0o.x + r.x, u0o.y + r.y);
-                    March3<MF, NT, true, ISO, GHOST>::track(rmax, r);
+                for (int n = MF - 1; n >= 0; --n) {
+                    rx = fma(c.fco[q][n], gout[n].x, rx);
+                    ry = fma(c.fco[q][n], gout[n].y, ry);
                 }
+                uout[q][gi] = make_double2(u0o.x + rx, u0o.y + ry);
+                March3<MF, NT, true, ISO, GHOST>::track(rmax, make_double2(rx, ry));
             }
-            pub_row(1, par)[cc] = g1;  // publish g1(i-1)
         }
-        // rotate the window: down <- centre <- new
+        // rotate the window: down <- centre <- new; advance the ring positions
         zw[2] = zw[1];
         zw[1] = zw[0];
         vw[2] = vw[1];
         vw[1] = vw[0];
+        zs = zs + 1 == S ? 0 : zs + 1;
+#pragma unroll
+        for (int n = 0; n + 3 <= MF; ++n) hs[n] = hs[n] + 1 == depth(n) ? 0 : hs[n] + 1;
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int band, int Y0,
                         int R, unsigned& rmax, double acc[kObsFields]) {
         const Coef<ISO> cf{c};
         Seg s;
-        s.X0 = band * G::TX;
+        s.X0 = band * TX;
         s.Y0 = Y0;
         s.R = R;
         s.nzrows = R + 2 * MF + 2;
@@ -661,8 +718,16 @@ struct MarchFirst {
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) issue_row(a, s, k, k);
+        zs = 0;
+#pragma unroll
+        for (int n = 0; n + 3 <= MF; ++n) hs[n] = 0;
         const int jend = R + 2 * MF + 2;
-        for (int j = 0; j < jend; ++j) body(a, cf, uout, s, j, rmax, acc);
+        int j = 0;
+        for (; j + 1 < jend; j += 2) {
+            body<0>(a, cf, uout, s, j, rmax, acc);
+            body<1>(a, cf, uout, s, j + 1, rmax, acc);
+        }
+        if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
         cp_async_wait<0>();
         __syncthreads();
     }
@@ -673,8 +738,9 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
                            const double2* const uin[3], double2* const uout[3],
                            unsigned& rmax, double acc[kObsFields]) {
     if constexpr (FIRST && M >= 1) {
-        MarchFirst<M, NT, ISO, GHOST> mf(smem);
-        const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
+        using MFirst = MarchFirst<M, NT, ISO, GHOST>;
+        MFirst mf(smem);
+        const long long total = static_cast<long long>((a.nx + MFirst::TX - 1) / MFirst::TX) * a.ny;
         const long long G = gridDim.x;
         const long long b0 = total * blockIdx.x / G;
         const long long b1 = total * (blockIdx.x + 1) / G;
@@ -686,22 +752,22 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
             mf.run(a, c, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
             pos = seg_end;
         }
-        return;
-    }
-    March3<M, NT, FIRST, ISO, GHOST, DEF> m(smem);
-    // band-rows of this sweep's band width (TX depends on M)
-    const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
-    const long long G = gridDim.x;
-    const long long b0 = total * blockIdx.x / G;
-    const long long b1 = total * (blockIdx.x + 1) / G;
-    long long pos = b0;
-    while (pos < b1) {
-        const int band = static_cast<int>(pos / a.ny);
-        const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
-        const long long band_end = static_cast<long long>(band + 1) * a.ny;
-        const long long seg_end = band_end < b1 ? band_end : b1;
-        m.run(a, c, uin, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
-        pos = seg_end;
+    } else {
+        March3<M, NT, FIRST, ISO, GHOST, DEF> m(smem);
+        // band-rows of this sweep's band width (TX depends on M)
+        const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
+        const long long G = gridDim.x;
+        const long long b0 = total * blockIdx.x / G;
+        const long long b1 = total * (blockIdx.x + 1) / G;
+        long long pos = b0;
+        while (pos < b1) {
+            const int band = static_cast<int>(pos / a.ny);
+            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
+            const long long band_end = static_cast<long long>(band + 1) * a.ny;
+            const long long seg_end = band_end < b1 ? band_end : b1;
+            m.run(a, c, uin, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
+            pos = seg_end;
+        }
     }
 }
 
@@ -859,8 +925,14 @@ int grid3(int device) {
 
 }  // namespace
 
+// (first-sweep depth, later-sweep depth) pairs with a compiled kernel
+#define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(6, 1) X(4, 2) X(6, 2) X(6, 0)
+
 bool march2_supported(int mf, int m) {
-    return (m >= 0 && m <= 2) && (mf == m || mf == 2);
+#define MB4_PAIR_EQ(F, N) if (mf == F && m == N) return true;
+    MB4_MARCH2_PAIRS(MB4_PAIR_EQ)
+#undef MB4_PAIR_EQ
+    return false;
 }
 
 cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0, const double* V,
@@ -884,24 +956,16 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
     a.ghost = ghost;
     a.pitch = nx + 2 * ghost;
     a.sweep0 = sweep0;
-    switch (mf * 4 + m) {
-        case 0: return dispatch3<0, 0>(a, c, device, s);
-        case 5: return dispatch3<1, 1>(a, c, device, s);
-        case 10: return dispatch3<2, 2>(a, c, device, s);
-        case 8: return dispatch3<2, 0>(a, c, device, s);
-        case 9: return dispatch3<2, 1>(a, c, device, s);
-    }
+#define MB4_PAIR_LAUNCH(F, N) if (mf == F && m == N) return dispatch3<F, N>(a, c, device, s);
+    MB4_MARCH2_PAIRS(MB4_PAIR_LAUNCH)
+#undef MB4_PAIR_LAUNCH
     return cudaErrorInvalidValue;
 }
 
 int march2_grid_size(int mf, int m, int device) {
-    switch (mf * 4 + m) {
-        case 0: return grid3<0, 0>(device);
-        case 5: return grid3<1, 1>(device);
-        case 10: return grid3<2, 2>(device);
-        case 8: return grid3<2, 0>(device);
-        case 9: return grid3<2, 1>(device);
-    }
+#define MB4_PAIR_GRID(F, N) if (mf == F && m == N) return grid3<F, N>(device);
+    MB4_MARCH2_PAIRS(MB4_PAIR_GRID)
+#undef MB4_PAIR_GRID
     return 0;
 }
 

@@ -2,8 +2,9 @@
 
 One process per GPU (torchrun); torch.distributed is the plumbing (NCCL on the
 GPU, gloo for the CPU tests).  Each rank owns a block of the global lattice in
-a ghost-padded libmb4cu sub-domain context (mb4cu_problem.ghost = m + 1).  One
-MB4 step:
+a ghost-padded libmb4cu sub-domain context (mb4cu_problem.ghost = max(mf, m) + 1;
+u0 / V halos are mf + 1 wide for the depth-mf first sweep, the stage-set halos
+m + 1).  One MB4 step:
 
     exchange u0 halos (x phase, then y phase: corners propagate)
     for s = 0, 1, ...:
@@ -284,7 +285,7 @@ class CudaBackend:
 
     def __init__(self, dec: Decomposition, V_block: np.ndarray, scheme, gamma: float, cx: float, cy: float,
                  epsilon: float, max_iters: int, neumann_terms: int, device: int,
-                 neumann_first: int = 2):
+                 neumann_first: int = 6):
         import torch
 
         self.torch = torch

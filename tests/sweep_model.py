@@ -49,14 +49,14 @@ def sweep(u0, U, V, gamma, h, scheme, m, nx, ny, cx=1.0, cy=1.0):
     return Un, rmax
 
 
-def step(u0, V, gamma, h, scheme, m, nx, ny, eps, max_iters=50, mf=None):
+def step(u0, V, gamma, h, scheme, m, nx, ny, eps, max_iters=50, mf=None, cx=1.0, cy=1.0):
     """One step; the first sweep uses depth mf (default m), the others m."""
     from paper_2003_04345_b200.dist import stage_converged, widen_residual
 
     U = None
     r_prev = float("nan")
     for it in range(1, max_iters + 1):
-        U, r = sweep(u0, U, V, gamma, h, scheme, m if (it > 1 or mf is None) else mf, nx, ny)
+        U, r = sweep(u0, U, V, gamma, h, scheme, m if (it > 1 or mf is None) else mf, nx, ny, cx, cy)
         r = widen_residual(r)
         if stage_converged(r, r_prev, it - 1, eps):
             return U[2], it

@@ -91,7 +91,8 @@ def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
     V, psi = configs.make_inputs(cfg)
     model = configs.model_for(cfg, V)
     scheme = nls2d.Mb4Scheme()
-    mf = m if (kernel == 2 or m > 2) else 2  # production/tiled default: first sweep depth 2
+    # default first-sweep depth: 6 on the production kernel, 2 on the tiled one, m on v1
+    mf = m if (kernel == 2 or m > 2) else (6 if kernel == 0 else 2)
     ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=mf)
     with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=m, kernel=kernel) as s:
         s.set_state(psi)
@@ -116,7 +117,7 @@ def _oracle_steps(cfg, V, psi, nsteps):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("m", [None, 0, 1, 2, 3])  # None: default (deep first sweep, adaptive m)
 def test_ten_steps_match_oracle(name, m):
     cfg = configs.CONFIGS[name]
     V, psi = configs.make_inputs(cfg)
@@ -157,6 +158,61 @@ def test_scheme_tables_runtime_and_compiled(alpha1, m):
     with nls2d.Session(model, nls2d.Mb4Scheme(alpha1), configs.newton_for(cfg), neumann_terms=m) as s:
         s.set_state(psi)
         obs, _ = s.run(cfg.dt, 5)
+        got = s.get_state()
+    assert rel(got, ref) <= 1e-10
+    assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * abs(ref_obs[0, 3])
+
+
+def _packet_lattice(nx, ny, lx, ly, seed=3):
+    g = nls2d.GridSpec(nx, ny, lx, ly)
+    rng = np.random.default_rng(seed)
+    V = np.where(rng.uniform(size=nx * ny) < 0.02, 5.0, 0.0)
+    x = (np.arange(nx) - nx / 3) / 9.0
+    y = (np.arange(ny) - ny / 2) / 7.0
+    psi = (np.exp(-(y[:, None] ** 2 + x[None, :] ** 2)) * np.exp(0.4j * np.arange(nx))[None, :]).reshape(-1)
+    psi = (psi / np.linalg.norm(psi) * 3.0).astype(np.complex128)
+    return g, V, psi
+
+
+@pytest.mark.parametrize("mf,m", [(2, 1), (3, 1), (4, 1), (6, 1), (4, 2), (6, 2)])
+@pytest.mark.parametrize("lattice", ["cfg1", "aniso_ragged"])
+def test_deep_first_sweep_matches_numpy_model(mf, m, lattice):
+    """The specialised first sweep at depth mf (one J-chain instead of three stage
+    recursions) gives the same sweep count and state as the numpy model, on an
+    isotropic lattice (compiled scheme tables) and on an anisotropic one whose
+    width is not a multiple of the band (runtime tables, partial bands)."""
+    scheme = nls2d.Mb4Scheme()
+    if lattice == "cfg1":
+        cfg = configs.CONFIGS["cfg1"]
+        V, psi = configs.make_inputs(cfg)
+        model = configs.model_for(cfg, V)
+        h, eps, nx, ny = cfg.dt, cfg.epsilon, cfg.nx, cfg.ny
+        newton = configs.newton_for(cfg)
+    else:
+        nx, ny = 250, 70
+        g, V, psi = _packet_lattice(nx, ny, 250.0, 84.0)
+        model = nls2d.GridModel(g, 0.7, V)
+        h, eps = 0.01, 1e-13
+        newton = nls2d.NewtonConfig(eps, 50, 0)
+    ref, its = SM.step(psi, V, model.gamma(), h, scheme, m, nx, ny, eps, mf=mf, cx=model.cx, cy=model.cy)
+    with nls2d.Session(model, scheme, newton, neumann_terms=m, neumann_first=mf) as s:
+        s.set_state(psi)
+        st = nls2d.StepStats()
+        s.step(h, st)
+        got = s.get_state()
+    assert st.newton_iters == its
+    assert rel(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("mf", [4, 6])
+def test_deep_first_sweep_ten_steps_match_oracle(mf):
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    ref, ref_obs = _oracle_steps(cfg, V, psi, 10)
+    model = configs.model_for(cfg, V)
+    with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg), neumann_terms=1, neumann_first=mf) as s:
+        s.set_state(psi)
+        obs, _ = s.run(cfg.dt, 10)
         got = s.get_state()
     assert rel(got, ref) <= 1e-10
     assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * abs(ref_obs[0, 3])

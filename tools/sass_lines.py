@@ -53,7 +53,7 @@ for (l, ins), (_, n) in zip(seq, counts):
     kind[l][op.split(".")[0]] += n
 tot = sum(per.values())
 src = {}
-for l, n in per.most_common(40):
+for l, n in per.most_common(int(sys.argv[4]) if len(sys.argv) > 4 else 40):
     if l is None:
         continue
     fn, no = l
