@@ -165,11 +165,19 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- helpers
 
 
-def measured_traffic(cfg_name: str, m: int):
+def schedule_key(args) -> str:
+    """Stage-iteration schedule of the run: 'default' (deep first sweep, adaptive m)
+    or mf<first>_m<terms> when set explicitly."""
+    if args.neumann < 0 and args.neumann_first < 0:
+        return "default"
+    return f"mf{args.neumann_first}_m{args.neumann}"
+
+
+def measured_traffic(cfg_name: str, schedule: str):
     """DRAM bytes per step-kernel launch from the committed ncu capture (profiles/traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            t = json.load(f).get(f"{cfg_name}_m{m}")
+            t = json.load(f).get(f"{cfg_name}_{schedule}")
         return None if t is None else float(t["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -341,7 +349,9 @@ def run_ours(args, d: Dist):
                         f"{cfg.defect_frac:.0%} defects, {cfg.npackets} packet(s) sigma={cfg.sigma}, eps={cfg.epsilon}",
             "lattice": [cfg.nx, cfg.ny],
             "sites_per_gpu": n,
-            "neumann_terms": args.neumann if args.neumann >= 0 else 1,
+            "neumann_terms": args.neumann if args.neumann >= 0 else "adaptive 1..2",
+            "neumann_first": args.neumann_first if args.neumann_first >= 0 else 6,
+            "schedule": schedule_key(args),
             "kernel": "tiled" if args.kernel == 1 else "default",
             "l2": "flushed between steps" if flush else "inputs larger than L2 (state+stages >= 3 GiB)",
             "parallelism": "replicas" if d.world > 1 else "single",
@@ -354,7 +364,7 @@ def run_ours(args, d: Dist):
             "peak": peak,
             "unit": "GB/s",
             "frac": achieved / peak,
-            "traffic": measured_traffic(cfg.name, args.neumann if args.neumann >= 0 else 1),
+            "traffic": measured_traffic(cfg.name, schedule_key(args)),
             "traffic_source": "ncu --set full, dram__bytes_read+write per launch (profiles/traffic.json)",
             "peak_kind": peak_kind,
             "kernel": "stage sweep",
