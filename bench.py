@@ -357,6 +357,7 @@ def run_ours(args, d: Dist):
             "parallelism": "replicas" if d.world > 1 else "single",
         },
         "sweeps_per_step": sweeps_per_step,
+        "final_sweep_misses": int(prof.get("redone", 0)),
         "energy_drift": drift,
         "roofline": {
             "bound": "hbm",

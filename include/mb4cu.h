@@ -202,7 +202,8 @@ int mb4cu_scale_state(double* psi, size_t nsites, double s, int threads);
 /* Kernel-level profiling of the stage sweeps (CUDA events around every sweep
  * launch, on the context stream).  alg_bytes counts the algorithmic HBM bytes
  * of the sweeps: 72 B/site for the first sweep of a step (u0, V in; U out) and
- * 120 B/site for the others (u0, V, U in; U out) -- see DESIGN.md. */
+ * 120 B/site for the others (u0, V, U in; U out), 88 B/site for a final sweep
+ * that stored U3 only (speculative final sweep) -- see DESIGN.md. */
 typedef struct {
     double kernel_ms;         /* summed device time of the sweep launches            */
     long long launches;       /* sweep-kernel launches                                */
@@ -212,6 +213,7 @@ typedef struct {
     double sweep_ms[8];       /* device time by sweep index within a step (0 = first),
                                  persistent kernel only (%globaltimer at grid barriers) */
     long long sweep_n[8];     /* samples accumulated in sweep_ms                      */
+    long long redone;         /* speculative final sweeps that missed and were redone */
 } mb4cu_profile;
 
 int mb4cu_profile_enable(mb4cu_ctx* ctx, int on);

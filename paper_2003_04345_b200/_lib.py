@@ -82,6 +82,7 @@ class Profile(C.Structure):
         ("other_launches", C.c_longlong),
         ("sweep_ms", D * 8),
         ("sweep_n", C.c_longlong * 8),
+        ("redone", C.c_longlong),
     ]
 
 

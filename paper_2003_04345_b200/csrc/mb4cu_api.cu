@@ -31,6 +31,7 @@ struct mb4cu_ctx {
     int max_iters = 0, max_halvings = 0, m = 2, mf = 2, kernel = 0;
     bool m_auto = false;  // neumann_terms = -1 on the production kernel: m adapts in {1, 2}
     int auto_steps = 0;
+    int last_sweeps = 0;  // sweeps of the last converged step (predicts the final sweep)
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
     mb4cu_scheme scheme{};
@@ -87,9 +88,11 @@ void adapt_neumann(mb4cu_ctx* ctx, int sweeps) {
     if (ctx->m == 1 && sweeps >= 4) {
         ctx->m = 2;
         ctx->auto_steps = 0;
+        ctx->last_sweeps = 0;
     } else if (ctx->m == 2 && ++ctx->auto_steps >= 64) {
         ctx->m = 1;
         ctx->auto_steps = 0;
+        ctx->last_sweeps = 0;
     }
 }
 
@@ -186,11 +189,14 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * ctx->max_iters,
                                   ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
+    // the step is predicted to converge at the previous step's sweep count: that
+    // sweep stores U3 only (redone in-kernel with all stages if the guess fails)
+    const int spec = ctx->last_sweeps >= 2 ? ctx->last_sweeps - 1 : -1;
     if (ctx->kernel == 0 && mb4cu::march2_supported(ctx->mf, ctx->m)) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
                                                 ctx->max_iters, ctx->eps, 1, c, ctx->device,
-                                                ctx->stream, 0, 0));
+                                                ctx->stream, 0, 0, spec));
     } else {
         MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
@@ -208,7 +214,10 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         ctx->prof.kernel_ms += ms;
         ctx->prof.launches += 1;
         ctx->prof.sweeps += st.sweeps;
-        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (st.sweeps - 1));
+        // U3-only final sweep: 88 instead of 120 B/site (a redone guess is overhead, not counted)
+        const bool spec_hit = st.converged && st.sweeps - 1 == spec && spec >= 1;
+        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (st.sweeps - 1) - (spec_hit ? 32.0 : 0.0));
+        ctx->prof.redone += st.redone;
         if (ctx->kernel == 0 && mb4cu::march2_supported(ctx->mf, ctx->m)) {
             for (int k = 0; k < st.sweeps && k < 8; ++k) {
                 ctx->prof.sweep_ms[k] += 1e-6 * static_cast<double>(st.t[k + 1] - st.t[k]);
@@ -228,6 +237,7 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     if (st.converged) {
         std::swap(ctx->u0, ctx->U[st.set][2]);
         ctx->obs_cached = false;
+        ctx->last_sweeps = mb4cu::march2_supported(ctx->mf, ctx->m) && ctx->kernel == 0 ? st.sweeps : 0;
         adapt_neumann(ctx, st.sweeps);
         return MB4CU_OK;
     }

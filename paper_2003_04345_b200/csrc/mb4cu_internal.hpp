@@ -99,7 +99,7 @@ struct StepStatus {
     int sweeps;        // sweeps executed
     int set;           // stage set holding the last iterate (0/1)
     int converged;     // 1: ||r||_inf <= eps reached
-    int pad;
+    int redone;        // speculative final sweeps redone with all stages (production kernel)
     double rlast;      // ||r||_inf of the last sweep
     double obs[kObsFields];  // energy sums of u0 (first sweep)
     // %globaltimer (ns) at kernel start and after each sweep's grid barrier
@@ -135,6 +135,7 @@ struct StepArgs {
     int ghost;
     int pitch;
     int sweep0;                 // global index of the first sweep of this launch
+    int spec_sweep;             // global sweep index stored as U3 only (-1: none)
 };
 
 // Launchers (sweep_tiled.cu, sweep_march.cu).
@@ -148,7 +149,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
-                               int ghost, int sweep0);
+                               int ghost, int sweep0, int spec_sweep = -1);
 int march2_grid_size(int mf, int m, int device);
 
 // Halo transfer between a padded sub-domain array set and a contiguous buffer

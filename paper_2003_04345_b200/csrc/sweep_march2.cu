@@ -173,6 +173,7 @@ struct March3 {
 
     struct Seg {
         int X0, Y0, R, yz0, nzrows;
+        int smask;       // stages stored (bit q): 7, or 4 = U3 only (speculative final sweep)
         int gxa, gxb;    // global columns of smem columns t and t + NT (t < 2)
         int next_row;    // global (periodic) row of the next z row to issue
         size_t next_off; // its element offset
@@ -357,7 +358,8 @@ struct March3 {
                         const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
                         for (int q = 0; q < 3; ++q) {
-                            uout[q][gi] = make_double2(z[q + 1].x - phi[q].x, z[q + 1].y - phi[q].y);
+                            if ((s.smask >> q) & 1)
+                                uout[q][gi] = make_double2(z[q + 1].x - phi[q].x, z[q + 1].y - phi[q].y);
                             track(rmax, phi[q]);
                         }
                     }
@@ -395,7 +397,7 @@ struct March3 {
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const double2 uo = FIRST ? zw[S_DN][0] : zw[S_DN][q + 1];
-                    uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
+                    if ((s.smask >> q) & 1) uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
                     track(rmax, tb[q]);
                 }
             }
@@ -421,7 +423,7 @@ struct March3 {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZW + cc];
-                uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
+                if ((s.smask >> q) & 1) uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
                 track(rmax, tb[q]);
             }
         }
@@ -431,9 +433,10 @@ struct March3 {
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
                         double2* const uout[3], int band, int Y0, int R, unsigned& rmax,
-                        double acc[kObsFields]) {
+                        double acc[kObsFields], int smask) {
         const Coef<ISO, DEF> cf{c};
         Seg s;
+        s.smask = smask;
         s.X0 = band * G::TX;
         s.Y0 = Y0;
         s.R = R;
@@ -736,7 +739,7 @@ struct MarchFirst {
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
-                           unsigned& rmax, double acc[kObsFields]) {
+                           unsigned& rmax, double acc[kObsFields], int smask = 7) {
     if constexpr (FIRST && M >= 1) {
         using MFirst = MarchFirst<M, NT, ISO, GHOST>;
         MFirst mf(smem);
@@ -765,7 +768,7 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
             const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
             const long long band_end = static_cast<long long>(band + 1) * a.ny;
             const long long seg_end = band_end < b1 ? band_end : b1;
-            m.run(a, c, uin, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
+            m.run(a, c, uin, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc, smask);
             pos = seg_end;
         }
     }
@@ -811,7 +814,8 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         reinterpret_cast<unsigned long long*>(smem)[q] = MB4_POISON_SMEM;
     __syncthreads();
 #endif
-    int sweeps = 0, set = 0, converged = 0;
+    int sweeps = 0, set = 0, converged = 0, redone = 0;
+    bool redo = false;  // this pass repeats the missed speculative sweep with all stages
     if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
     double rlast = 0.0;
     for (int s = 0; s < a.max_iters; ++s) {
@@ -839,9 +843,20 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
                 }
             }
         } else {
+            // Speculative final sweep (sg == spec_sweep, predicted by the host from the
+            // previous step): only U3 -- the step result -- is stored, saving 32 of the
+            // 120 B/site.  If it does not converge, it is redone below with all stages
+            // (same inputs, same arithmetic, so the result is independent of the guess).
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
+            sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc,
+                                                       sg == a.spec_sweep && !redo ? 4 : 7);
+        }
+        if (redo) {  // same residual as the speculative pass: no new test
+            redo = false;
+            ++redone;
+            grid.sync();
+            continue;
         }
         block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[s]);
         grid.sync();
@@ -857,11 +872,16 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             converged = 1;
             break;
         }
+        if (sg > 0 && sg == a.spec_sweep && s + 1 < a.max_iters) {
+            redo = true;
+            --s;  // repeat sweep sg with all stages stored
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.status->sweeps = sweeps;
         a.status->set = set;
         a.status->converged = converged;
+        a.status->redone = redone;
         a.status->rlast = rlast;
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
@@ -939,7 +959,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
-                               int ghost, int sweep0) {
+                               int ghost, int sweep0, int spec_sweep) {
     StepArgs a{};
     a.nx = nx;
     a.ny = ny;
@@ -956,6 +976,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
     a.ghost = ghost;
     a.pitch = nx + 2 * ghost;
     a.sweep0 = sweep0;
+    a.spec_sweep = spec_sweep;
 #define MB4_PAIR_LAUNCH(F, N) if (mf == F && m == N) return dispatch3<F, N>(a, c, device, s);
     MB4_MARCH2_PAIRS(MB4_PAIR_LAUNCH)
 #undef MB4_PAIR_LAUNCH

@@ -216,3 +216,31 @@ def test_deep_first_sweep_ten_steps_match_oracle(mf):
         got = s.get_state()
     assert rel(got, ref) <= 1e-10
     assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * abs(ref_obs[0, 3])
+
+
+def test_speculative_final_sweep_miss_is_redone_exactly():
+    """The production kernel stores only U3 in the sweep the previous step's count
+    predicts to be final; when the prediction misses (here: the second step is
+    twice as long and needs more sweeps) the sweep is redone with all stages.  The
+    result and the sweep counts equal the numpy model's (no speculation there)."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    model = configs.model_for(cfg, V)
+    scheme = nls2d.Mb4Scheme()
+    u1, it1 = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+    u2, it2 = SM.step(u1, V, cfg.gamma, 2 * cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+    u3, it3 = SM.step(u2, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+    assert it2 > it1
+    with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=1, neumann_first=6) as s:
+        s.set_state(psi)
+        s.profile_enable(True)
+        got = []
+        for h in (cfg.dt, 2 * cfg.dt, cfg.dt):
+            st = nls2d.StepStats()
+            s.step(h, st)
+            got.append((s.get_state(), st.newton_iters))
+        prof = s.profile()
+    assert [g[1] for g in got] == [it1, it2, it3]
+    for (u, _), ref in zip(got, (u1, u2, u3)):
+        assert rel(u, ref) <= 1e-13
+    assert prof["redone"] >= 1
