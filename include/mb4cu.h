@@ -133,6 +133,25 @@ int mb4cu_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats);
 int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* iters_series,
               mb4cu_stats* stats);
 
+/* The reference's other integrators on the resident state (StepDriver::advance,
+ * integrators.cpp:425-455; methods integrators.cpp:45-395), for the harness's
+ * method comparison / convergence studies.  method = the reference's MethodId
+ * order: */
+#define MB4CU_METHOD_RK4 0    /* rk4_step, explicit, no halving                  */
+#define MB4CU_METHOD_GAUSS2 1 /* gauss_step(1): implicit midpoint               */
+#define MB4CU_METHOD_GAUSS4 2 /* gauss_step(2): 2-stage Gauss, coupled system   */
+#define MB4CU_METHOD_AVF2 3   /* avf2_step                                      */
+#define MB4CU_METHOD_AVF4 4   /* avf4_step, coupled system                      */
+#define MB4CU_METHOD_MB4 5    /* = mb4cu_step / mb4cu_run                        */
+/* Implicit methods: the reference's simplified Newton iteration (J at u0, stop on
+ * ||delta||_inf <= epsilon) with the linear systems solved matrix-free by GMRES
+ * on the GPU; halving on failure as the reference.  stats->newton_iters counts
+ * Newton iterations.  Not available in sub-domain mode. */
+int mb4cu_method_step(mb4cu_ctx* ctx, int method, double h, mb4cu_stats* stats);
+/* mb4cu_run for any method (energy record from a separate monitor pass). */
+int mb4cu_method_run(mb4cu_ctx* ctx, int method, double h, int nsteps, double* obs_series, int* iters_series,
+                     mb4cu_stats* stats);
+
 /* Energy monitor of the resident state (observables, lattice.cpp:106-137). */
 int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out);
 

@@ -12,8 +12,9 @@
 //     lattice.hpp:54, is not offered);
 //   - WorkerPool / SolverKind / cached_order are accepted and ignored (no sparse
 //     factorization, no CPU threads on this path);
-//   - StepStats::newton_iters counts stage sweeps; solve_seconds is device time;
-//   - StepDriver supports MethodId::Mb4 only (other methods are out of scope).
+//   - for MB4, StepStats::newton_iters counts stage sweeps; solve_seconds is device time;
+//   - every MethodId runs on the GPU (RK4 / GAUSS / AVF: methods.cu, their linear
+//     systems by matrix-free GMRES instead of sparse LU).
 #pragma once
 
 #include <array>
@@ -143,11 +144,21 @@ private:
 
 class GridModel;
 
-/// RAII device session: one mb4cu context, state resident in HBM.
+enum class MethodId { Rk4, Gauss2, Gauss4, Avf2, Avf4, Mb4 };
+
+/// integrators.cpp:13-43
+inline int method_order(MethodId m) { return m == MethodId::Gauss2 || m == MethodId::Avf2 ? 2 : 4; }
+inline std::string method_name(MethodId m) {
+    static const char* names[] = {"RK4", "GAUSS2", "GAUSS4", "AVF2", "AVF4", "MB4"};
+    return names[static_cast<int>(m)];
+}
+
+/// RAII device session: one mb4cu context, state resident in HBM; step()/run()
+/// advance with `method` (default MB4).
 class DeviceSession {
 public:
     DeviceSession(const GridModel& model, const Mb4Scheme& scheme, const NewtonConfig& cfg,
-                  int neumann_terms = -1, int device = 0, int kernel = 0);
+                  int neumann_terms = -1, int device = 0, int kernel = 0, MethodId method = MethodId::Mb4);
     ~DeviceSession() { mb4cu_destroy(ctx_); }
     DeviceSession(const DeviceSession&) = delete;
     DeviceSession& operator=(const DeviceSession&) = delete;
@@ -162,7 +173,7 @@ public:
     }
     void step(double h, StepStats* stats = nullptr) {
         mb4cu_stats st{};
-        const int rc = mb4cu_step(ctx_, h, &st);
+        const int rc = mb4cu_method_step(ctx_, method_, h, &st);
         if (stats) {
             stats->newton_iters += st.newton_iters;
             stats->halvings += st.halvings;
@@ -176,7 +187,8 @@ public:
         std::vector<int> it(static_cast<size_t>(nsteps));
         mb4cu_stats st{};
         static_assert(sizeof(Observables) == 7 * sizeof(double), "layout");
-        const int rc = mb4cu_run(ctx_, h, nsteps, reinterpret_cast<double*>(rows.data()), it.data(), &st);
+        const int rc = mb4cu_method_run(ctx_, method_, h, nsteps, reinterpret_cast<double*>(rows.data()), it.data(),
+                                        &st);
         check(rc, st.last_residual);
         if (iters) *iters = it;
         return rows;
@@ -196,6 +208,7 @@ public:
 private:
     mb4cu_ctx* ctx_ = nullptr;
     int n_ = 0;
+    int method_ = MB4CU_METHOD_MB4;
 };
 
 class GridModel {
@@ -228,7 +241,8 @@ private:
 
 inline DeviceSession::DeviceSession(const GridModel& model, const Mb4Scheme& scheme,
                                     const NewtonConfig& cfg, int neumann_terms, int device,
-                                    int kernel) {
+                                    int kernel, MethodId method)
+    : method_(static_cast<int>(method)) {
     cfg.validate();
     mb4cu_problem p{};
     p.nx = model.grid().nx;
@@ -290,21 +304,52 @@ inline State mb4_step(const GridModel& model, const Mb4Scheme& scheme, const Sta
     return s.get_state();
 }
 
-enum class MethodId { Rk4, Gauss2, Gauss4, Avf2, Avf4, Mb4 };
+namespace detail {
+inline State plain_method_step(MethodId m, const GridModel& model, const State& u0, double h,
+                               const NewtonConfig& cfg, StepStats* stats) {
+    cfg.validate();
+    if (!(h > 0.0)) throw std::invalid_argument("step: h must be positive");
+    // the free functions of integrators.hpp do not halve
+    DeviceSession s(model, Mb4Scheme(), NewtonConfig{cfg.epsilon, cfg.max_iters, 0}, -1, 0, 0, m);
+    s.set_state(u0);
+    s.step(h, stats);
+    return s.get_state();
+}
+}  // namespace detail
 
-/// integrators.hpp:46-66, MB4 branch.  Keeps one device session per driver.
+/// integrators.hpp:17-43 on the GPU (host vectors in and out)
+inline State rk4_step(const GridModel& model, const State& u0, double h) {
+    return detail::plain_method_step(MethodId::Rk4, model, u0, h, NewtonConfig{}, nullptr);
+}
+inline State gauss_step(const GridModel& model, const State& u0, double h, int stages, const NewtonConfig& cfg,
+                        StepStats* stats = nullptr, SolverKind = SolverKind::Direct,
+                        const std::vector<int>* = nullptr) {
+    if (stages != 1 && stages != 2) throw std::invalid_argument("gauss_step: stages must be 1 or 2");
+    return detail::plain_method_step(stages == 1 ? MethodId::Gauss2 : MethodId::Gauss4, model, u0, h, cfg, stats);
+}
+inline State avf2_step(const GridModel& model, const State& u0, double h, const NewtonConfig& cfg,
+                       StepStats* stats = nullptr, SolverKind = SolverKind::Direct,
+                       const std::vector<int>* = nullptr) {
+    return detail::plain_method_step(MethodId::Avf2, model, u0, h, cfg, stats);
+}
+inline State avf4_step(const GridModel& model, const State& u0, double h, const NewtonConfig& cfg,
+                       StepStats* stats = nullptr, SolverKind = SolverKind::Direct,
+                       const std::vector<int>* = nullptr) {
+    return detail::plain_method_step(MethodId::Avf4, model, u0, h, cfg, stats);
+}
+
+/// integrators.hpp:46-66.  Keeps one device session per driver; the halving
+/// policy of advance() (integrators.cpp:425-455) runs inside the library.
 class StepDriver {
 public:
     StepDriver(const GridModel& model, MethodId method, NewtonConfig cfg,
                SolverKind = SolverKind::Direct, WorkerPool* = nullptr)
         : cfg_(cfg) {
         cfg_.validate();
-        if (method != MethodId::Mb4)
-            throw std::invalid_argument("StepDriver: only MethodId::Mb4 runs on the GPU path");
-        session_ = std::make_unique<DeviceSession>(model, scheme_, cfg_);
+        session_ = std::make_unique<DeviceSession>(model, scheme_, cfg_, -1, 0, 0, method);
     }
     State advance(const State& u0, double h, StepStats* stats = nullptr) {
-        if (!(h > 0.0)) throw std::invalid_argument("mb4_step: h must be positive");
+        if (!(h > 0.0)) throw std::invalid_argument("advance: h must be positive");
         session_->set_state(u0);
         session_->step(h, stats);
         return session_->get_state();

@@ -97,6 +97,8 @@ def ref_lib() -> C.CDLL:
         L.ref_mb4_run.argtypes = [C.c_int, C.c_int, D, D, D, DP, DP, D, C.c_int, D, C.c_int,
                                   C.c_int, C.c_int, C.c_int, DP, IP, DP]
         L.ref_mb4_run.restype = C.c_int
+        L.ref_method_run.argtypes = [C.c_int] + L.ref_mb4_run.argtypes
+        L.ref_method_run.restype = C.c_int
         _rlib = L
     return _rlib
 
@@ -215,9 +217,12 @@ def ref_eval_phi(nx, ny, lx, ly, gamma, V, u0, stages, h):
     return out
 
 
+METHODS = ("rk4", "gauss2", "gauss4", "avf2", "avf4", "mb4")  # integrators.hpp:12 order
+
+
 def ref_run(nx, ny, lx, ly, gamma, V, u0, h, nsteps, eps=1e-14, max_iters=50, max_halvings=4,
-            solver: str = "direct", workers: int = 1, record: bool = True):
-    """The reference stepping loop (StepDriver(MB4) -> mb4_step) on the host cores.
+            solver: str = "direct", workers: int = 1, record: bool = True, method: str = "mb4"):
+    """The reference stepping loop (StepDriver(method) -> advance) on the host cores.
 
     Returns (u_final, obs[(nsteps+1),7] or None, iters[nsteps], seconds)."""
     V = np.ascontiguousarray(V, dtype=np.float64)
@@ -225,10 +230,10 @@ def ref_run(nx, ny, lx, ly, gamma, V, u0, h, nsteps, eps=1e-14, max_iters=50, ma
     obs = np.zeros((nsteps + 1, 7)) if record else None
     iters = np.zeros(nsteps, dtype=np.int32)
     secs = D(0.0)
-    rc = ref_lib().ref_mb4_run(nx, ny, lx, ly, gamma, _p(V), _p(u), h, nsteps, eps, max_iters,
-                               max_halvings, 1 if solver == "gmres" else 0, workers,
-                               _p(obs) if record else None, iters.ctypes.data_as(IP),
-                               C.byref(secs))
+    rc = ref_lib().ref_method_run(METHODS.index(method.lower()), nx, ny, lx, ly, gamma, _p(V), _p(u), h,
+                                  nsteps, eps, max_iters, max_halvings, 1 if solver == "gmres" else 0,
+                                  workers, _p(obs) if record else None, iters.ctypes.data_as(IP),
+                                  C.byref(secs))
     if rc != 0:
-        raise RuntimeError(f"ref_mb4_run failed with status {rc}")
+        raise RuntimeError(f"ref_method_run({method}) failed with status {rc}")
     return u, obs, iters, secs.value

@@ -104,15 +104,29 @@ int ref_eval_phi(int nx, int ny, double lx, double ly, double gamma, const doubl
 // observables recorded per step as run() does (harness.cpp:105-122).
 // solver: 0 = Direct (default), 1 = Gmres.  obs: (nsteps+1)*7 or NULL.
 // Returns 0 ok, 2 non-convergence, 1 invalid argument, 3 other error.
+int ref_method_run(int method, int nx, int ny, double lx, double ly, double gamma, const double* v,
+                   double* u, double h, int nsteps, double eps, int max_iters, int max_halvings, int solver,
+                   int workers, double* obs, int* iters, double* seconds);
+
 int ref_mb4_run(int nx, int ny, double lx, double ly, double gamma, const double* v, double* u,
                 double h, int nsteps, double eps, int max_iters, int max_halvings, int solver,
                 int workers, double* obs, int* iters, double* seconds) {
+    return ref_method_run(static_cast<int>(MethodId::Mb4), nx, ny, lx, ly, gamma, v, u, h, nsteps, eps,
+                          max_iters, max_halvings, solver, workers, obs, iters, seconds);
+}
+
+// StepDriver(model, method, ...) stepping loop; method = the reference's MethodId
+// order (Rk4, Gauss2, Gauss4, Avf2, Avf4, Mb4), integrators.hpp:12.
+int ref_method_run(int method, int nx, int ny, double lx, double ly, double gamma, const double* v,
+                   double* u, double h, int nsteps, double eps, int max_iters, int max_halvings, int solver,
+                   int workers, double* obs, int* iters, double* seconds) {
+    if (method < 0 || method > 5) return 1;
     try {
         const int n = nx * ny;
         const GridModel model(GridSpec(nx, ny, lx, ly), gamma,
                               std::vector<double>(v, v + static_cast<size_t>(n)));
         WorkerPool pool(workers);
-        StepDriver driver(model, MethodId::Mb4, NewtonConfig{eps, max_iters, max_halvings},
+        StepDriver driver(model, static_cast<MethodId>(method), NewtonConfig{eps, max_iters, max_halvings},
                           solver == 1 ? SolverKind::Gmres : SolverKind::Direct, &pool);
         State s = to_state(u, n);
         if (obs) put_obs(obs, observables(model, s));

@@ -9,7 +9,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["mb4cu_api.cu", "sweep_tiled.cu", "sweep_march.cu", "sweep_march2.cu", "halo.cu", "krylov.cu"]
+CUDA_SOURCES = ["mb4cu_api.cu", "sweep_tiled.cu", "sweep_march.cu", "sweep_march2.cu", "halo.cu", "krylov.cu",
+                "methods.cu"]
 HOST_SOURCES = ["scheme_host.cpp", "inputs_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]

@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
         "mb4cu_get_state_device": (I, [P, P]),
         "mb4cu_step": (I, [P, D, C.POINTER(Stats)]),
         "mb4cu_run": (I, [P, D, I, DP, IP, C.POINTER(Stats)]),
+        "mb4cu_method_step": (I, [P, I, D, C.POINTER(Stats)]),
+        "mb4cu_method_run": (I, [P, I, D, I, DP, IP, C.POINTER(Stats)]),
         "mb4cu_observables": (I, [P, C.POINTER(Obs)]),
         "mb4cu_set_stream": (I, [P, P]),
         "mb4cu_apply_kv": (I, [P, DP, DP]),
@@ -166,7 +168,8 @@ def dptr(a: np.ndarray):
 EXPORTED = [
     "mb4cu_scheme_init", "mb4cu_create", "mb4cu_destroy", "mb4cu_last_error",
     "mb4cu_create_error", "mb4cu_set_state", "mb4cu_get_state", "mb4cu_set_state_device",
-    "mb4cu_get_state_device", "mb4cu_step", "mb4cu_run", "mb4cu_observables",
+    "mb4cu_get_state_device", "mb4cu_step", "mb4cu_run", "mb4cu_method_step", "mb4cu_method_run",
+    "mb4cu_observables",
     "mb4cu_set_stream", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
     "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
     "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",

@@ -58,6 +58,7 @@ struct mb4cu_ctx {
     struct {
         int m = 0;                  // GMRES restart length
         int nblk = 0;
+        size_t len = 0;             // complex entries per vector (N, or 2N for coupled systems)
         double2* mem = nullptr;     // basis (m+1) + b[3] + x[3] + w + y vectors
         double2** v_dev = nullptr;  // device array of basis pointers
         double* partial = nullptr;  // [m+1][nblk]
@@ -282,16 +283,40 @@ constexpr int kKrylovRestart = 50;
 constexpr int kKrylovMaxIters = 2000;
 constexpr double kKrylovTol = 1e-13;
 
-int kr_alloc(mb4cu_ctx* ctx) {
+void kr_free(mb4cu_ctx* ctx) {
     auto& k = ctx->kr;
-    if (k.mem) return MB4CU_OK;
+    cudaFree(k.mem);
+    cudaFree(k.v_dev);
+    cudaFree(k.partial);
+    cudaFreeHost(k.h_partial);
+    cudaFree(k.coef);
+    cudaFreeHost(k.h_coef);
+    k.mem = nullptr;
+    k.v_dev = nullptr;
+    k.partial = nullptr;
+    k.h_partial = nullptr;
+    k.coef = nullptr;
+    k.h_coef = nullptr;
+    k.len = 0;
+}
+
+// Krylov arena for vectors of len complex entries: basis (m+1), then 8 work
+// vectors (b, x, ... of the callers; w, y of kr_gmres).
+int kr_alloc(mb4cu_ctx* ctx, size_t len) {
+    auto& k = ctx->kr;
+    if (k.mem && k.len == len) return MB4CU_OK;
+    if (k.mem) {
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        kr_free(ctx);
+    }
     k.m = kKrylovRestart;
-    k.nblk = mb4cu::krylov_blocks(ctx->n);
+    k.len = len;
+    k.nblk = mb4cu::krylov_blocks(len);
     const size_t nvec = static_cast<size_t>(k.m + 1) + 3 + 3 + 2;
-    MB4_CUDA(ctx, cudaMalloc(&k.mem, nvec * ctx->n * sizeof(double2)));
+    MB4_CUDA(ctx, cudaMalloc(&k.mem, nvec * len * sizeof(double2)));
     MB4_CUDA(ctx, cudaMalloc(&k.v_dev, sizeof(double2*) * (k.m + 1)));
     std::vector<double2*> ptrs(k.m + 1);
-    for (int i = 0; i <= k.m; ++i) ptrs[i] = k.mem + static_cast<size_t>(i) * ctx->n;
+    for (int i = 0; i <= k.m; ++i) ptrs[i] = k.mem + static_cast<size_t>(i) * len;
     // on the context stream (a legacy-stream copy does not order against it)
     MB4_CUDA(ctx, cudaMemcpyAsync(k.v_dev, ptrs.data(), sizeof(double2*) * (k.m + 1), cudaMemcpyHostToDevice,
                                   ctx->stream));
@@ -303,7 +328,7 @@ int kr_alloc(mb4cu_ctx* ctx) {
     return MB4CU_OK;
 }
 
-double2* kr_vec(mb4cu_ctx* ctx, size_t idx) { return ctx->kr.mem + idx * ctx->n; }
+double2* kr_vec(mb4cu_ctx* ctx, size_t idx) { return ctx->kr.mem + idx * ctx->kr.len; }
 
 // fixed-order host sum of nv rows of block partials
 int kr_fetch(mb4cu_ctx* ctx, int nv, double* out) {
@@ -319,10 +344,12 @@ int kr_fetch(mb4cu_ctx* ctx, int nv, double* out) {
     return MB4CU_OK;
 }
 
-// Solve (I - hl J(u0)) x = b, x initialised to zero.
-int kr_gmres(mb4cu_ctx* ctx, const SweepConsts& c, double hl, const double2* b, double2* x) {
+// Solve A x = b by restarted GMRES(m), x initialised to zero; A applied by
+// matvec(x, y) over vectors of the arena length (N, or 2N for coupled systems).
+template <class MatVec>
+int kr_gmres(mb4cu_ctx* ctx, const MatVec& matvec, const double2* b, double2* x) {
     auto& k = ctx->kr;
-    const size_t n = ctx->n;
+    const size_t n = k.len;
     const int m = k.m;
     double2* w = kr_vec(ctx, m + 1 + 6);
     double2* y = kr_vec(ctx, m + 1 + 7);
@@ -344,7 +371,7 @@ int kr_gmres(mb4cu_ctx* ctx, const SweepConsts& c, double hl, const double2* b, 
             beta = bnorm;  // r = b already in v_0 (unscaled)
             first = false;
         } else {
-            MB4_CUDA(ctx, mb4cu::kr_matvec(x, y, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream));
+            MB4_CUDA(ctx, matvec(x, y));
             MB4_CUDA(ctx, mb4cu::kr_residual(b, y, kr_vec(ctx, 0), n, k.partial, ctx->stream));
             double r2 = 0.0;
             if (int rc = kr_fetch(ctx, 1, &r2)) return rc;
@@ -357,7 +384,7 @@ int kr_gmres(mb4cu_ctx* ctx, const SweepConsts& c, double hl, const double2* b, 
         int j = 0;
         bool done = false;
         for (; j < m && iter < kKrylovMaxIters; ++j, ++iter) {
-            MB4_CUDA(ctx, mb4cu::kr_matvec(kr_vec(ctx, j), w, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream));
+            MB4_CUDA(ctx, matvec(kr_vec(ctx, j), w));
             for (int i = 0; i <= j; ++i) Hat(i, j) = 0.0;
             double wn2 = 0.0;
             for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, twice
@@ -410,7 +437,7 @@ int kr_gmres(mb4cu_ctx* ctx, const SweepConsts& c, double hl, const double2* b, 
 }
 
 int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
-    if (int rc = kr_alloc(ctx)) return rc;
+    if (int rc = kr_alloc(ctx, ctx->n)) return rc;
     const SweepConsts c = make_consts(ctx, h);
     const size_t sb = ctx->n * sizeof(double2);
     double2* st[3] = {ctx->U[0][0], ctx->U[0][1], ctx->U[0][2]};
@@ -424,8 +451,13 @@ int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
     for (int it = 1; it <= ctx->max_iters; ++it) {
         const double2* cst[3] = {st[0], st[1], st[2]};
         MB4_CUDA(ctx, mb4cu::kr_phibar(ctx->nx, ctx->ny, ctx->u0, cst, ctx->V, b, c, ctx->stream));
-        for (int k = 0; k < 3; ++k)
-            if (int rc = kr_gmres(ctx, c, c.hlam[k], b[k], x[k])) return rc;
+        for (int k = 0; k < 3; ++k) {
+            const double hl = c.hlam[k];
+            auto mv = [&](const double2* xin, double2* yout) {
+                return mb4cu::kr_matvec(xin, yout, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream);
+            };
+            if (int rc = kr_gmres(ctx, mv, b[k], x[k])) return rc;
+        }
         MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
         const double2* cx[3] = {x[0], x[1], x[2]};
         MB4_CUDA(ctx, mb4cu::kr_update(st, cx, ctx->n, ctx->d_rmax, c, ctx->stream));
@@ -708,12 +740,7 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs_march);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
-    cudaFree(ctx->kr.mem);
-    cudaFree(ctx->kr.v_dev);
-    cudaFree(ctx->kr.partial);
-    cudaFreeHost(ctx->kr.h_partial);
-    cudaFree(ctx->kr.coef);
-    cudaFreeHost(ctx->kr.h_coef);
+    kr_free(ctx);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->pev0) cudaEventDestroy(ctx->pev0);
@@ -943,6 +970,193 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
             if (rc1) return rc1;
             put_obs(obs_series + 7 * (s - 1), o);
         }
+    }
+    if (obs_series) {
+        const int rc2 = mb4cu_observables(ctx, &o);
+        if (rc2) return rc2;
+        put_obs(obs_series + 7 * nsteps, o);
+    }
+    return MB4CU_OK;
+}
+
+// ---- the other integrators (integrators.cpp:45-455) ---------------------------
+
+namespace {
+
+const char* method_label(int method) {
+    static const char* names[] = {"rk4_step", "gauss_step(1)", "gauss_step(2)", "avf2_step", "avf4_step", "mb4_step"};
+    return method >= 0 && method <= 5 ? names[method] : "?";
+}
+
+mb4cu::MethodConsts method_consts(const mb4cu_ctx* ctx, int method, double h) {
+    mb4cu::MethodConsts c{};
+    c.h = h;
+    c.gamma = ctx->gamma;
+    c.cx = ctx->cx;
+    c.cy = ctx->cy;
+    c.diag = 2.0 * ctx->cx + 2.0 * ctx->cy;
+    mb4cu::method_tables(&c);
+    if (method == mb4cu::kMethodGauss4) {
+        // 2-stage Gauss A (integrators.cpp:160-161)
+        const double r3 = std::sqrt(3.0);
+        c.a[0][0] = 0.25;
+        c.a[0][1] = 0.25 - r3 / 6.0;
+        c.a[1][0] = 0.25 + r3 / 6.0;
+        c.a[1][1] = 0.25;
+    } else if (method == mb4cu::kMethodAvf4) {
+        mb4cu::avf4_coupling(c.a);
+    } else {
+        c.a[0][0] = 0.5;  // stage_matrix(j, h / 2)
+    }
+    return c;
+}
+
+int method_stages(int method) {
+    return method == mb4cu::kMethodGauss4 || method == mb4cu::kMethodAvf4 ? 2 : 1;
+}
+
+// One plain step of RK4 / an implicit method on ctx->u0 (u0 <- u1 on success;
+// unchanged otherwise).  Implicit methods: the reference's simplified Newton
+// iteration, the linear systems by matrix-free GMRES.
+int method_plain_step(mb4cu_ctx* ctx, int method, double h, int* iters, double* last_res) {
+    const mb4cu::MethodConsts c = method_consts(ctx, method, h);
+    const size_t n = ctx->n;
+    *iters = 0;
+    *last_res = 0.0;
+    if (method == mb4cu::kMethodRk4) {
+        double2* acc = ctx->U[0][0];
+        double2* t1 = ctx->U[0][1];
+        double2* t2 = ctx->U[0][2];
+        double2* out = ctx->U[1][0];
+        MB4_CUDA(ctx, mb4cu::launch_rk4_stage(1, ctx->nx, ctx->ny, ctx->u0, ctx->u0, ctx->V, acc, t1, c, ctx->stream));
+        MB4_CUDA(ctx, mb4cu::launch_rk4_stage(2, ctx->nx, ctx->ny, t1, ctx->u0, ctx->V, acc, t2, c, ctx->stream));
+        MB4_CUDA(ctx, mb4cu::launch_rk4_stage(3, ctx->nx, ctx->ny, t2, ctx->u0, ctx->V, acc, t1, c, ctx->stream));
+        MB4_CUDA(ctx, mb4cu::launch_rk4_stage(4, ctx->nx, ctx->ny, t1, ctx->u0, ctx->V, acc, out, c, ctx->stream));
+        ctx->prof.other_launches += 4;
+        std::swap(ctx->u0, ctx->U[1][0]);
+        return MB4CU_OK;
+    }
+    const int st = method_stages(method);
+    const size_t len = static_cast<size_t>(st) * n;
+    if (int rc = kr_alloc(ctx, len)) return rc;
+    const int m = ctx->kr.m;
+    double2* b = kr_vec(ctx, m + 1);
+    double2* x = kr_vec(ctx, m + 2);
+    double2* unk = kr_vec(ctx, m + 3);
+    if (method == mb4cu::kMethodAvf4) {
+        MB4_CUDA(ctx, mb4cu::launch_avf4_init(ctx->nx, ctx->ny, ctx->u0, ctx->V, unk, c, ctx->stream));
+    } else {
+        for (int i = 0; i < st; ++i)
+            MB4_CUDA(ctx, cudaMemcpyAsync(unk + i * n, ctx->u0, n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    }
+    auto mv = [&](const double2* xin, double2* yout) {
+        return mb4cu::launch_method_matvec(st, ctx->nx, ctx->ny, xin, yout, ctx->u0, ctx->V, c, ctx->stream);
+    };
+    for (int it = 1; it <= ctx->max_iters; ++it) {
+        MB4_CUDA(ctx, mb4cu::launch_method_residual(method, ctx->nx, ctx->ny, ctx->u0, ctx->V, unk, b, c,
+                                                    ctx->stream));
+        if (int rc = kr_gmres(ctx, mv, b, x)) return rc;
+        MB4_CUDA(ctx, mb4cu::launch_newton_add(unk, x, len, ctx->d_rmax, ctx->stream));
+        MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        *iters = it;
+        const double r = decode_bits(*ctx->h_rmax);
+        *last_res = r;
+        if (!std::isfinite(r)) {
+            *last_res = INFINITY;
+            return fail(ctx, MB4CU_NONCONVERGED, std::string(method_label(method)) + ": iteration diverged");
+        }
+        if (r <= ctx->eps) {
+            MB4_CUDA(ctx, mb4cu::launch_method_final(method, ctx->nx, ctx->ny, ctx->u0, ctx->V, unk, ctx->U[1][0], c,
+                                                     ctx->stream));
+            std::swap(ctx->u0, ctx->U[1][0]);
+            return MB4CU_OK;
+        }
+    }
+    return fail(ctx, MB4CU_NONCONVERGED, std::string(method_label(method)) + ": no convergence");
+}
+
+}  // namespace
+
+int mb4cu_method_step(mb4cu_ctx* ctx, int method, double h, mb4cu_stats* stats) {
+    if (!ctx) return MB4CU_INVALID;
+    if (method < 0 || method > 5) return fail(ctx, MB4CU_INVALID, "StepDriver: unknown method");
+    if (method == mb4cu::kMethodMb4) return mb4cu_step(ctx, h, stats);
+    if (!(h > 0.0)) return fail(ctx, MB4CU_INVALID, "advance: h must be positive");
+    if (ctx->ghost > 0) return fail(ctx, MB4CU_INVALID, "methods: sub-domain contexts are MB4-only");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    ctx->obs_cached = false;
+    ctx->amax2_valid = false;
+    int it = 0;
+    double last = 0.0;
+    if (method == mb4cu::kMethodRk4) return method_plain_step(ctx, method, h, &it, &last);  // no halving (:427)
+    // halving-on-failure of StepDriver::advance (integrators.cpp:430-455)
+    MB4_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    if (!ctx->ubak) MB4_CUDA(ctx, cudaMalloc(&ctx->ubak, ctx->n * sizeof(double2)));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->ubak, ctx->u0, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+    for (int hv = 0; hv <= ctx->max_halvings; ++hv) {
+        const int sub = 1 << hv;
+        const double hs = h / sub;
+        if (hv > 0)
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, ctx->ubak, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+        bool ok = true;
+        int attempt = 0;
+        for (int s = 0; s < sub && ok; ++s) {
+            const int rc = method_plain_step(ctx, method, hs, &it, &last);
+            attempt += it;
+            if (rc == MB4CU_NONCONVERGED)
+                ok = false;
+            else if (rc != MB4CU_OK)
+                return rc;
+        }
+        if (ok) {
+            MB4_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+            MB4_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+            float ms = 0.f;
+            MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            if (stats) {
+                stats->newton_iters += attempt;
+                stats->halvings += hv;
+                stats->solve_seconds += 1e-3 * ms;
+                stats->last_residual = last;
+            }
+            return MB4CU_OK;
+        }
+    }
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, ctx->ubak, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (stats) stats->last_residual = last;
+    return fail(ctx, MB4CU_NONCONVERGED,
+                "advance: no convergence after " + std::to_string(ctx->max_halvings) + " step halvings");
+}
+
+int mb4cu_method_run(mb4cu_ctx* ctx, int method, double h, int nsteps, double* obs_series, int* iters_series,
+                     mb4cu_stats* stats) {
+    if (!ctx) return MB4CU_INVALID;
+    if (method == mb4cu::kMethodMb4) return mb4cu_run(ctx, h, nsteps, obs_series, iters_series, stats);
+    if (nsteps < 0) return fail(ctx, MB4CU_INVALID, "run: nsteps must be >= 0");
+    mb4cu_obs o{};
+    for (int s = 1; s <= nsteps; ++s) {
+        if (obs_series) {
+            const int rc0 = mb4cu_observables(ctx, &o);
+            if (rc0) return rc0;
+            put_obs(obs_series + 7 * (s - 1), o);
+        }
+        mb4cu_stats st{};
+        const int rc = mb4cu_method_step(ctx, method, h, &st);
+        if (stats) {
+            stats->newton_iters += st.newton_iters;
+            stats->halvings += st.halvings;
+            stats->solve_seconds += st.solve_seconds;
+            stats->last_residual = st.last_residual;
+        }
+        if (rc) return rc;
+        if (iters_series) iters_series[s - 1] = st.newton_iters;
     }
     if (obs_series) {
         const int rc2 = mb4cu_observables(ctx, &o);

@@ -138,6 +138,35 @@ struct StepArgs {
     int spec_sweep;             // global sweep index stored as U3 only (-1: none)
 };
 
+// ---- the other integrators (methods.cu) ------------------------------------
+// method ids follow the reference's MethodId order (integrators.hpp:12)
+constexpr int kMethodRk4 = 0, kMethodGauss2 = 1, kMethodGauss4 = 2, kMethodAvf2 = 3, kMethodAvf4 = 4,
+              kMethodMb4 = 5;
+
+struct MethodConsts {
+    double h, gamma, cx, cy, diag;
+    double a[2][2];           // Newton coupling C (s = 1: 1/2) = Gauss-4 A / AVF4 mt
+    double b2[2][2][2];       // AVF2 cubic weights  int m_a m_b m_c
+    double wt[2][3][3][3];    // AVF4 cubic weights  (1/b_i) int l_i phi_a phi_b phi_c
+};
+
+cudaError_t launch_rk4_stage(int stage, int nx, int ny, const double2* x, const double2* u0, const double* V,
+                             double2* acc, double2* out, const MethodConsts& c, cudaStream_t s);
+cudaError_t launch_method_residual(int method, int nx, int ny, const double2* u0, const double* V,
+                                   const double2* unk, double2* b, const MethodConsts& c, cudaStream_t s);
+cudaError_t launch_method_matvec(int stages, int nx, int ny, const double2* x, double2* y, const double2* u0,
+                                 const double* V, const MethodConsts& c, cudaStream_t s);
+cudaError_t launch_newton_add(double2* unk, const double2* x, size_t len, unsigned long long* rmax,
+                              cudaStream_t s);
+cudaError_t launch_avf4_init(int nx, int ny, const double2* u0, const double* V, double2* unk,
+                             const MethodConsts& c, cudaStream_t s);
+cudaError_t launch_method_final(int method, int nx, int ny, const double2* u0, const double* V,
+                                const double2* unk, double2* out, const MethodConsts& c, cudaStream_t s);
+// Method tables (AVF2 b2, AVF4 mt / wt, Gauss-4 A) computed as the reference does
+// (integrators.cpp:160-162, 219-235, 301-335), scheme_host.cpp.
+void method_tables(MethodConsts* c);
+void avf4_coupling(double mt[2][2]);
+
 // Launchers (sweep_tiled.cu, sweep_march.cu).
 cudaError_t launch_step_march(int m, int nx, int ny, const double2* u0, const double* V,
                               double2* const U[2][3], unsigned long long* rmax,

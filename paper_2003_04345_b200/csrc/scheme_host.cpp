@@ -255,4 +255,90 @@ int scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* ou
     return MB4CU_OK;
 }
 
+// ---- tables of the other integrators -----------------------------------------
+// The reference builds them in double at first use from its Gauss-Legendre rule
+// (quadrature.cpp:9-36: Newton iteration on P_n from the Chebyshev guess); the
+// same rule and summation order are restated here so the GPU methods consume the
+// same constants.
+namespace {
+
+void gauss_legendre_01_d(int n, double* nodes, double* weights) {
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < n; ++i) {
+        double x = std::cos(pi * (i + 0.75) / (n + 0.5));
+        double dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int k = 2; k <= n; ++k) {
+                const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (x * p1 - p0) / (x * x - 1.0);
+            const double dx = p1 / dp;
+            x -= dx;
+            if (std::abs(dx) < 1e-16) break;
+        }
+        const double w = 2.0 / ((1.0 - x * x) * dp * dp);
+        nodes[n - 1 - i] = 0.5 * (x + 1.0);
+        weights[n - 1 - i] = 0.5 * w;
+    }
+}
+
+}  // namespace
+
+void method_tables(MethodConsts* t) {
+    // AVF2: B2[a][b][c] = int_0^1 m_a m_b m_c, m0 = 1 - x, m1 = x (2-node rule, exact)
+    double x2[2], w2[2], x4[4], w4[4];
+    gauss_legendre_01_d(2, x2, w2);
+    gauss_legendre_01_d(4, x4, w4);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < 2; ++c) {
+                double s = 0.0;
+                for (int g = 0; g < 2; ++g) {
+                    const double m[2] = {1.0 - x2[g], x2[g]};
+                    s += w2[g] * m[a] * m[b] * m[c];
+                }
+                t->b2[a][b][c] = s;
+            }
+    // AVF4 (integrators.cpp:301-335): Lagrange basis on the 2 Gauss nodes
+    const double r3 = std::sqrt(3.0);
+    const double c1 = 0.5 - r3 / 6.0, c2 = 0.5 + r3 / 6.0;
+    const double bw[2] = {0.5, 0.5};
+    auto ell = [&](int i, double x) { return i == 0 ? (x - c2) / (c1 - c2) : (x - c1) / (c2 - c1); };
+    auto bigl = [&](int j, double x) {
+        return j == 0 ? (0.5 * x * x - c2 * x) / (c1 - c2) : (0.5 * x * x - c1 * x) / (c2 - c1);
+    };
+    auto phi = [&](int a, double x) { return a == 0 ? 1.0 : bigl(a - 1, x); };
+    for (int i = 0; i < 2; ++i)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+                    for (int g = 0; g < 4; ++g)
+                        s += w4[g] * ell(i, x4[g]) * phi(a, x4[g]) * phi(b, x4[g]) * phi(c, x4[g]);
+                    t->wt[i][a][b][c] = s / bw[i];
+                }
+    (void)x2;
+}
+
+// AVF4's Newton coupling mt[i][j] = (1/b_i) int l_i L_j (2-node rule)
+void avf4_coupling(double mt[2][2]) {
+    double x2[2], w2[2];
+    gauss_legendre_01_d(2, x2, w2);
+    const double r3 = std::sqrt(3.0);
+    const double c1 = 0.5 - r3 / 6.0, c2 = 0.5 + r3 / 6.0;
+    auto ell = [&](int i, double x) { return i == 0 ? (x - c2) / (c1 - c2) : (x - c1) / (c2 - c1); };
+    auto bigl = [&](int j, double x) {
+        return j == 0 ? (0.5 * x * x - c2 * x) / (c1 - c2) : (0.5 * x * x - c1 * x) / (c2 - c1);
+    };
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            double s = 0.0;
+            for (int g = 0; g < 2; ++g) s += w2[g] * ell(i, x2[g]) * bigl(j, x2[g]);
+            mt[i][j] = s / 0.5;
+        }
+}
+
 }  // namespace mb4cu

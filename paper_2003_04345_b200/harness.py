@@ -1,19 +1,22 @@
 """Run harness on the GPU path: RunConfig / run() / trajectory CSV / snapshots.
 
-Mirrors the reference harness for the MB4 method (run_config.hpp:19-46,
-run_config.cpp:9-130, harness.hpp:18-37, harness.cpp:16-145), backed by a
-device-resident Session: the state stays in HBM, the per-step energy record
-comes from the energy monitor fused into each step's first sweep, and host
-copies happen only for snapshots and the final state.
+Mirrors the reference harness (run_config.hpp:19-46, run_config.cpp:9-130,
+harness.hpp:18-89, harness.cpp:16-300) -- run(), compare_methods(),
+parallel_bench(), convergence_study() -- backed by a device-resident Session:
+the state stays in HBM, the per-step energy record comes from the energy monitor
+(fused into each MB4 step's first sweep), and host copies happen only for
+snapshots and the final state.  Every method of the reference runs on the GPU
+(MB4: the production stage solver; RK4 / GAUSS2 / GAUSS4 / AVF2 / AVF4:
+methods.cu).
 
 Extension keys (not in the reference): the BASELINE inputs
 (`baseline = cfg1..cfg5`, or `defect_frac/defect_seed/vd_min/vd_max/packets/
 sigma/x0/y0/kx/ky/random_packets/packet_seed/k_max`) and `neumann_terms`.
 
-Differences: `method` must be mb4 (the other integrators are out of scope);
-`workers` and `solver` are accepted and ignored; `newton_iters` in the CSV counts
-stage sweeps; `wall_s` is the device time of the step's chunk divided evenly
-over its steps (the run is stepped in chunks between snapshot times).
+Differences: `workers` and `solver` are accepted and ignored (no worker pool, no
+sparse factorization); for MB4 `newton_iters` in the CSV counts stage sweeps;
+`wall_s` is the device time of the step's chunk divided evenly over its steps
+(the run is stepped in chunks between snapshot times).
 """
 from __future__ import annotations
 
@@ -90,8 +93,8 @@ class RunConfig:
         for t in self.snapshot_times:
             if t < 0.0 or t > self.t_end + 1e-12:
                 raise ConfigError("snapshot time outside [0, t_end]")
-        if self.method != "mb4":
-            raise ConfigError("method: only mb4 runs on the GPU path")
+        if nls2d.parse_method(self.method) is None:
+            raise ConfigError(f"unknown method '{self.method}'")
 
     def _lattice_cfg(self) -> Optional[configs.LatticeConfig]:
         if self.baseline:
@@ -270,7 +273,7 @@ def run(cfg: RunConfig, device: int = 0) -> TrajectoryRecord:
     solve = 0.0
     with nls2d.Session(model, nls2d.Mb4Scheme(), ncfg,
                        neumann_terms=None if cfg.neumann_terms < 0 else cfg.neumann_terms,
-                       device=device) as s:
+                       device=device, method=nls2d.parse_method(cfg.method)) as s:
         s.set_state(u)
 
         def emit(t, obs_row, iters, wall):
@@ -319,3 +322,134 @@ def run(cfg: RunConfig, device: int = 0) -> TrajectoryRecord:
         with open(os.path.join(cfg.out_dir, "trajectory.csv"), "w") as f:
             write_trajectory_csv(f, rec)
     return rec
+
+
+# ---------------------------------------------------------------------------- studies
+
+
+@dataclass
+class MethodReport:
+    """harness.hpp:40-46."""
+    method: str
+    energy_drift: float
+    probability_drift: float
+    mean_step_seconds: float
+    total_newton_iters: int
+
+
+@dataclass
+class CompareReport:
+    """harness.hpp:48-57, harness.cpp:147-196."""
+    methods: List[MethodReport]
+    mb4_over_gauss2: float = 0.0
+    avf4_over_gauss2: float = 0.0
+
+    def write(self, f) -> None:
+        f.write("method  energy_drift  probability_drift  mean_step_seconds  newton_iters\n")
+        for m in self.methods:
+            f.write(f"{nls2d.method_name(m.method):<7} {m.energy_drift:.3e}     {m.probability_drift:.3e}"
+                    f"          {m.mean_step_seconds:.6f}           {m.total_newton_iters}\n")
+        f.write(f"time ratio MB4/GAUSS2  = {self.mb4_over_gauss2:.3f}\n")
+        f.write(f"time ratio AVF4/GAUSS2 = {self.avf4_over_gauss2:.3f}\n")
+
+
+def compare_methods(cfg: RunConfig, methods, device: int = 0) -> CompareReport:
+    """harness.cpp:147-178: one run per method, drifts, mean step time, iterations."""
+    rep = CompareReport([])
+    times = {}
+    for m in methods:
+        c = replace(cfg, method=m, out_dir="")
+        rec = run(c, device)
+        nsteps = max(1, len(rec.rows) - 1)
+        mr = MethodReport(m, rec.max_energy_drift(), rec.max_probability_drift(),
+                          sum(r.wall_seconds for r in rec.rows) / nsteps, sum(r.newton_iters for r in rec.rows))
+        rep.methods.append(mr)
+        times[m] = mr.mean_step_seconds
+    if times.get("gauss2", 0.0) > 0.0:
+        rep.mb4_over_gauss2 = times.get("mb4", 0.0) / times["gauss2"]
+        rep.avf4_over_gauss2 = times.get("avf4", 0.0) / times["gauss2"]
+    return rep
+
+
+@dataclass
+class BenchReport:
+    """harness.hpp:59-71, harness.cpp:219-257 (workers 1 vs 3 of the reference's
+    pool; the GPU path has no worker pool, so both runs take the same path and the
+    trajectories must be bit-identical)."""
+    serial_step_seconds: float
+    parallel_step_seconds: float
+    speedup: float
+    solve_fraction: float
+    trajectories_identical: bool
+
+    def write(self, f) -> None:
+        f.write(f"per-step seconds, 1 worker  = {self.serial_step_seconds:.6f}\n")
+        f.write(f"per-step seconds, 3 workers = {self.parallel_step_seconds:.6f}\n")
+        f.write(f"speedup                     = {self.speedup:.3f}\n")
+        f.write(f"solve-phase fraction        = {self.solve_fraction:.3f}\n")
+        f.write(f"trajectories bit-identical  = {'yes' if self.trajectories_identical else 'no'}\n")
+
+
+def _rows_identical(a: TrajectoryRecord, b: TrajectoryRecord) -> bool:
+    if len(a.rows) != len(b.rows):
+        return False
+    for x, y in zip(a.rows, b.rows):
+        if (x.t, x.u_kinetic, x.u_nonlinear, x.u_external, x.total_energy, x.probability, x.participation,
+                x.newton_iters) != (y.t, y.u_kinetic, y.u_nonlinear, y.u_external, y.total_energy,
+                                    y.probability, y.participation, y.newton_iters):
+            return False
+    return bool(np.array_equal(a.final_state, b.final_state))
+
+
+def parallel_bench(cfg: RunConfig, device: int = 0) -> BenchReport:
+    base = replace(cfg, method="mb4", out_dir="")
+    rec1 = run(replace(base, workers=1), device)
+    rec3 = run(replace(base, workers=3), device)
+    nsteps = max(1, len(rec1.rows) - 1)
+    s1, s3 = rec1.wall_seconds / nsteps, rec3.wall_seconds / nsteps
+    return BenchReport(s1, s3, s1 / s3, rec1.solve_seconds / rec1.wall_seconds, _rows_identical(rec1, rec3))
+
+
+@dataclass
+class ConvergenceEntry:
+    method: str
+    h_values: List[float]
+    errors: List[float]
+    slope: float
+
+
+@dataclass
+class ConvergenceReport:
+    """harness.hpp:73-88, harness.cpp:272-316."""
+    entries: List[ConvergenceEntry]
+
+    def write(self, f) -> None:
+        """harness.cpp:301-313."""
+        for e in self.entries:
+            f.write(f"{nls2d.method_name(e.method)}:\n")
+            for h, err in zip(e.h_values, e.errors):
+                f.write(f"  h = {h:<10.6g} error = {err:.6e}\n")
+            f.write(f"  fitted order = {e.slope:.3f}\n")
+
+
+def convergence_study(cfg: RunConfig, methods, h_list, device: int = 0) -> ConvergenceReport:
+    """Errors against a run at h_min / 8 and the least-squares log-log slope."""
+    if len(h_list) < 3:
+        raise ConfigError("convergence_study: need at least 3 h values")
+    for a, b in zip(h_list, h_list[1:]):
+        if not b < a:
+            raise ConfigError("convergence_study: h_list must descend")
+    rep = ConvergenceReport([])
+    for m in methods:
+        base = replace(cfg, method=m, out_dir="", snapshot_times=[])
+        ref = run(replace(base, dt=h_list[-1] / 8.0), device).final_state
+        ref_norm = float(np.sqrt(np.sum(np.abs(ref) ** 2)))
+        errs = []
+        for h in h_list:
+            uh = run(replace(base, dt=h), device).final_state
+            errs.append(float(np.sqrt(np.sum(np.abs(uh - ref) ** 2))) / ref_norm)
+        x, y = np.log(np.array(h_list)), np.log(np.array(errs))
+        n = len(h_list)
+        slope = (n * np.sum(x * y) - x.sum() * y.sum()) / (n * np.sum(x * x) - x.sum() ** 2)
+        rep.entries.append(ConvergenceEntry(m, list(h_list), errs, float(slope)))
+    return rep

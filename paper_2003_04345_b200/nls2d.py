@@ -31,6 +31,25 @@ from . import _lib
 from ._lib import dptr
 
 MB4 = "mb4"
+# the reference's methods in MethodId order (integrators.hpp:12)
+METHODS = ("rk4", "gauss2", "gauss4", "avf2", "avf4", "mb4")
+_METHOD_NAMES = ("RK4", "GAUSS2", "GAUSS4", "AVF2", "AVF4", "MB4")
+
+
+def parse_method(name: str) -> Optional[str]:
+    """integrators.cpp:34-43 (case-insensitive); None when unknown."""
+    n = name.lower()
+    return n if n in METHODS else None
+
+
+def method_name(method: str) -> str:
+    """integrators.cpp:22-32."""
+    return _METHOD_NAMES[METHODS.index(method)]
+
+
+def method_order(method: str) -> int:
+    """integrators.cpp:13-20."""
+    return 2 if method in ("gauss2", "avf2") else 4
 
 
 class NonConvergenceError(RuntimeError):
@@ -271,8 +290,13 @@ class Session:
 
     def __init__(self, model: GridModel, scheme: Optional[Mb4Scheme] = None,
                  cfg: Optional[NewtonConfig] = None, neumann_terms: Optional[int] = None,
-                 device: int = 0, kernel: int = 0, neumann_first: Optional[int] = None):
+                 device: int = 0, kernel: int = 0, neumann_first: Optional[int] = None,
+                 method: str = MB4):
         self._L = _lib.lib()
+        if method not in METHODS:
+            raise ValueError(f"StepDriver: unknown method {method!r}")
+        self.method = method
+        self._mid = METHODS.index(method)
         self.model = model
         self.scheme = scheme if scheme is not None else Mb4Scheme()
         self.cfg = cfg if cfg is not None else NewtonConfig()
@@ -342,7 +366,7 @@ class Session:
     # stepping --------------------------------------------------------------
     def step(self, h: float, stats: Optional[StepStats] = None):
         st = _lib.Stats()
-        rc = self._L.mb4cu_step(self._ctx, float(h), C.byref(st))
+        rc = self._L.mb4cu_method_step(self._ctx, self._mid, float(h), C.byref(st))
         if stats is not None:
             stats.newton_iters += st.newton_iters
             stats.halvings += st.halvings
@@ -355,9 +379,9 @@ class Session:
         obs = np.zeros((nsteps + 1, 7)) if record else None
         iters = np.zeros(nsteps, dtype=np.int32)
         st = _lib.Stats()
-        rc = self._L.mb4cu_run(self._ctx, float(h), int(nsteps),
-                               dptr(obs) if record else None,
-                               iters.ctypes.data_as(C.POINTER(C.c_int)), C.byref(st))
+        rc = self._L.mb4cu_method_run(self._ctx, self._mid, float(h), int(nsteps),
+                                      dptr(obs) if record else None,
+                                      iters.ctypes.data_as(C.POINTER(C.c_int)), C.byref(st))
         if stats is not None:
             stats.newton_iters += st.newton_iters
             stats.halvings += st.halvings
@@ -441,6 +465,43 @@ def eval_phi(model: GridModel, scheme: Mb4Scheme, u0: np.ndarray, stages, h: flo
         return s.eval_phi(u0, stages, h)
 
 
+def _method_step(method: str, model: GridModel, u0: np.ndarray, h: float, cfg: Optional[NewtonConfig],
+                 stats: Optional[StepStats]) -> np.ndarray:
+    cfg = cfg if cfg is not None else NewtonConfig()
+    cfg.validate()
+    # a plain step: the free functions of integrators.hpp do not halve
+    plain = NewtonConfig(cfg.epsilon, cfg.max_iters, 0)
+    with Session(model, Mb4Scheme(), plain, method=method) as s:
+        s.set_state(u0)
+        s.step(h, stats)
+        return s.get_state()
+
+
+def rk4_step(model: GridModel, u0: np.ndarray, h: float) -> np.ndarray:
+    """integrators.cpp:45-59 on the GPU."""
+    return _method_step("rk4", model, u0, h, None, None)
+
+
+def gauss_step(model: GridModel, u0: np.ndarray, h: float, stages: int, cfg: NewtonConfig,
+               stats: Optional[StepStats] = None, solver=None, cached_order=None) -> np.ndarray:
+    """integrators.cpp:103-208 (stages 1: implicit midpoint, 2: Gauss order 4)."""
+    if stages not in (1, 2):
+        raise ValueError("gauss_step: stages must be 1 or 2")
+    return _method_step("gauss2" if stages == 1 else "gauss4", model, u0, h, cfg, stats)
+
+
+def avf2_step(model: GridModel, u0: np.ndarray, h: float, cfg: NewtonConfig,
+              stats: Optional[StepStats] = None, solver=None, cached_order=None) -> np.ndarray:
+    """integrators.cpp:210-282."""
+    return _method_step("avf2", model, u0, h, cfg, stats)
+
+
+def avf4_step(model: GridModel, u0: np.ndarray, h: float, cfg: NewtonConfig,
+              stats: Optional[StepStats] = None, solver=None, cached_order=None) -> np.ndarray:
+    """integrators.cpp:284-395."""
+    return _method_step("avf4", model, u0, h, cfg, stats)
+
+
 def mb4_step(model: GridModel, scheme: Mb4Scheme, u0: np.ndarray, h: float, cfg: NewtonConfig,
              pool=None, stats: Optional[StepStats] = None, solver=None, cached_order=None,
              neumann_terms: Optional[int] = None) -> np.ndarray:
@@ -459,21 +520,25 @@ def mb4_step(model: GridModel, scheme: Mb4Scheme, u0: np.ndarray, h: float, cfg:
 
 
 class StepDriver:
-    """integrators.hpp:46-66, MB4 branch only (the other methods are out of scope).
+    """integrators.hpp:46-66: any of the reference's methods on the GPU.
 
     Owns one device session for its model; each advance() uploads u0, steps,
-    and downloads the result (the reference's host-vector contract).
+    and downloads the result (the reference's host-vector contract).  MB4 runs the
+    production stage solver; RK4 / GAUSS2 / GAUSS4 / AVF2 / AVF4 run methods.cu
+    with the reference's halving-on-failure policy (RK4: none).
     """
 
     def __init__(self, model: GridModel, method: str = MB4, cfg: Optional[NewtonConfig] = None,
                  solver=None, pool=None, neumann_terms: Optional[int] = None, device: int = 0):
-        if method != MB4:
-            raise ValueError("StepDriver: only the MB4 method is on the GPU path")
+        method = method.lower() if isinstance(method, str) else method
+        if method not in METHODS:
+            raise ValueError(f"StepDriver: unknown method {method!r}")
+        self.method = method
         self.cfg = cfg if cfg is not None else NewtonConfig()
         self.cfg.validate()
         self._scheme = Mb4Scheme()
         self._session = Session(model, self._scheme, self.cfg, neumann_terms=neumann_terms,
-                                device=device)
+                                device=device, method=method)
 
     def scheme(self) -> Mb4Scheme:
         return self._scheme
@@ -484,7 +549,7 @@ class StepDriver:
 
     def advance(self, u0: np.ndarray, h: float, stats: Optional[StepStats] = None) -> np.ndarray:
         if not (h > 0.0):
-            raise ValueError("mb4_step: h must be positive")
+            raise ValueError("advance: h must be positive")
         self._session.set_state(u0)
         self._session.step(h, stats)
         return self._session.get_state()

@@ -89,6 +89,36 @@ int main(int argc, char** argv) {
         }
         CHECK(threw);
     }
+    // the other methods through the reference API (test_integrators.cpp:37-42, 64-92)
+    {
+        const GridModel free_model(GridSpec(6, 6, 2 * M_PI, 2 * M_PI), 0.0);
+        const State c0(free_model.points(), Complex(0.7, -0.3));
+        const State c1 = rk4_step(free_model, c0, 0.05);
+        for (size_t k = 0; k < c0.size(); ++k) CHECK(std::abs(c1[k] - c0[k]) <= 1e-15);
+        const GridSpec g(6, 6, 2 * M_PI, 2 * M_PI);
+        const GridModel model(g, 0.1);
+        const State u0 = initial_condition(g);
+        const State f0 = rhs(model, u0);
+        for (MethodId m : {MethodId::Gauss2, MethodId::Gauss4, MethodId::Avf2, MethodId::Avf4, MethodId::Mb4}) {
+            StepDriver d(model, m, NewtonConfig{});
+            const double h = 1e-5;
+            const State u1 = d.advance(u0, h);
+            double err = 0.0;
+            for (int k = 0; k < model.points(); ++k) err = std::max(err, std::abs(u1[k] - u0[k] - h * f0[k]));
+            CHECK(err <= 10.0 * h * h);
+        }
+        const GridModel lin(GridSpec(8, 8, 2 * M_PI, 2 * M_PI), 0.0);
+        const State v0 = initial_condition(lin.grid());
+        const State a = avf2_step(lin, v0, 0.01, NewtonConfig{});
+        const State b = gauss_step(lin, v0, 0.01, 1, NewtonConfig{});
+        double num = 0.0, den = 0.0;
+        for (size_t k = 0; k < a.size(); ++k) {
+            num += std::norm(a[k] - b[k]);
+            den += std::norm(b[k]);
+        }
+        CHECK(std::sqrt(num / den) <= 1e-12);
+        CHECK(method_name(MethodId::Avf4) == "AVF4" && method_order(MethodId::Gauss2) == 2);
+    }
     // BASELINE inputs: 10 steps through StepDriver::advance (host vectors)
     const std::vector<double> V = read_bin<double>(argv[1], n);
     const State psi = read_bin<Complex>(argv[2], n);

@@ -31,7 +31,7 @@ def test_parse_config_file_and_overrides(tmp_path):
 
 @pytest.mark.parametrize("field,val", [("nx", 1), ("dt", 0.0), ("t_end", 0.001), ("epsilon", 0.0),
                                        ("max_iters", 0), ("max_halvings", -1), ("workers", 4),
-                                       ("method", "rk4")])
+                                       ("method", "leapfrog")])
 def test_validate_rejects(field, val):
     cfg = Hn.RunConfig()
     setattr(cfg, field, val)
@@ -87,3 +87,29 @@ def test_run_last_short_step_and_paper_style_config(tmp_path):
     u, _, _ = o.run(u0, 0.01, 2, eps=1e-14)
     u, _, _ = o.run(u, 0.005, 1, eps=1e-14)
     assert np.linalg.norm(rec.final_state - u) / np.linalg.norm(u) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_compare_methods_and_convergence_study():
+    # harness.cpp:147-196 / 272-316 on the GPU: every method, the reference's
+    # conservation classes and orders on a short paper-scale run
+    cfg = Hn.RunConfig(nx=16, ny=16, t_end=0.1, dt=0.01, gamma=0.1)
+    rep = Hn.compare_methods(cfg, ["gauss2", "gauss4", "avf2", "avf4", "mb4", "rk4"])
+    d = {m.method: m for m in rep.methods}
+    for m in ("mb4", "avf2", "avf4"):
+        assert d[m].energy_drift <= 1e-11
+    for m in ("gauss2", "gauss4"):
+        assert d[m].probability_drift <= 1e-12
+    assert d["rk4"].total_newton_iters == 0 and d["mb4"].total_newton_iters > 0
+    assert rep.mb4_over_gauss2 > 0.0
+    import io
+    buf = io.StringIO()
+    rep.write(buf)
+    assert buf.getvalue().startswith("method  energy_drift")
+    conv = Hn.convergence_study(Hn.RunConfig(nx=16, ny=16, t_end=0.2, gamma=0.1), ["avf2", "gauss4"],
+                                [0.02, 0.01, 0.005])
+    slopes = {e.method: e.slope for e in conv.entries}
+    assert 1.8 <= slopes["avf2"] <= 2.2
+    assert 3.6 <= slopes["gauss4"] <= 4.4
+    bench = Hn.parallel_bench(Hn.RunConfig(nx=16, ny=16, t_end=0.05, dt=0.01))
+    assert bench.trajectories_identical
