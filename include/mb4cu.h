@@ -156,7 +156,8 @@ int mb4cu_method_run(mb4cu_ctx* ctx, int method, double h, int nsteps, double* o
 int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out);
 
 /* Bind the context to an external CUDA stream (e.g. torch's current stream);
- * NULL restores the context's own stream. */
+ * NULL restores the context's own (non-blocking) stream.  For the legacy default
+ * stream (torch's default stream reports handle 0) pass cudaStreamLegacy. */
 int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
 
 /* ---- Sub-domain (multi-GPU) stepping, ghost > 0 ---------------------------------
@@ -178,6 +179,14 @@ int mb4cu_halo_unpack(mb4cu_ctx* ctx, int field, int side, const double* dev_buf
  * *local_rmax = max over owned sites of the split-real update. */
 int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* local_sums5);
 /* Accept the iterate after `sweeps` sweeps as the step result (u0 <- U3). */
+/* Asynchronous sweep for device-side collectives: enqueues sweep s on the context
+ * stream and a copy of [local ||r||_inf, 5 local energy sums of u0 (s = 0 only)]
+ * into dev_out6 (device memory), without a host synchronisation, so the caller
+ * can all-reduce the buffer on the same stream (NCCL) and read it once.
+ * final_guess != 0 (s > 0): the sweep is predicted to be the last, only U3 (the
+ * step result) is stored; if the reduced residual does not converge the caller
+ * repeats the same sweep with final_guess = 0 before going on. */
+int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6);
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
 /* Local energy sums of the resident state (ghosts of u0 must be current). */
 int mb4cu_observables_sums(mb4cu_ctx* ctx, double* local_sums5);

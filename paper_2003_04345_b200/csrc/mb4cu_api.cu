@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -1252,6 +1253,30 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
     if (local_rmax) *local_rmax = ctx->h_status->rlast;
     if (local_sums5 && s == 0)
         for (int f = 0; f < mb4cu::kObsFields; ++f) local_sums5[f] = ctx->h_status->obs[f];
+    return MB4CU_OK;
+}
+
+int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6) {
+    if (!ctx || ctx->ghost <= 0) return fail(ctx, MB4CU_INVALID, "sweep: sub-domain contexts only");
+    if (!(h > 0.0) || s < 0 || !dev_out6) return fail(ctx, MB4CU_INVALID, "sweep: h > 0, s >= 0, output buffer");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    const SweepConsts c = make_consts(ctx, h);
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
+    MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
+                                            ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
+                                            ctx->device, ctx->stream, ctx->ghost, s,
+                                            final_guess && s > 0 ? s : -1));
+    // [local ||r||_inf, the 5 energy sums of u0 (s = 0)] -> the caller's device buffer
+    static_assert(offsetof(mb4cu::StepStatus, obs) == offsetof(mb4cu::StepStatus, rlast) + sizeof(double),
+                  "rlast and obs are contiguous");
+    MB4_CUDA(ctx, cudaMemcpyAsync(dev_out6, reinterpret_cast<const char*>(ctx->d_status) +
+                                                offsetof(mb4cu::StepStatus, rlast),
+                                  sizeof(double) * (1 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->profiling) {
+        ctx->prof.launches += 1;
+        ctx->prof.sweeps += 1;
+        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : (final_guess ? 88.0 : 120.0));
+    }
     return MB4CU_OK;
 }
 

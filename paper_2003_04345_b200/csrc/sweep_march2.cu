@@ -591,6 +591,7 @@ struct MarchFirst {
         double2 up;   // g_{n-1}(i - n + 1), computed this iteration
         double2 low;  // g_{MF-2}(i - MF)
         double2 mid;  // g_{MF-1}(i - MF)
+        double2 u0o;  // u0(i - MF), loaded by level MF (the output row)
     };
 
     // level N (compile-time recursion: every ring offset and slot depth is static)
@@ -616,7 +617,10 @@ struct MarchFirst {
             own[cc] = ch.up;  // publish g_{N-1}(i - N + 1) for the neighbours / the output
             gp[N - 1][PAR] = ch.up;
             if (N == MF - 1) ch.low = gd;
-            if (N == MF) ch.mid = gc;
+            if (N == MF) {
+                ch.mid = gc;
+                ch.u0o = u0n;
+            }
             ch.up = gn;
             levels<N + 1, PAR>(cf, j, ch);
         }
@@ -661,7 +665,7 @@ struct MarchFirst {
         }
 
         // ---- levels 1..MF: g_n at row i - n from g_{n-1} rows i-n-1, i-n, i-n+1 ----
-        Chain ch{f, f, f};
+        Chain ch{f, f, f, f};
         levels<1, PAR>(cf, j, ch);
         const double2 up = ch.up;
         const double2 g_low = ch.low, g_mid = ch.mid;
@@ -673,8 +677,7 @@ struct MarchFirst {
             if (MF >= 2) gout[MF - 2] = g_low;
             gout[MF - 1] = g_mid;
             gout[MF] = up;
-            const int slot_o = zslot(MF + 1);  // z row of output row i - MF
-            const double2 u0o = MF == 1 ? zw[2] : zu0[slot_o * ZW + cc];
+            const double2 u0o = ch.u0o;
             const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -977,6 +980,9 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
     a.pitch = nx + 2 * ghost;
     a.sweep0 = sweep0;
     a.spec_sweep = spec_sweep;
+#ifdef MB4_DEBUG_FIRST_ONLY
+    a.max_iters = 1;  // profiling builds: the first sweep alone
+#endif
 #define MB4_PAIR_LAUNCH(F, N) if (mf == F && m == N) return dispatch3<F, N>(a, c, device, s);
     MB4_MARCH2_PAIRS(MB4_PAIR_LAUNCH)
 #undef MB4_PAIR_LAUNCH

@@ -142,6 +142,13 @@ class Comm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def allreduce_max_(self, t) -> None:
+        """In-place MAX all-reduce of a device tensor (no host synchronisation)."""
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+
+    def allreduce_sum_(self, t) -> None:
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+
     def allreduce_sum(self, xs) -> np.ndarray:
         t = self.torch.tensor(np.asarray(xs, dtype=np.float64), device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
@@ -229,6 +236,8 @@ class DistributedSession:
         return self.finish(self.comm.allreduce_sum(self.b.obs_sums()))
 
     def _substep(self, h: float) -> Tuple[int, float]:
+        if hasattr(self.b, "sweep_reduce"):
+            return self._substep_device(h)
         self.halo.exchange(F_U0)
         r = r_prev = float("nan")
         for s in range(self.max_iters):
@@ -243,6 +252,31 @@ class DistributedSession:
             if stage_converged(r, r_prev, s, self.eps):
                 self.b.commit(s + 1)
                 return s + 1, r
+            r_prev = r
+        raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
+
+    def _substep_device(self, h: float) -> Tuple[int, float]:
+        """Device-side reductions (one host read per sweep) and the speculative final
+        sweep: the sweep predicted by the previous sub-step's count stores U3 only and
+        is repeated with all stages if the reduced residual does not converge."""
+        self.halo.exchange(F_U0)
+        guess = getattr(self, "_guess", 0)
+        r = r_prev = float("nan")
+        for s in range(self.max_iters):
+            if s > 0:
+                self.halo.exchange(F_SET0 + ((s - 1) & 1))
+            final = s > 0 and s == guess - 1
+            r, sums = self.b.sweep_reduce(h, s, final, self.comm, want_sums=(s == 0 and self.entry_sums is None))
+            if sums is not None:
+                self.entry_sums = sums
+            if not math.isfinite(r):
+                raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
+            if stage_converged(r, r_prev, s, self.eps):
+                self.b.commit(s + 1)
+                self._guess = s + 1
+                return s + 1, r
+            if final:
+                self.b.sweep_repeat(h, s)
             r_prev = r
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
@@ -307,9 +341,14 @@ class CudaBackend:
         if rc:
             raise RuntimeError(self.L.mb4cu_create_error().decode())
         # run on torch's stream so NCCL and our kernels are ordered
-        self.L.mb4cu_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream))
+        # torch's default stream reports handle 0, which the C ABI reads as "own
+        # stream"; pass cudaStreamLegacy (0x1) for it so that the sweeps, the halo
+        # pack/unpack kernels and NCCL are ordered on one stream
+        self.L.mb4cu_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream or 1))
         self.n = dec.lnx * dec.lny
         self._saved = None
+        self._red = None
+        self._scratch = None
 
     def _chk(self, rc):
         if rc:
@@ -335,6 +374,25 @@ class CudaBackend:
         sums = np.zeros(5)
         self._chk(self.L.mb4cu_sweep(self.ctx, h, s, C.byref(r), _lib.dptr(sums)))
         return r.value, sums
+
+    def sweep_reduce(self, h, s, final, comm, want_sums=False):
+        """Sweep s with the residual max (and the energy sums) all-reduced on the
+        device, on the stream shared with NCCL; one host read."""
+        if self._red is None:
+            self._red = self.torch.zeros(6, dtype=self.torch.float64, device=self.dev)
+        red = self._red
+        self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, int(final), C.c_void_p(red.data_ptr())))
+        comm.allreduce_max_(red[0:1])
+        if want_sums:
+            comm.allreduce_sum_(red[1:6])
+        host = red.cpu().numpy()
+        return float(host[0]), (host[1:6].copy() if want_sums else None)
+
+    def sweep_repeat(self, h, s):
+        """Repeat sweep s storing every stage (after a missed final guess)."""
+        if self._scratch is None:
+            self._scratch = self.torch.zeros(6, dtype=self.torch.float64, device=self.dev)
+        self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, 0, C.c_void_p(self._scratch.data_ptr())))
 
     def commit(self, sweeps):
         self._chk(self.L.mb4cu_commit_step(self.ctx, sweeps))

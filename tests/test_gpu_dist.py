@@ -47,6 +47,13 @@ class LoopbackComm:
             acc = acc + v
         return acc
 
+    # device-tensor variants used by the production path (dist.CudaBackend.sweep_reduce)
+    def allreduce_max_(self, t):
+        t.copy_(torch.from_numpy(np.max(np.stack(self._gather(t.cpu().numpy().copy())), axis=0)))
+
+    def allreduce_sum_(self, t):
+        t.copy_(torch.from_numpy(self.allreduce_sum(t.cpu().numpy().copy())))
+
     def exchange(self, pairs):
         torch.cuda.synchronize()
         counts = {}
