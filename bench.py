@@ -238,6 +238,7 @@ def cpu_baseline(cfg, V, psi, steps=16):
         "value": value,
         "unit": UNIT,
         "cores": cores,
+        "nproc": os.cpu_count(),
         "kind": kind,
         "sample": (f"{win}x{win} window of the {cfg.name} inputs, {steps} MB4 steps "
                    f"(dt={cfg.dt}, eps={cfg.epsilon}), reference StepDriver(MB4) solver=gmres "
@@ -570,7 +571,7 @@ def run_reference(args, d: Dist):
         "data": "synthetic (seeded defects + Gaussian packets, configs.py)",
         "config": {"workload": f"{cfg.name} (sampled: {win}x{win} window of its inputs per step)",
                    "lattice": [cfg.nx, cfg.ny]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "nproc": os.cpu_count(), "kind": kind,
                          "sample": f"{win}x{win} window of the {cfg.name} inputs, one MB4 step per "
                                    f"bench step, reference StepDriver(MB4) solver=gmres workers=3"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
