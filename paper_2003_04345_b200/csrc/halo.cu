@@ -68,20 +68,21 @@ constexpr int kThreads = 256;
 __global__ void __launch_bounds__(kThreads)
 observables_ghost_kernel(const ObsArgs a, int ghost, int pitch) {
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    const size_t n = static_cast<size_t>(a.nx) * a.ny;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(k / a.nx), i = static_cast<int>(k - static_cast<size_t>(j) * a.nx);
-        const size_t g = static_cast<size_t>(j + ghost) * pitch + (i + ghost);
-        const double2 u = a.u[g], l = a.u[g - 1], r = a.u[g + 1], d = a.u[g - pitch], up = a.u[g + pitch];
-        const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
-        const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
-        acc[0] += fma(u.x, kx, u.y * ky);
-        acc[1] += fma(u.x, ky, -u.y * kx);
-        const double n2 = fma(u.x, u.x, u.y * u.y);
-        acc[2] += n2;
-        acc[3] += n2 * n2;
-        acc[4] += a.V[g] * n2;
+    // rows round-robin over the blocks, columns over the threads (no division)
+    for (int j = blockIdx.x; j < a.ny; j += gridDim.x) {
+        const size_t g0 = static_cast<size_t>(j + ghost) * pitch + ghost;
+        for (int i = threadIdx.x; i < a.nx; i += blockDim.x) {
+            const size_t g = g0 + i;
+            const double2 u = a.u[g], l = a.u[g - 1], r = a.u[g + 1], d = a.u[g - pitch], up = a.u[g + pitch];
+            const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
+            const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
+            acc[0] += fma(u.x, kx, u.y * ky);
+            acc[1] += fma(u.x, ky, -u.y * kx);
+            const double n2 = fma(u.x, u.x, u.y * u.y);
+            acc[2] += n2;
+            acc[3] += n2 * n2;
+            acc[4] += a.V[g] * n2;
+        }
     }
     __shared__ double red[kObsFields][kThreads / 32];
 #pragma unroll

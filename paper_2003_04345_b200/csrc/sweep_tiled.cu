@@ -174,23 +174,36 @@ constexpr int kObsThreads = 256;
 
 __global__ void __launch_bounds__(kObsThreads) observables_partial_kernel(const ObsArgs a) {
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    const size_t n = static_cast<size_t>(a.nx) * a.ny;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(k / a.nx), i = static_cast<int>(k - static_cast<size_t>(j) * a.nx);
-        const double2 u = a.u[k];
-        const double2 l = a.u[static_cast<size_t>(j) * a.nx + wrap_index(i - 1, a.nx)];
-        const double2 r = a.u[static_cast<size_t>(j) * a.nx + wrap_index(i + 1, a.nx)];
-        const double2 d = a.u[static_cast<size_t>(wrap_index(j - 1, a.ny)) * a.nx + i];
-        const double2 up = a.u[static_cast<size_t>(wrap_index(j + 1, a.ny)) * a.nx + i];
-        const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
-        const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
-        acc[0] += fma(u.x, kx, u.y * ky);   // Re conj(u) Ku
-        acc[1] += fma(u.x, ky, -u.y * kx);  // Im conj(u) Ku
-        const double n2 = fma(u.x, u.x, u.y * u.y);
-        acc[2] += n2;
-        acc[3] += n2 * n2;
-        acc[4] += a.V[k] * n2;
+    // Tiles of kObsThreads columns x a band of rows; each thread marches down its
+    // column with the vertical neighbours in registers (one HBM read of u per site;
+    // left/right come from the same row, L1-resident), periodic wrap by
+    // compare-and-select.  Fixed work split -> bit-reproducible sums.
+    const int ntx = (a.nx + kObsThreads - 1) / kObsThreads;
+    const int nby = gridDim.x / ntx;
+    const int tx = blockIdx.x % ntx, by = blockIdx.x / ntx;
+    const int i = tx * kObsThreads + threadIdx.x;
+    if (by < nby && i < a.nx) {
+        const int y0 = static_cast<int>(static_cast<long long>(a.ny) * by / nby);
+        const int y1 = static_cast<int>(static_cast<long long>(a.ny) * (by + 1) / nby);
+        const int il = i == 0 ? a.nx - 1 : i - 1, ir = i == a.nx - 1 ? 0 : i + 1;
+        auto at = [&](int j) { return a.u + static_cast<size_t>(j) * a.nx; };
+        double2 dn = at(y0 == 0 ? a.ny - 1 : y0 - 1)[i];
+        double2 u = at(y0)[i];
+        for (int j = y0; j < y1; ++j) {
+            const double2* row = at(j);
+            const double2 up = at(j == a.ny - 1 ? 0 : j + 1)[i];
+            const double2 l = row[il], r = row[ir];
+            const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (dn.x + up.x)));
+            const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (dn.y + up.y)));
+            acc[0] += fma(u.x, kx, u.y * ky);   // Re conj(u) Ku
+            acc[1] += fma(u.x, ky, -u.y * kx);  // Im conj(u) Ku
+            const double n2 = fma(u.x, u.x, u.y * u.y);
+            acc[2] += n2;
+            acc[3] += n2 * n2;
+            acc[4] += a.V[static_cast<size_t>(j) * a.nx + i] * n2;
+            dn = u;
+            u = up;
+        }
     }
     __shared__ double red[kObsFields][kObsThreads / 32];
 #pragma unroll
@@ -339,7 +352,12 @@ cudaError_t launch_amax2(const double2* u, size_t n, unsigned long long* out, cu
 }
 
 int obs_blocks(int nx, int ny) {
-    return grid_for(static_cast<size_t>(nx) * ny, kObsThreads);
+    // column tiles x row bands, ~8 blocks per SM, bands of >= 8 rows
+    const int ntx = (nx + kObsThreads - 1) / kObsThreads;
+    int nby = (148 * 8 + ntx - 1) / ntx;
+    if (nby > (ny + 7) / 8) nby = (ny + 7) / 8;
+    if (nby < 1) nby = 1;
+    return ntx * nby;
 }
 
 cudaError_t launch_observables(const ObsArgs& a, double* out5, cudaStream_t s) {
