@@ -173,14 +173,25 @@ def schedule_key(args) -> str:
     return f"mf{args.neumann_first}_m{args.neumann}"
 
 
-def measured_traffic(cfg_name: str, schedule: str):
-    """DRAM bytes per step-kernel launch from the committed ncu capture (profiles/traffic.json)."""
+def _traffic_entry(cfg_name: str, schedule: str):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            t = json.load(f).get(f"{cfg_name}_{schedule}")
-        return None if t is None else float(t["dram_bytes_per_launch"])
+            return json.load(f).get(f"{cfg_name}_{schedule}")
     except Exception:
         return None
+
+
+def measured_traffic(cfg_name: str, schedule: str):
+    """DRAM bytes per step-kernel launch from the committed ncu capture (profiles/traffic.json)."""
+    t = _traffic_entry(cfg_name, schedule)
+    return None if t is None else float(t["dram_bytes_per_launch"])
+
+
+def measured_limiters(cfg_name: str, schedule: str):
+    """Pipe utilisations of the same ncu capture: with a depth-6 first sweep the
+    step kernel is bounded on-chip (FP64 pipe, shared memory) rather than by HBM."""
+    t = _traffic_entry(cfg_name, schedule)
+    return None if t is None else t.get("limiters")
 
 
 def measured_peaks():
@@ -368,6 +379,7 @@ def run_ours(args, d: Dist):
             "frac": achieved / peak,
             "traffic": measured_traffic(cfg.name, schedule_key(args)),
             "traffic_source": "ncu --set full, dram__bytes_read+write per launch (profiles/traffic.json)",
+            "limiters": measured_limiters(cfg.name, schedule_key(args)),
             "peak_kind": peak_kind,
             "kernel": "stage sweep",
             "alg_bytes_per_step": step_alg_bytes,
