@@ -201,3 +201,19 @@ def test_run_energy_record_matches_explicit_observables():
     for k, f in enumerate(nls2d.OBS_FIELDS):
         assert abs(obs[0, k] - getattr(o, f)) <= 1e-13 * max(1.0, abs(getattr(o, f)))
         assert obs[-1, k] == getattr(last, f)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_full_baseline_run_energy_drift(name):
+    """BASELINE.json configs 3-5 at their full lattice and step counts (500 / 200 /
+    100 steps) with the default schedule: relative energy drift <= 1e-13."""
+    cfg = configs.CONFIGS[name]
+    if name == "cfg5":
+        cfg = cfg.with_lattice(8192, 8192)
+    V, psi = configs.make_inputs(cfg)
+    with session(cfg, V) as s:
+        s.set_state(psi)
+        obs, iters = s.run(cfg.dt, cfg.steps)
+    H = obs[:, 3]
+    assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
+    assert iters.min() >= 2
