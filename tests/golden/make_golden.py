@@ -8,8 +8,10 @@ Sources (nothing here is hand-written data):
   ref_*.npz          -- the reference library itself (oracle/_ref/libnls2d_ref.so,
                         StepDriver(MB4) -> mb4_step, eps = 1e-14) on the BASELINE
                         inputs produced by paper_2003_04345_b200.configs.
+  ref_methods_cfg1_5.npz -- the same library's StepDriver(RK4 / GAUSS2 / GAUSS4 /
+                        AVF2 / AVF4), direct solver, 5 cfg1 steps.
 
-usage: python tests/golden/make_golden.py
+usage: python tests/golden/make_golden.py [--methods-only]
 """
 import hashlib
 import json
@@ -84,8 +86,24 @@ def ref_case(name, nsteps, solver, keep_steps=(1, 10)):
     return out
 
 
+def methods_case():
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    out = {"input_sha256": input_digest(V, psi), "nsteps": 5, "solver": "direct"}
+    for m in ("rk4", "gauss2", "gauss4", "avf2", "avf4"):
+        u, obs, iters, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi, cfg.dt, 5,
+                                     eps=cfg.epsilon, solver="direct", method=m)
+        out[f"{m}_state"] = u
+        out[f"{m}_obs"] = obs
+        out[f"{m}_iters"] = iters
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
+    np.savez_compressed(os.path.join(HERE, "ref_methods_cfg1_5.npz"), **methods_case())
+    if "--methods-only" in sys.argv:
+        return
     with open(os.path.join(HERE, "scheme_exact.json"), "w") as f:
         json.dump(scheme_exact(), f, indent=1)
     # cfg1: direct solver (reference default), states after 1 and 10 steps, 10-step H series

@@ -191,3 +191,29 @@ def test_restatement_matches_reference_library_eval_phi():
     a = o.eval_phi(u0, st, 0.03)
     b = O.ref_eval_phi(6, 5, TWO_PI, 2.0, -0.7, V, u0, st, 0.03)
     assert max(np.abs(x - y).max() for x, y in zip(a, b)) <= 1e-13
+
+
+def test_methods_golden_fixture_pinned():
+    """The other integrators' fixture (reference StepDriver, 5 cfg1 steps) belongs to
+    the current inputs; with the reference built here it is reproduced bit for bit,
+    and its conservation classes hold (AVF energy, Gauss probability)."""
+    g = np.load(os.path.join(GOLD, "ref_methods_cfg1_5.npz"))
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(V.tobytes())
+    h.update(psi.tobytes())
+    assert h.hexdigest() == str(g["input_sha256"])
+    for m in ("avf2", "avf4"):
+        H = g[f"{m}_obs"][:, 3]
+        assert np.abs(H - H[0]).max() <= 1e-13 * abs(H[0])
+    for m in ("gauss2", "gauss4"):
+        P = g[f"{m}_obs"][:, 4]
+        assert np.abs(P - P[0]).max() <= 1e-13 * P[0]
+    assert list(g["rk4_iters"]) == [0] * 5
+    if O.ref_available():
+        u, _, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi, cfg.dt, 5,
+                               eps=cfg.epsilon, solver="direct", method="avf2")
+        assert np.array_equal(u, g["avf2_state"])
