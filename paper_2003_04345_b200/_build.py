@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["mb4cu_api.cu", "sweep_tiled.cu", "sweep_march.cu", "sweep_march2.cu", "halo.cu", "krylov.cu",
-                "methods.cu"]
+                "methods.cu", "fft_precond.cu"]
 HOST_SOURCES = ["scheme_host.cpp", "inputs_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
@@ -74,7 +74,7 @@ def build_lib(force: bool = False, verbose: bool = False, defines=(), name: str 
         if verbose and out:
             print(out)
     tmp = target + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcufft", "-lpthread"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, target)
     return target

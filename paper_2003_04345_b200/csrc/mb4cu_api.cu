@@ -3,6 +3,7 @@
 // entry points.  See include/mb4cu.h for the contract and the reference
 // interfaces each entry point replaces.
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
@@ -68,6 +69,14 @@ struct mb4cu_ctx {
         double* h_coef = nullptr;   // pinned
         long long gmres_iters = 0;  // total inner iterations (stats)
     } kr;
+    // Fourier preconditioner of the Krylov solves (fft_precond.cu), created on first use
+    struct {
+        cufftHandle plan1 = 0, plan2 = 0;  // N-point 2-D Z2Z; batch of 2 (coupled systems)
+        bool have1 = false, have2 = false;
+        double* partial = nullptr;         // shift partial sums [blocks][2]
+        double* h_partial = nullptr;
+        double shift = 0.0;                // mean(V) - 2 gamma mean(|u0|^2) of the current u0
+    } fft;
     bool profiling = false;
     mb4cu_profile prof{};
     std::string err;
@@ -313,7 +322,7 @@ int kr_alloc(mb4cu_ctx* ctx, size_t len) {
     k.m = kKrylovRestart;
     k.len = len;
     k.nblk = mb4cu::krylov_blocks(len);
-    const size_t nvec = static_cast<size_t>(k.m + 1) + 3 + 3 + 2;
+    const size_t nvec = static_cast<size_t>(k.m + 1) + 3 + 3 + 2 + 1;  // + preconditioner scratch
     MB4_CUDA(ctx, cudaMalloc(&k.mem, nvec * len * sizeof(double2)));
     MB4_CUDA(ctx, cudaMalloc(&k.v_dev, sizeof(double2*) * (k.m + 1)));
     std::vector<double2*> ptrs(k.m + 1);
@@ -437,6 +446,83 @@ int kr_gmres(mb4cu_ctx* ctx, const MatVec& matvec, const double2* b, double2* x)
     return MB4CU_OK;  // best effort after the iteration cap, as the reference (iterative.cpp:152)
 }
 
+// ---- Fourier preconditioner (fft_precond.cu) ---------------------------------
+
+int fft_fail(mb4cu_ctx* ctx, cufftResult r, const char* where) {
+    return fail(ctx, MB4CU_CUDA_ERROR, std::string("cufft ") + where + ": error " + std::to_string(static_cast<int>(r)));
+}
+
+// plans (on first use) and the diagonal shift of the current u0
+int fft_prepare(mb4cu_ctx* ctx, int stages) {
+    auto& f = ctx->fft;
+    cufftResult r;
+    if (stages == 1 && !f.have1) {
+        if ((r = cufftPlan2d(&f.plan1, ctx->ny, ctx->nx, CUFFT_Z2Z)) != CUFFT_SUCCESS) return fft_fail(ctx, r, "plan");
+        f.have1 = true;
+    }
+    if (stages == 2 && !f.have2) {
+        int dims[2] = {ctx->ny, ctx->nx};
+        if ((r = cufftPlanMany(&f.plan2, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 2)) != CUFFT_SUCCESS)
+            return fft_fail(ctx, r, "plan");
+        f.have2 = true;
+    }
+    const int nb = mb4cu::fft_shift_blocks(ctx->n);
+    if (!f.partial) {
+        MB4_CUDA(ctx, cudaMalloc(&f.partial, sizeof(double) * 2 * nb));
+        MB4_CUDA(ctx, cudaMallocHost(&f.h_partial, sizeof(double) * 2 * nb));
+    }
+    MB4_CUDA(ctx, mb4cu::launch_fft_shift_partials(ctx->u0, ctx->V, ctx->n, f.partial, ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(f.h_partial, f.partial, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    double sv = 0.0, su = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        sv += f.h_partial[2 * b];
+        su += f.h_partial[2 * b + 1];
+    }
+    const double n = static_cast<double>(ctx->n);
+    f.shift = sv / n - 2.0 * ctx->gamma * (su / n);
+    return MB4CU_OK;
+}
+
+// y <- P^-1 y in place (len = stages * N).  stages 1: P = I + i sigma (K + shift);
+// stages 2: P = I + i h C (x) (K + shift).
+int fft_apply(mb4cu_ctx* ctx, int stages, double sigma_or_h, const double C[2][2], double2* y) {
+    auto& f = ctx->fft;
+    const cufftHandle plan = stages == 1 ? f.plan1 : f.plan2;
+    cufftResult r;
+    if ((r = cufftSetStream(plan, ctx->stream)) != CUFFT_SUCCESS) return fft_fail(ctx, r, "stream");
+    auto* z = reinterpret_cast<cufftDoubleComplex*>(y);
+    if ((r = cufftExecZ2Z(plan, z, z, CUFFT_FORWARD)) != CUFFT_SUCCESS) return fft_fail(ctx, r, "forward");
+    if (stages == 1)
+        MB4_CUDA(ctx, mb4cu::launch_fft_scale1(y, ctx->nx, ctx->ny, ctx->cx, ctx->cy, f.shift, sigma_or_h, ctx->stream));
+    else
+        MB4_CUDA(ctx, mb4cu::launch_fft_scale2(y, y + ctx->n, ctx->nx, ctx->ny, ctx->cx, ctx->cy, f.shift, sigma_or_h,
+                                               C, ctx->stream));
+    if ((r = cufftExecZ2Z(plan, z, z, CUFFT_INVERSE)) != CUFFT_SUCCESS) return fft_fail(ctx, r, "inverse");
+    ctx->prof.other_launches += 3;
+    return MB4CU_OK;
+}
+
+// Right-preconditioned GMRES: solve (A P^-1) x' = b, x = P^-1 x'; A applied by
+// amul(x, y) over len = stages * N.
+template <class AMul>
+int kr_gmres_fft(mb4cu_ctx* ctx, int stages, double sigma_or_h, const double C[2][2], const AMul& amul,
+                 const double2* b, double2* x) {
+    const size_t len = ctx->kr.len;
+    double2* tmp = kr_vec(ctx, ctx->kr.m + 9);
+    int prc = MB4CU_OK;
+    auto mv = [&](const double2* xin, double2* yout) -> cudaError_t {
+        cudaError_t e = cudaMemcpyAsync(tmp, xin, len * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream);
+        if (e != cudaSuccess) return e;
+        if ((prc = fft_apply(ctx, stages, sigma_or_h, C, tmp)) != MB4CU_OK) return cudaErrorUnknown;
+        return amul(tmp, yout);
+    };
+    if (int rc = kr_gmres(ctx, mv, b, x)) return prc ? prc : rc;
+    if (prc) return prc;
+    return fft_apply(ctx, stages, sigma_or_h, C, x);
+}
+
 int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
     if (int rc = kr_alloc(ctx, ctx->n)) return rc;
     const SweepConsts c = make_consts(ctx, h);
@@ -449,6 +535,7 @@ int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
     double2* b[3] = {kr_vec(ctx, m + 1), kr_vec(ctx, m + 2), kr_vec(ctx, m + 3)};
     double2* x[3] = {kr_vec(ctx, m + 4), kr_vec(ctx, m + 5), kr_vec(ctx, m + 6)};
     *iters = 0;
+    if (int rc = fft_prepare(ctx, 1)) return rc;
     for (int it = 1; it <= ctx->max_iters; ++it) {
         const double2* cst[3] = {st[0], st[1], st[2]};
         MB4_CUDA(ctx, mb4cu::kr_phibar(ctx->nx, ctx->ny, ctx->u0, cst, ctx->V, b, c, ctx->stream));
@@ -457,7 +544,7 @@ int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
             auto mv = [&](const double2* xin, double2* yout) {
                 return mb4cu::kr_matvec(xin, yout, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream);
             };
-            if (int rc = kr_gmres(ctx, mv, b[k], x[k])) return rc;
+            if (int rc = kr_gmres_fft(ctx, 1, hl, nullptr, mv, b[k], x[k])) return rc;
         }
         MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
         const double2* cx[3] = {x[0], x[1], x[2]};
@@ -742,6 +829,10 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
     kr_free(ctx);
+    if (ctx->fft.have1) cufftDestroy(ctx->fft.plan1);
+    if (ctx->fft.have2) cufftDestroy(ctx->fft.plan2);
+    cudaFree(ctx->fft.partial);
+    cudaFreeHost(ctx->fft.h_partial);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->pev0) cudaEventDestroy(ctx->pev0);
@@ -1054,10 +1145,13 @@ int method_plain_step(mb4cu_ctx* ctx, int method, double h, int* iters, double* 
     auto mv = [&](const double2* xin, double2* yout) {
         return mb4cu::launch_method_matvec(st, ctx->nx, ctx->ny, xin, yout, ctx->u0, ctx->V, c, ctx->stream);
     };
+    if (int rc = fft_prepare(ctx, st)) return rc;
     for (int it = 1; it <= ctx->max_iters; ++it) {
         MB4_CUDA(ctx, mb4cu::launch_method_residual(method, ctx->nx, ctx->ny, ctx->u0, ctx->V, unk, b, c,
                                                     ctx->stream));
-        if (int rc = kr_gmres(ctx, mv, b, x)) return rc;
+        if (int rc = st == 1 ? kr_gmres_fft(ctx, 1, 0.5 * h, nullptr, mv, b, x)
+                             : kr_gmres_fft(ctx, 2, h, c.a, mv, b, x))
+            return rc;
         MB4_CUDA(ctx, mb4cu::launch_newton_add(unk, x, len, ctx->d_rmax, ctx->stream));
         MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                       ctx->stream));

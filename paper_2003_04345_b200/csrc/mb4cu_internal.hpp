@@ -167,6 +167,15 @@ cudaError_t launch_method_final(int method, int nx, int ny, const double2* u0, c
 void method_tables(MethodConsts* c);
 void avf4_coupling(double mt[2][2]);
 
+// Fourier preconditioner of the Krylov solves (fft_precond.cu)
+int fft_shift_blocks(size_t n);
+cudaError_t launch_fft_shift_partials(const double2* u0, const double* V, size_t n, double* partial,
+                                      cudaStream_t s);
+cudaError_t launch_fft_scale1(double2* y, int nx, int ny, double cx, double cy, double shift, double sigma,
+                              cudaStream_t s);
+cudaError_t launch_fft_scale2(double2* y0, double2* y1, int nx, int ny, double cx, double cy, double shift,
+                              double h, const double C[2][2], cudaStream_t s);
+
 // Launchers (sweep_tiled.cu, sweep_march.cu).
 cudaError_t launch_step_march(int m, int nx, int ny, const double2* u0, const double* V,
                               double2* const U[2][3], unsigned long long* rmax,

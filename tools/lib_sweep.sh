@@ -1,0 +1,10 @@
+#!/bin/bash
+# usage: tools/lib_sweep.sh "<bench args>" lib1.so lib2.so ...  (run on the GPU box)
+ARGS="$1"; shift
+for lib in "$@"; do
+  MB4CU_LIB=$PWD/paper_2003_04345_b200/$lib python bench.py $ARGS --no-cpu-baseline --no-e2e 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read())
+r=d['roofline']
+print('$lib', '%.3e'%d['value'], d['sweeps_per_step'], 'ms/launch=%.3f'%r['kernel_ms_per_launch'], r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
+done
