@@ -242,6 +242,7 @@ typedef struct {
                                  persistent kernel only (%globaltimer at grid barriers) */
     long long sweep_n[8];     /* samples accumulated in sweep_ms                      */
     long long redone;         /* speculative final sweeps that missed and were redone */
+    long long krylov_iters;   /* GMRES inner iterations (Newton-Krylov / other methods) */
 } mb4cu_profile;
 
 int mb4cu_profile_enable(mb4cu_ctx* ctx, int on);

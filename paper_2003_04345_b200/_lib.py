@@ -83,6 +83,7 @@ class Profile(C.Structure):
         ("sweep_ms", D * 8),
         ("sweep_n", C.c_longlong * 8),
         ("redone", C.c_longlong),
+        ("krylov_iters", C.c_longlong),
     ]
 
 

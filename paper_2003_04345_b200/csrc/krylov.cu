@@ -12,6 +12,7 @@
 // AXPYs, norms); the host keeps the (m+1) x m Hessenberg bookkeeping.  Dot
 // products are block partials summed on the host in a fixed order, so runs are
 // bit-reproducible.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "mb4cu_internal.hpp"
@@ -202,7 +203,93 @@ int blocks(size_t n) {
     return static_cast<int>(b < 148 * 4 ? (b ? b : 1) : 148 * 4);
 }
 
+// One Arnoldi step after w = A v_j, in ONE cooperative launch (grid barriers
+// instead of host round trips): classical Gram-Schmidt twice against v_0..v_j,
+// hcol[i] = h_ij (both passes), hcol[j+1] = ||w||, v_{j+1} = w / ||w||.  Dot
+// products are block partials summed by block 0 in a fixed order (bit-
+// reproducible; the same grid as the other Krylov kernels).
+__global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, double2* const* __restrict__ v, int j,
+                                                     size_t n, double* __restrict__ partial,
+                                                     double* __restrict__ hbuf, double* __restrict__ hcol) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int i = 0; i <= j; ++i) {
+            const double2* vi = v[i];
+            double acc = 0.0;
+            GRID_LOOP(k, n) {
+                const double2 a = w[k], b = vi[k];
+                acc = fma(a.x, b.x, fma(a.y, b.y, acc));
+            }
+            const double sblk = block_sum(acc);
+            if (threadIdx.x == 0) partial[static_cast<size_t>(i) * G + blockIdx.x] = sblk;
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+                double t = 0.0;
+                for (int b = 0; b < G; ++b) t += partial[static_cast<size_t>(i) * G + b];
+                hbuf[i] = t;
+                hcol[i] = pass == 0 ? t : hcol[i] + t;
+            }
+        }
+        grid.sync();
+        double acc = 0.0;
+        GRID_LOOP(k, n) {  // the same sites per thread in every loop: no barrier needed before the next dots
+            double2 a = w[k];
+            for (int i = 0; i <= j; ++i) {
+                const double2 b = v[i][k];
+                a.x = fma(-hbuf[i], b.x, a.x);
+                a.y = fma(-hbuf[i], b.y, a.y);
+            }
+            w[k] = a;
+            acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+        }
+        if (pass == 1) {
+            const double sblk = block_sum(acc);
+            if (threadIdx.x == 0) partial[blockIdx.x] = sblk;
+        }
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < G; ++b) t += partial[b];
+        const double hn = sqrt(t);
+        hcol[j + 1] = hn;
+        hbuf[0] = hn > 0.0 ? 1.0 / hn : 0.0;
+    }
+    grid.sync();
+    const double inv = hbuf[0];
+    double2* vn = v[j + 1];
+    if (inv > 0.0) {
+        GRID_LOOP(k, n) {
+            const double2 a = w[k];
+            vn[k] = make_double2(inv * a.x, inv * a.y);
+        }
+    }
+}
+
 }  // namespace
+
+int arnoldi_grid(size_t n) {
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_kernel, kT, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int b = blocks(n);
+    return b < per_sm * sms ? b : per_sm * sms;
+}
+
+cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,
+                       double* hcol, cudaStream_t s) {
+    const int g = arnoldi_grid(n);
+    void* args[] = {&w, const_cast<double2***>(&v_dev), &j, &n, &partial, &hbuf, &hcol};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(g), dim3(kT), args, 0, s);
+}
 
 int krylov_blocks(size_t n) { return blocks(n); }
 

@@ -67,6 +67,8 @@ struct mb4cu_ctx {
         double* h_partial = nullptr;  // pinned copy
         double* coef = nullptr;     // device coefficients [m+1]
         double* h_coef = nullptr;   // pinned
+        double* hcol = nullptr;     // device Hessenberg column [m+2] (kr_arnoldi)
+        double* h_hcol = nullptr;   // pinned
         long long gmres_iters = 0;  // total inner iterations (stats)
     } kr;
     // Fourier preconditioner of the Krylov solves (fft_precond.cu), created on first use
@@ -301,6 +303,10 @@ void kr_free(mb4cu_ctx* ctx) {
     cudaFreeHost(k.h_partial);
     cudaFree(k.coef);
     cudaFreeHost(k.h_coef);
+    cudaFree(k.hcol);
+    cudaFreeHost(k.h_hcol);
+    k.hcol = nullptr;
+    k.h_hcol = nullptr;
     k.mem = nullptr;
     k.v_dev = nullptr;
     k.partial = nullptr;
@@ -335,6 +341,8 @@ int kr_alloc(mb4cu_ctx* ctx, size_t len) {
     MB4_CUDA(ctx, cudaMallocHost(&k.h_partial, sizeof(double) * (k.m + 1) * k.nblk));
     MB4_CUDA(ctx, cudaMalloc(&k.coef, sizeof(double) * (k.m + 1)));
     MB4_CUDA(ctx, cudaMallocHost(&k.h_coef, sizeof(double) * (k.m + 1)));
+    MB4_CUDA(ctx, cudaMalloc(&k.hcol, sizeof(double) * (k.m + 2)));
+    MB4_CUDA(ctx, cudaMallocHost(&k.h_hcol, sizeof(double) * (k.m + 2)));
     return MB4CU_OK;
 }
 
@@ -395,23 +403,14 @@ int kr_gmres(mb4cu_ctx* ctx, const MatVec& matvec, const double2* b, double2* x)
         bool done = false;
         for (; j < m && iter < kKrylovMaxIters; ++j, ++iter) {
             MB4_CUDA(ctx, matvec(kr_vec(ctx, j), w));
-            for (int i = 0; i <= j; ++i) Hat(i, j) = 0.0;
-            double wn2 = 0.0;
-            for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, twice
-                MB4_CUDA(ctx, mb4cu::kr_dots(w, k.v_dev, j + 1, n, k.partial, ctx->stream));
-                if (int rc = kr_fetch(ctx, j + 1, tmp.data())) return rc;
-                for (int i = 0; i <= j; ++i) {
-                    Hat(i, j) += tmp[i];
-                    k.h_coef[i] = tmp[i];
-                }
-                MB4_CUDA(ctx, cudaMemcpyAsync(k.coef, k.h_coef, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
-                                              ctx->stream));
-                MB4_CUDA(ctx, mb4cu::kr_axpy_norm(w, k.v_dev, k.coef, j + 1, n, k.partial, ctx->stream));
-                if (int rc = kr_fetch(ctx, 1, &wn2)) return rc;
-            }
-            const double hn = std::sqrt(wn2);
+            // classical Gram-Schmidt twice + normalisation, one cooperative launch
+            MB4_CUDA(ctx, mb4cu::kr_arnoldi(w, k.v_dev, j, n, k.partial, k.coef, k.hcol, ctx->stream));
+            MB4_CUDA(ctx, cudaMemcpyAsync(k.h_hcol, k.hcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost,
+                                          ctx->stream));
+            MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            for (int i = 0; i <= j; ++i) Hat(i, j) = k.h_hcol[i];
+            const double hn = k.h_hcol[j + 1];
             Hat(j + 1, j) = hn;
-            if (hn > 0.0) MB4_CUDA(ctx, mb4cu::kr_scale(w, kr_vec(ctx, j + 1), 1.0 / hn, n, ctx->stream));
             for (int i = 0; i < j; ++i) {
                 const double t = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);
                 Hat(i + 1, j) = -sn[i] * Hat(i, j) + cs[i] * Hat(i + 1, j);
@@ -433,6 +432,7 @@ int kr_gmres(mb4cu_ctx* ctx, const MatVec& matvec, const double2* b, double2* x)
             }
         }
         k.gmres_iters += j;
+        ctx->prof.krylov_iters += j;
         for (int i = j - 1; i >= 0; --i) {
             double s = g[i];
             for (int q = i + 1; q < j; ++q) s -= Hat(i, q) * yv[q];

@@ -167,6 +167,12 @@ cudaError_t launch_method_final(int method, int nx, int ny, const double2* u0, c
 void method_tables(MethodConsts* c);
 void avf4_coupling(double mt[2][2]);
 
+// One Arnoldi (CGS2) step in one cooperative launch (krylov.cu); partial must hold
+// (j+1) * arnoldi_grid(n) doubles, hbuf j+1, hcol j+2 (device)
+int arnoldi_grid(size_t n);
+cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,
+                       double* hcol, cudaStream_t s);
+
 // Fourier preconditioner of the Krylov solves (fft_precond.cu)
 int fft_shift_blocks(size_t n);
 cudaError_t launch_fft_shift_partials(const double2* u0, const double* V, size_t n, double* partial,
