@@ -15,6 +15,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
 
@@ -273,15 +275,19 @@ __global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, do
 }  // namespace
 
 int arnoldi_grid(size_t n) {
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    static std::atomic<int> cap[64];  // co-resident blocks per device (0 = unknown)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int c = dev >= 0 && dev < 64 ? cap[dev].load(std::memory_order_acquire) : 0;
+    if (!c) {
+        int per_sm = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_kernel, kT, 0);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        c = per_sm * sms;
+        if (dev >= 0 && dev < 64) cap[dev].store(c, std::memory_order_release);
     }
     const int b = blocks(n);
-    return b < per_sm * sms ? b : per_sm * sms;
+    return b < c ? b : c;
 }
 
 cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,

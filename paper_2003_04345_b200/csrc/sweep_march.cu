@@ -25,6 +25,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
 #include "async_copy.cuh"
@@ -339,8 +341,9 @@ mb4_step_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 template <int M, int NT>
 struct Launcher {
     static int grid_size(int device) {
-        static int cached[64] = {0};
-        if (device < 64 && cached[device]) return cached[device];
+        static std::atomic<int> cached[64];  // per device (0 = not yet computed)
+        if (device >= 0 && device < 64 && cached[device].load(std::memory_order_acquire))
+            return cached[device].load(std::memory_order_acquire);
         const size_t smem = MarchGeom<M, NT>::bytes;
         cudaFuncSetAttribute(mb4_step_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
@@ -349,7 +352,7 @@ struct Launcher {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
-        if (device < 64) cached[device] = g;
+        if (device >= 0 && device < 64) cached[device].store(g, std::memory_order_release);
         return g;
     }
 

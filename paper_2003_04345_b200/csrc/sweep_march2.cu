@@ -26,6 +26,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "async_copy.cuh"
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
@@ -897,8 +899,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
 struct Launcher3 {
     static int grid_size(int device) {
-        static int cached[64] = {0};
-        if (device >= 0 && device < 64 && cached[device]) return cached[device];
+        static std::atomic<int> cached[64];  // per device (0 = not yet computed)
+        if (device >= 0 && device < 64 && cached[device].load(std::memory_order_acquire))
+            return cached[device].load(std::memory_order_acquire);
         const size_t smem = KGeom<MF, M, NT>::bytes;
         cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
@@ -907,7 +910,7 @@ struct Launcher3 {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
-        if (device >= 0 && device < 64) cached[device] = g;
+        if (device >= 0 && device < 64) cached[device].store(g, std::memory_order_release);
         return g;
     }
 

@@ -13,6 +13,8 @@
 // outputs stages z on a halo of M+1 sites.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "mb4cu_internal.hpp"
 #include "site_math.cuh"
 
@@ -154,13 +156,15 @@ size_t tiled_smem() {
 template <int M, bool FIRST>
 cudaError_t launch_tiled(const SweepArgs& a, const SweepConsts& c, cudaStream_t s) {
     const size_t smem = tiled_smem<M, FIRST>();
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static std::atomic<bool> configured[64];  // per instantiation and device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(sweep_tiled_kernel<M, FIRST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        configured = true;
+        if (dev >= 0 && dev < 64) configured[dev].store(true, std::memory_order_release);
     }
     const dim3 grid((a.nx + kTX - 1) / kTX, (a.ny + kTY - 1) / kTY);
     sweep_tiled_kernel<M, FIRST><<<grid, kTX * kTY, smem, s>>>(a, c);
