@@ -21,7 +21,9 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <cctype>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -148,6 +150,14 @@ enum class MethodId { Rk4, Gauss2, Gauss4, Avf2, Avf4, Mb4 };
 
 /// integrators.cpp:13-43
 inline int method_order(MethodId m) { return m == MethodId::Gauss2 || m == MethodId::Avf2 ? 2 : 4; }
+inline std::optional<MethodId> parse_method(const std::string& name) {
+    std::string u;
+    for (char c : name) u.push_back(static_cast<char>(std::toupper(static_cast<unsigned char>(c))));
+    static const char* names[] = {"RK4", "GAUSS2", "GAUSS4", "AVF2", "AVF4", "MB4"};
+    for (int i = 0; i < 6; ++i)
+        if (u == names[i]) return static_cast<MethodId>(i);
+    return std::nullopt;
+}
 inline std::string method_name(MethodId m) {
     static const char* names[] = {"RK4", "GAUSS2", "GAUSS4", "AVF2", "AVF4", "MB4"};
     return names[static_cast<int>(m)];
@@ -182,13 +192,19 @@ public:
         check(rc, st.last_residual);
     }
     /// nsteps device-resident steps; returns the (nsteps+1) x 7 energy record.
-    std::vector<Observables> run(double h, int nsteps, std::vector<int>* iters = nullptr) {
+    std::vector<Observables> run(double h, int nsteps, std::vector<int>* iters = nullptr,
+                                 StepStats* stats = nullptr) {
         std::vector<Observables> rows(static_cast<size_t>(nsteps) + 1);
         std::vector<int> it(static_cast<size_t>(nsteps));
         mb4cu_stats st{};
         static_assert(sizeof(Observables) == 7 * sizeof(double), "layout");
         const int rc = mb4cu_method_run(ctx_, method_, h, nsteps, reinterpret_cast<double*>(rows.data()), it.data(),
                                         &st);
+        if (stats) {
+            stats->newton_iters += st.newton_iters;
+            stats->halvings += st.halvings;
+            stats->solve_seconds += st.solve_seconds;
+        }
         check(rc, st.last_residual);
         if (iters) *iters = it;
         return rows;

@@ -10,11 +10,12 @@ from paper_2003_04345_b200 import configs
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "tests", "cpp", "test_drop_in.cpp")
+SRC_HARNESS = os.path.join(ROOT, "tests", "cpp", "test_harness.cpp")
 LIBDIR = os.path.join(ROOT, "paper_2003_04345_b200")
 
 
-def build(out):
-    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-o", out,
+def build(out, src=SRC):
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", out,
            "-L", LIBDIR, "-lmb4cu", f"-Wl,-rpath,{LIBDIR}"]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
 
@@ -41,3 +42,19 @@ def test_cpp_drop_in_matches_reference_golden(tmp_path):
     g = np.load(os.path.join(ROOT, "tests", "golden", "ref_cfg1_10.npz"))
     ref = g["state_10"]
     assert np.linalg.norm(u - ref) / np.linalg.norm(ref) <= 1e-10
+
+
+def test_cpp_harness_mirror_compiles(tmp_path):
+    exe = str(tmp_path / "test_harness")
+    build(exe, SRC_HARNESS)
+    assert os.path.exists(exe)
+
+
+@pytest.mark.gpu
+def test_cpp_harness_drop_in_runs(tmp_path):
+    # reference-style harness code (RunConfig, parse_config_file, run, compare_methods,
+    # convergence_study, parallel_bench) compiled against include/nls2d
+    exe = str(tmp_path / "test_harness")
+    build(exe, SRC_HARNESS)
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
