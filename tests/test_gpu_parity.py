@@ -244,3 +244,25 @@ def test_speculative_final_sweep_miss_is_redone_exactly():
     for (u, _), ref in zip(got, (u1, u2, u3)):
         assert rel(u, ref) <= 1e-13
     assert prof["redone"] >= 1
+
+
+@pytest.mark.parametrize("nx,ny,lx,ly", [(2, 3, 2.0, 3.0), (5, 4, 5.0, 4.0), (7, 130, 7.0, 130.0),
+                                         (130, 7, 130.0, 7.0), (255, 33, 255.0, 40.0), (129, 129, 129.0, 129.0)])
+def test_ragged_lattices_default_path_match_oracle(nx, ny, lx, ly):
+    """Edge shapes through the default production path (deep first sweep,
+    speculative final sweep, isotropic and anisotropic, widths below / just above
+    one column band, the smallest lattices): 4 steps against the oracle."""
+    g = nls2d.GridSpec(nx, ny, lx, ly)
+    rng = np.random.default_rng(nx * 1000 + ny)
+    V = np.where(rng.uniform(size=nx * ny) < 0.1, 3.0, 0.0)
+    model = nls2d.GridModel(g, -1.0, V)
+    psi = random_state(nx * ny, nx + ny, 0.2)
+    h = 0.01
+    o = O.Oracle(nx, ny, -1.0, V, cx=model.cx, cy=model.cy)
+    ref, ref_obs, _ = o.run(psi, h, 4, eps=1e-14)
+    with nls2d.Session(model, nls2d.Mb4Scheme(), nls2d.NewtonConfig(1e-14, 50, 4)) as s:
+        s.set_state(psi)
+        obs, iters = s.run(h, 4)
+        got = s.get_state()
+    assert rel(got, ref) <= 1e-10
+    assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * max(1.0, abs(ref_obs[0, 3]))
