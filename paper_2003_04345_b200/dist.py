@@ -236,7 +236,7 @@ class DistributedSession:
         return self.finish(self.comm.allreduce_sum(self.b.obs_sums()))
 
     def _substep(self, h: float) -> Tuple[int, float]:
-        if hasattr(self.b, "sweep_reduce"):
+        if hasattr(self.b, "sweep_launch"):
             return self._substep_device(h)
         self.halo.exchange(F_U0)
         r = r_prev = float("nan")
@@ -261,12 +261,27 @@ class DistributedSession:
         is repeated with all stages if the reduced residual does not converge."""
         self.halo.exchange(F_U0)
         guess = getattr(self, "_guess", 0)
-        r = r_prev = float("nan")
-        for s in range(self.max_iters):
+        want0 = self.entry_sums is None
+        finals = {}
+
+        def launch(s):
+            # sweep s with its halo exchange and device-side reductions, no host wait
             if s > 0:
                 self.halo.exchange(F_SET0 + ((s - 1) & 1))
-            final = s > 0 and s == guess - 1
-            r, sums = self.b.sweep_reduce(h, s, final, self.comm, want_sums=(s == 0 and self.entry_sums is None))
+            finals[s] = s > 0 and s == guess - 1
+            self.b.sweep_launch(h, s, finals[s], self.comm, slot=s & 1, want_sums=(s == 0 and want0))
+
+        launch(0)
+        launched = 0
+        r = r_prev = float("nan")
+        for s in range(self.max_iters):
+            # look-ahead: a sweep the previous sub-step says will be needed is enqueued
+            # before this one's residual is read, so the host round trip overlaps the
+            # GPU work (every rank takes the same decision: the guess is global)
+            if launched == s and s + 1 < self.max_iters and s + 1 <= guess - 1:
+                launch(s + 1)
+                launched = s + 1
+            r, sums = self.b.sweep_read(slot=s & 1, want_sums=(s == 0 and want0))
             if sums is not None:
                 self.entry_sums = sums
             if not math.isfinite(r):
@@ -275,9 +290,12 @@ class DistributedSession:
                 self.b.commit(s + 1)
                 self._guess = s + 1
                 return s + 1, r
-            if final:
+            if finals[s]:
                 self.b.sweep_repeat(h, s)
             r_prev = r
+            if launched == s and s + 1 < self.max_iters:
+                launch(s + 1)
+                launched = s + 1
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
     def step(self, h: float) -> Tuple[int, int]:
@@ -375,18 +393,25 @@ class CudaBackend:
         self._chk(self.L.mb4cu_sweep(self.ctx, h, s, C.byref(r), _lib.dptr(sums)))
         return r.value, sums
 
-    def sweep_reduce(self, h, s, final, comm, want_sums=False):
-        """Sweep s with the residual max (and the energy sums) all-reduced on the
-        device, on the stream shared with NCCL; one host read."""
+    def sweep_launch(self, h, s, final, comm, slot=0, want_sums=False):
+        """Enqueue sweep s and the all-reduce of [residual max, energy sums] into the
+        device buffer `slot`, on the stream shared with NCCL (no host wait)."""
         if self._red is None:
-            self._red = self.torch.zeros(6, dtype=self.torch.float64, device=self.dev)
-        red = self._red
+            self._red = [self.torch.zeros(6, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
+        red = self._red[slot]
         self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, int(final), C.c_void_p(red.data_ptr())))
         comm.allreduce_max_(red[0:1])
         if want_sums:
             comm.allreduce_sum_(red[1:6])
-        host = red.cpu().numpy()
+
+    def sweep_read(self, slot=0, want_sums=False):
+        """Host read of a launched sweep's reduced [r, sums] (waits for it)."""
+        host = self._red[slot].cpu().numpy()
         return float(host[0]), (host[1:6].copy() if want_sums else None)
+
+    def sweep_reduce(self, h, s, final, comm, want_sums=False):
+        self.sweep_launch(h, s, final, comm, 0, want_sums)
+        return self.sweep_read(0, want_sums)
 
     def sweep_repeat(self, h, s):
         """Repeat sweep s storing every stage (after a missed final guess)."""
