@@ -511,7 +511,10 @@ struct MarchFirst {
     // z rows kept behind the newest: levels n >= 2 read u0 / V of row i - n from the ring
     static constexpr int BACK = MF >= 2 ? MF + 1 : 1;
     // rows in flight: light rows, prefetch deep to cover HBM latency (smem-bounded)
-    static constexpr int P = MF <= 2 ? 10 - (MF == 2 ? 2 : 0) : 8;
+#ifndef MB4_FIRST_P
+#define MB4_FIRST_P 8
+#endif
+    static constexpr int P = MF <= 2 ? 10 - (MF == 2 ? 2 : 0) : MB4_FIRST_P;
     static constexpr int S = P + 1 + BACK;
     // history depth of level n: the output reads g_n(i - MF), written MF - n iterations ago
     __host__ __device__ static constexpr int depth(int n) { return n >= MF - 2 ? 2 : MF - n + 1; }
