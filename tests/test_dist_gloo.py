@@ -125,6 +125,41 @@ class NumpyBackend:
         self.set_state(self._saved)
 
 
+class NumpyAsyncBackend(NumpyBackend):
+    """The device-reduction interface of dist.CudaBackend (sweep_launch / sweep_read /
+    sweep_repeat): reductions go through the Comm on tensors, reads are deferred, and
+    a sweep launched as the predicted final one does not store U1 / U2 (poisoned with
+    NaN here, stricter than the GPU's stale values) -- so the session's look-ahead,
+    speculation and repeat logic is exercised across processes."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self._red = [torch.zeros(6, dtype=torch.float64) for _ in range(2)]
+        self.launches = 0
+        self.repeats = 0
+
+    def sweep_launch(self, h, s, final, comm, slot=0, want_sums=False):
+        r, sums = NumpyBackend.sweep(self, h, s)
+        self.launches += 1
+        if final and s > 0:
+            for q in (0, 1):
+                self.U[s & 1][q][...] = np.nan
+        red = self._red[slot]
+        red[0] = r
+        red[1:6] = torch.from_numpy(np.asarray(sums, dtype=np.float64))
+        comm.allreduce_max_(red[0:1])
+        if want_sums:
+            comm.allreduce_sum_(red[1:6])
+
+    def sweep_read(self, slot=0, want_sums=False):
+        v = self._red[slot].numpy().copy()
+        return float(v[0]), (v[1:6] if want_sums else None)
+
+    def sweep_repeat(self, h, s):
+        NumpyBackend.sweep(self, h, s)
+        self.repeats += 1
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -159,6 +194,48 @@ def _reference(m, nsteps):
         u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=2)
         its.append(it)
     return u, its
+
+
+def _worker_async(rank, world, port, px, py, hs, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = configs.CONFIGS["cfg1"]
+        V, psi = configs.make_inputs(cfg)
+        dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
+        be = NumpyAsyncBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, 1, mf=6)
+        be.set_state(dec.block(psi))
+        sess = D.DistributedSession(dec, be, D.Comm("cpu"), cfg.gamma, 1.0, 1.0, cfg.epsilon)
+        sweeps = [sess.step(h)[0] for h in hs]
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), u=be.get_state(), sweeps=sweeps, repeats=be.repeats)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (2, 2)])
+def test_device_reduction_path_lookahead_and_speculation(tmp_path, px, py):
+    """The production multi-GPU control flow (deferred device reductions, the
+    look-ahead launch, the speculative U3-only final sweep and its repeat on a
+    miss -- forced by a longer second step) reproduces the single-domain iteration
+    bit for bit."""
+    cfg = configs.CONFIGS["cfg1"]
+    hs = [cfg.dt, cfg.dt, 2 * cfg.dt, cfg.dt]
+    world = px * py
+    mp.spawn(_worker_async, args=(world, _free_port(), px, py, hs, str(tmp_path)), nprocs=world, join=True)
+    V, psi = configs.make_inputs(cfg)
+    scheme = nls2d.Mb4Scheme()
+    u, its = psi, []
+    for h in hs:
+        u, it = SM.step(u, V, cfg.gamma, h, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+        its.append(it)
+    glob = np.zeros((cfg.ny, cfg.nx), dtype=np.complex128)
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        dec = D.Decomposition(cfg.nx, cfg.ny, px, py, r)
+        glob[dec.y0:dec.y0 + dec.lny, dec.x0:dec.x0 + dec.lnx] = d["u"].reshape(dec.lny, dec.lnx)
+        assert list(d["sweeps"]) == its
+        assert int(d["repeats"]) >= 1  # the longer step missed its predicted final sweep
+    assert np.array_equal(glob.reshape(-1), u)
 
 
 @pytest.mark.parametrize("px,py,m", [(2, 1, 1), (1, 2, 2), (2, 2, 1)])
