@@ -380,6 +380,10 @@ def run_ours(args, d: Dist):
             "traffic": measured_traffic(cfg.name, schedule_key(args)),
             "traffic_source": "ncu --set full, dram__bytes_read+write per launch (profiles/traffic.json)",
             "limiters": measured_limiters(cfg.name, schedule_key(args)),
+            # the same metric against the HBM bound of the stage iteration SURVEY.md 8(d)
+            # projected (5 sweeps at cfg5: 72 + 4 x 120 = 552 B/site-step): the deep first
+            # sweep and the U3-only final sweep remove bytes, so frac above understates it
+            "vs_hbm_bound_of_5_sweep_schedule": (value / d.world / (peak * 1e9 / 552.0)) if cfg.name == "cfg5" else None,
             "peak_kind": peak_kind,
             "kernel": "stage sweep",
             "alg_bytes_per_step": step_alg_bytes,
