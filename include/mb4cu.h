@@ -166,7 +166,9 @@ int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
  *   exchange u0 halos;  for s = 0, 1, ...: (s > 0: exchange halos of stage set
  *   (s-1) & 1);  mb4cu_sweep(ctx, h, s, &r, sums);  r = allreduce_max(r);
  *   stop when r <= eps;  mb4cu_commit_step(ctx, s + 1).
- * Fields: 0 = u0, 1 = V, 2 = stage set 0 (U1..U3), 3 = stage set 1.
+ * Fields: 0 = u0, 1 = V, 2 = stage set 0 (U1..U3), 3 = stage set 1 (sets m + 1 wide;
+ * u0 / V ghost wide); 4, 5 = stage set 0 / 1 ghost wide (halo-overlap mode, where the
+ * last sweep's U3 halos become the next step's u0 halos).
  * Sides: 0 = west (x low), 1 = east, 2 = south (y low), 3 = north.  Pack reads the
  * ghost-wide strip of owned sites adjacent to the side; unpack writes the ghost strip
  * on that side.  x sides cover the owned rows; y sides the full padded width, so an
@@ -187,6 +189,14 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
  * step result) is stored; if the reduced residual does not converge the caller
  * repeats the same sweep with final_guess = 0 before going on. */
 int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6);
+/* Halo-exchange overlap: sweep s in two launches.  region 1 = the boundary frame
+ * (the `ghost`-wide strips the neighbours' halos need; run it first, then start
+ * exchanging them), region 2 = the interior (needs no halo; launched with at most
+ * grid_cap CTAs, 0 = all, to leave SMs to the concurrent NCCL kernels) which then
+ * leaves [||r||_inf over both, energy sums] in dev_out6 like mb4cu_sweep_async.
+ * region 0 = the whole sub-domain (= mb4cu_sweep_async). */
+int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
+                       double* dev_out6);
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
 /* Local energy sums of the resident state (ghosts of u0 must be current). */
 int mb4cu_observables_sums(mb4cu_ctx* ctx, double* local_sums5);

@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
         "mb4cu_halo_unpack": (I, [P, I, I, P]),
         "mb4cu_sweep": (I, [P, D, I, DP, DP]),
         "mb4cu_sweep_async": (I, [P, D, I, I, P]),
+        "mb4cu_sweep_region": (I, [P, D, I, I, I, I, P]),
         "mb4cu_commit_step": (I, [P, I]),
         "mb4cu_observables_sums": (I, [P, DP]),
     }
@@ -175,5 +176,5 @@ EXPORTED = [
     "mb4cu_set_stream", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
     "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
     "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",
-    "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_commit_step", "mb4cu_observables_sums",
+    "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_sweep_region", "mb4cu_commit_step", "mb4cu_observables_sums",
 ]

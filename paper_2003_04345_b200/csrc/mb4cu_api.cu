@@ -1266,9 +1266,11 @@ int mb4cu_method_run(mb4cu_ctx* ctx, int method, double h, int nsteps, double* o
 namespace {
 
 // Halo width of a field: u0 and V feed the first sweep (depth mf -> mf + 1 layers);
-// the stage sets only the later sweeps (m + 1 layers).
+// the stage sets (fields 2, 3) only the later sweeps (m + 1 layers); fields 4, 5 are
+// the stage sets at the full ghost width (halo-overlap mode: U3 of the last sweep
+// becomes u0 of the next step, halos included).
 int halo_width(const mb4cu_ctx* ctx, int field) {
-    return field <= 1 ? ctx->ghost : std::min(ctx->ghost, ctx->m + 1);
+    return field <= 1 || field >= 4 ? ctx->ghost : std::min(ctx->ghost, ctx->m + 1);
 }
 
 // rectangle (x0, y0, w, h) of a halo side; pack == owned strip, unpack == ghost strip
@@ -1283,7 +1285,7 @@ void halo_rect(const mb4cu_ctx* ctx, int field, int side, bool pack, int* x0, in
 }
 
 int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
-    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3 || !buf)
+    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 5 || side < 0 || side > 3 || !buf)
         return fail(ctx, MB4CU_INVALID, "halo: bad context / field / side / buffer");
     int x0, y0, w, h;
     halo_rect(ctx, field, side, pack, &x0, &y0, &w, &h);
@@ -1296,7 +1298,7 @@ int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
             arr[0] = ctx->u0;
         } else {
             narr = 3;
-            for (int q = 0; q < 3; ++q) arr[q] = ctx->U[field - 2][q];
+            for (int q = 0; q < 3; ++q) arr[q] = ctx->U[(field - 2) & 1][q];
         }
         MB4_CUDA(ctx, mb4cu::launch_halo_copy2(arr, narr, ctx->pitch, ctx->ghost, x0, y0, w, h,
                                                reinterpret_cast<double2*>(buf), pack, ctx->stream));
@@ -1307,7 +1309,7 @@ int halo_xfer(mb4cu_ctx* ctx, int field, int side, double* buf, bool pack) {
 }  // namespace
 
 size_t mb4cu_halo_count(const mb4cu_ctx* ctx, int field, int side) {
-    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 3 || side < 0 || side > 3) return 0;
+    if (!ctx || ctx->ghost <= 0 || field < 0 || field > 5 || side < 0 || side > 3) return 0;
     int x0, y0, w, h;
     halo_rect(ctx, field, side, true, &x0, &y0, &w, &h);
     const size_t sites = static_cast<size_t>(w) * h;
@@ -1350,28 +1352,67 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
     return MB4CU_OK;
 }
 
-int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6) {
+namespace {
+
+// Output rectangles of a region of the sub-domain: 0 all, 1 the boundary frame of
+// width ghost (the sites the neighbours' halos need), 2 the interior (needs no halo).
+int region_rects(const mb4cu_ctx* ctx, int region, int rects[4][4]) {
+    const int w = ctx->ghost, nx = ctx->nx, ny = ctx->ny;
+    const bool thin = nx <= 2 * w || ny <= 2 * w;  // no interior: the frame is everything
+    if (region == 0 || (region == 1 && thin)) {
+        const int r[4] = {0, 0, nx, ny};
+        std::memcpy(rects[0], r, sizeof(r));
+        return 1;
+    }
+    if (region == 2) {
+        if (thin) return 0;
+        const int r[4] = {w, w, nx - 2 * w, ny - 2 * w};
+        std::memcpy(rects[0], r, sizeof(r));
+        return 1;
+    }
+    const int f[4][4] = {{0, 0, nx, w}, {0, ny - w, nx, w}, {0, w, w, ny - 2 * w}, {nx - w, w, w, ny - 2 * w}};
+    std::memcpy(rects, f, sizeof(f));
+    return 4;
+}
+
+}  // namespace
+
+int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
+                       double* dev_out6) {
     if (!ctx || ctx->ghost <= 0) return fail(ctx, MB4CU_INVALID, "sweep: sub-domain contexts only");
-    if (!(h > 0.0) || s < 0 || !dev_out6) return fail(ctx, MB4CU_INVALID, "sweep: h > 0, s >= 0, output buffer");
+    if (!(h > 0.0) || s < 0 || region < 0 || region > 2 || (region != 1 && !dev_out6))
+        return fail(ctx, MB4CU_INVALID, "sweep: h > 0, s >= 0, region 0..2, output buffer");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     const SweepConsts c = make_consts(ctx, h);
-    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
-    MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
-                                            ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
-                                            ctx->device, ctx->stream, ctx->ghost, s,
-                                            final_guess && s > 0 ? s : -1));
-    // [local ||r||_inf, the 5 energy sums of u0 (s = 0)] -> the caller's device buffer
-    static_assert(offsetof(mb4cu::StepStatus, obs) == offsetof(mb4cu::StepStatus, rlast) + sizeof(double),
-                  "rlast and obs are contiguous");
-    MB4_CUDA(ctx, cudaMemcpyAsync(dev_out6, reinterpret_cast<const char*>(ctx->d_status) +
-                                                offsetof(mb4cu::StepStatus, rlast),
-                                  sizeof(double) * (1 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
-    if (ctx->profiling) {
-        ctx->prof.launches += 1;
-        ctx->prof.sweeps += 1;
-        ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : (final_guess ? 88.0 : 120.0));
+    int rects[4][4];
+    const int nrect = region_rects(ctx, region, rects);
+    // the frame (or the whole domain) starts the residual max; the interior adds to it
+    if (region != 2) MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
+    if (nrect > 0) {
+        MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
+                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status, 1, -1.0,
+                                                s == 0 ? 1 : 0, c, ctx->device, ctx->stream, ctx->ghost, s,
+                                                final_guess && s > 0 ? s : -1, nrect, rects, region == 2 ? 1 : 0,
+                                                region == 2 ? grid_cap : 0));
+        if (ctx->profiling) ctx->prof.launches += 1;
+    }
+    if (region != 1) {
+        // [local ||r||_inf, the 5 energy sums of u0 (s = 0)] -> the caller's device buffer
+        static_assert(offsetof(mb4cu::StepStatus, obs) == offsetof(mb4cu::StepStatus, rlast) + sizeof(double),
+                      "rlast and obs are contiguous");
+        MB4_CUDA(ctx, cudaMemcpyAsync(dev_out6, reinterpret_cast<const char*>(ctx->d_status) +
+                                                    offsetof(mb4cu::StepStatus, rlast),
+                                      sizeof(double) * (1 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (ctx->profiling) {
+            ctx->prof.sweeps += 1;
+            ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : (final_guess ? 88.0 : 120.0));
+        }
     }
     return MB4CU_OK;
+}
+
+int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6) {
+    return mb4cu_sweep_region(ctx, h, s, final_guess, 0, 0, dev_out6);
 }
 
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps) {

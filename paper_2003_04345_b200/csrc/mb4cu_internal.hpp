@@ -136,6 +136,14 @@ struct StepArgs {
     int pitch;
     int sweep0;                 // global index of the first sweep of this launch
     int spec_sweep;             // global sweep index stored as U3 only (-1: none)
+    // Output rectangles (x0, y0, w, h) of this launch in sub-domain mode: the
+    // boundary frame or the interior, so the halo exchange of the frame overlaps
+    // the interior sweep.  nrect = 0: the whole (sub-)domain.
+    int nrect;
+    int rect[4][4];
+    int obs_accumulate;         // add this launch's energy sums to status->obs
+    int grid_cap;               // host side: at most this many CTAs (0 = full occupancy), e.g.
+                                // to leave SMs to NCCL kernels running concurrently
 };
 
 // ---- the other integrators (methods.cu) ------------------------------------
@@ -193,7 +201,8 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
-                               int ghost, int sweep0, int spec_sweep = -1);
+                               int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
+                               const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0);
 int march2_grid_size(int mf, int m, int device);
 
 // Halo transfer between a padded sub-domain array set and a contiguous buffer

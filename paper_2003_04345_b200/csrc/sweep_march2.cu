@@ -175,6 +175,7 @@ struct March3 {
 
     struct Seg {
         int X0, Y0, R, yz0, nzrows;
+        int xlim;        // right edge (exclusive) of the output rectangle
         int smask;       // stages stored (bit q): 7, or 4 = U3 only (speculative final sweep)
         int gxa, gxb;    // global columns of smem columns t and t + NT (t < 2)
         int next_row;    // global (periodic) row of the next z row to issue
@@ -251,7 +252,7 @@ struct March3 {
 
         const int yrel = i - 2 * M;  // output row offset from Y0
         const int xout = s.X0 - M + t;
-        const bool out_ok = yrel >= 0 && yrel < s.R && t >= M && t < NT - M && xout < a.nx;
+        const bool out_ok = yrel >= 0 && yrel < s.R && t >= M && t < NT - M && xout < s.xlim;
         const int par = j & 1, ppar = par ^ 1;
 
         // ---- own column: new z row j --------------------------------------------
@@ -302,7 +303,7 @@ struct March3 {
                     for (int k = 0; k < 3; ++k) pb[k] = make_double2(cf.fs(k) * f.x, cf.fs(k) * f.y);
                 }
                 // energy monitor of u0 on owned sites (lattice.cpp:106-137)
-                if (i >= M && i < M + s.R && t >= M && t < NT - M && xout < a.nx) {
+                if (i >= M && i < M + s.R && t >= M && t < NT - M && xout < s.xlim) {
                     const double vn = v * n2;
                     const double sc = ISO ? c.cx : 1.0;
                     acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
@@ -434,12 +435,13 @@ struct March3 {
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
-                        double2* const uout[3], int band, int Y0, int R, unsigned& rmax,
+                        double2* const uout[3], int X0, int xlim, int Y0, int R, unsigned& rmax,
                         double acc[kObsFields], int smask) {
         const Coef<ISO, DEF> cf{c};
         Seg s;
         s.smask = smask;
-        s.X0 = band * G::TX;
+        s.X0 = X0;
+        s.xlim = xlim;
         s.Y0 = Y0;
         s.R = R;
         s.yz0 = Y0 - M - 1;
@@ -565,6 +567,7 @@ struct MarchFirst {
 
     struct Seg {
         int X0, Y0, R, nzrows, gxa, gxb, next_row;
+        int xlim;  // right edge (exclusive) of the output rectangle
         size_t next_off;
     };
 
@@ -645,7 +648,7 @@ struct MarchFirst {
 
         const int yrel = i - 2 * MF;
         const int xout = s.X0 - MF + t;
-        const bool out_ok = yrel >= 0 && yrel < s.R && t >= MF && t < NT - MF && xout < a.nx;
+        const bool out_ok = yrel >= 0 && yrel < s.R && t >= MF && t < NT - MF && xout < s.xlim;
 
         zw[0] = zu0[slot_new * ZW + cc];  // window: [0] new (z row j), [1] centre, [2] down
         vw[0] = zv[slot_new * ZW + cc];
@@ -659,7 +662,7 @@ struct MarchFirst {
         const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
         const double gy = fma(-cf.g() * n2, u0c.y, w0.y);
         const double2 f = make_double2(gy, -gx);
-        if (i >= MF && i < MF + s.R && t >= MF && t < NT - MF && xout < a.nx) {
+        if (i >= MF && i < MF + s.R && t >= MF && t < NT - MF && xout < s.xlim) {
             const double vn = v * n2;
             const double sc = ISO ? c.cx : 1.0;
             acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
@@ -706,11 +709,12 @@ struct MarchFirst {
         for (int n = 0; n + 3 <= MF; ++n) hs[n] = hs[n] + 1 == depth(n) ? 0 : hs[n] + 1;
     }
 
-    __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int band, int Y0,
-                        int R, unsigned& rmax, double acc[kObsFields]) {
+    __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int X0, int xlim,
+                        int Y0, int R, unsigned& rmax, double acc[kObsFields]) {
         const Coef<ISO> cf{c};
         Seg s;
-        s.X0 = band * TX;
+        s.X0 = X0;
+        s.xlim = xlim;
         s.Y0 = Y0;
         s.R = R;
         s.nzrows = R + 2 * MF + 2;
@@ -744,6 +748,39 @@ struct MarchFirst {
     }
 };
 
+// Split the band-rows of this launch's output rectangles evenly over the grid and
+// march each segment (a run of rows of one band of one rectangle).
+template <int TX, class Run>
+__device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) {
+    const int nr = a.nrect > 0 ? a.nrect : 1;
+    auto rect = [&](int r, int k) {
+        if (a.nrect > 0) return a.rect[r][k];
+        return k == 2 ? a.nx : (k == 3 ? a.ny : 0);
+    };
+    long long total = 0;
+    for (int r = 0; r < nr; ++r) total += static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
+    const long long G = gridDim.x;
+    const long long b0 = total * blockIdx.x / G;
+    const long long b1 = total * (blockIdx.x + 1) / G;
+    for (long long pos = b0; pos < b1;) {
+        long long base = 0;
+        int r = 0;
+        for (; r + 1 < nr; ++r) {
+            const long long cnt = static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
+            if (pos < base + cnt) break;
+            base += cnt;
+        }
+        const int h = rect(r, 3);
+        const long long local = pos - base;
+        const int band = static_cast<int>(local / h);
+        const int row = static_cast<int>(local - static_cast<long long>(band) * h);
+        const long long band_end = base + static_cast<long long>(band + 1) * h;
+        const long long seg_end = band_end < b1 ? band_end : b1;
+        run(rect(r, 0) + band * TX, rect(r, 0) + rect(r, 2), rect(r, 1) + row, static_cast<int>(seg_end - pos));
+        pos = seg_end;
+    }
+}
+
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
@@ -751,34 +788,15 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
     if constexpr (FIRST && M >= 1) {
         using MFirst = MarchFirst<M, NT, ISO, GHOST>;
         MFirst mf(smem);
-        const long long total = static_cast<long long>((a.nx + MFirst::TX - 1) / MFirst::TX) * a.ny;
-        const long long G = gridDim.x;
-        const long long b0 = total * blockIdx.x / G;
-        const long long b1 = total * (blockIdx.x + 1) / G;
-        for (long long pos = b0; pos < b1;) {
-            const int band = static_cast<int>(pos / a.ny);
-            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
-            const long long band_end = static_cast<long long>(band + 1) * a.ny;
-            const long long seg_end = band_end < b1 ? band_end : b1;
-            mf.run(a, c, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc);
-            pos = seg_end;
-        }
+        for_segments<MFirst::TX>(a, [&](int X0, int xlim, int Y0, int R) {
+            mf.run(a, c, uout, X0, xlim, Y0, R, rmax, acc);
+        });
     } else {
         March3<M, NT, FIRST, ISO, GHOST, DEF> m(smem);
         // band-rows of this sweep's band width (TX depends on M)
-        const long long total = static_cast<long long>((a.nx + Geom3<M, NT>::TX - 1) / Geom3<M, NT>::TX) * a.ny;
-        const long long G = gridDim.x;
-        const long long b0 = total * blockIdx.x / G;
-        const long long b1 = total * (blockIdx.x + 1) / G;
-        long long pos = b0;
-        while (pos < b1) {
-            const int band = static_cast<int>(pos / a.ny);
-            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
-            const long long band_end = static_cast<long long>(band + 1) * a.ny;
-            const long long seg_end = band_end < b1 ? band_end : b1;
-            m.run(a, c, uin, uout, band, row, static_cast<int>(seg_end - pos), rmax, acc, smask);
-            pos = seg_end;
-        }
+        for_segments<Geom3<M, NT>::TX>(a, [&](int X0, int xlim, int Y0, int R) {
+            m.run(a, c, uin, uout, X0, xlim, Y0, R, rmax, acc, smask);
+        });
     }
 }
 
@@ -895,7 +913,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
         double v = 0.0;
         for (int b = 0; b < static_cast<int>(gridDim.x); ++b) v += a.obs_partial[b * kObsFields + threadIdx.x];
-        a.status->obs[threadIdx.x] = v;
+        a.status->obs[threadIdx.x] = (a.obs_accumulate ? a.status->obs[threadIdx.x] : 0.0) + v;
     }
 }
 
@@ -918,7 +936,8 @@ struct Launcher3 {
     }
 
     static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
-        const int grid = grid_size(device);
+        int grid = grid_size(device);
+        if (a.grid_cap > 0 && a.grid_cap < grid) grid = a.grid_cap;
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
         return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>),
@@ -968,8 +987,14 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
-                               int ghost, int sweep0, int spec_sweep) {
+                               int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
+                               int obs_accumulate, int grid_cap) {
     StepArgs a{};
+    a.nrect = nrect;
+    for (int r = 0; r < nrect && r < 4; ++r)
+        for (int k = 0; k < 4; ++k) a.rect[r][k] = rects[r][k];
+    a.obs_accumulate = obs_accumulate;
+    a.grid_cap = grid_cap;
     a.nx = nx;
     a.ny = ny;
     a.u0 = u0;

@@ -31,6 +31,7 @@ from . import _lib
 
 WEST, EAST, SOUTH, NORTH = 0, 1, 2, 3
 F_U0, F_V, F_SET0, F_SET1 = 0, 1, 2, 3
+F_SETFULL0 = 4  # stage set 0 / 1 at the full ghost width (halo-overlap mode)
 
 # Stopping rule, identical to the device kernels (mb4cu_internal.hpp: stage_converged):
 # the reference test r <= eps plus a margin on the predicted next update.
@@ -232,10 +233,14 @@ class DistributedSession:
         return np.array([uk, ui, ext, uk + ui + ext, prob, quart / (prob * prob) if prob > 0 else 0.0, quart])
 
     def observables(self) -> np.ndarray:
+        if getattr(self.b, "overlap", False):
+            self.b.wait_exchange()
         self.halo.exchange(F_U0)
         return self.finish(self.comm.allreduce_sum(self.b.obs_sums()))
 
     def _substep(self, h: float) -> Tuple[int, float]:
+        if getattr(self.b, "overlap", False):
+            return self._substep_overlap(h)
         if hasattr(self.b, "sweep_launch"):
             return self._substep_device(h)
         self.halo.exchange(F_U0)
@@ -298,9 +303,62 @@ class DistributedSession:
                 launched = s + 1
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
+    def _substep_overlap(self, h: float) -> Tuple[int, float]:
+        """Halo-exchange overlap: each sweep runs its boundary frame
+        first, the frame's halo exchange then proceeds on a side stream while the
+        interior is swept, and the next sweep waits for both.  The exchange after the
+        last sweep carries U3 at the full ghost width, so the next step's u0 halos
+        are already in place.  Device-side reductions, look-ahead and the speculative
+        final sweep as in _substep_device."""
+        if not self.b.u0_halo_ok:
+            self.b.wait_exchange()
+            self.halo.exchange(F_U0)
+        self.b.u0_halo_ok = False
+        guess = getattr(self, "_guess", 0)
+        want0 = self.entry_sums is None
+        finals = {}
+
+        def launch(s, final=None):
+            finals[s] = (s > 0 and s == guess - 1) if final is None else final
+            self.b.wait_exchange()  # halos of the input (u0 or the previous stage set)
+            self.b.sweep_frame(h, s, finals[s])
+            self.b.exchange_async(self.halo, F_SETFULL0 + (s & 1))
+            self.b.sweep_interior(h, s, finals[s], self.comm, slot=s & 1, want_sums=(s == 0 and want0))
+
+        launch(0)
+        launched = 0
+        r = r_prev = float("nan")
+        for s in range(self.max_iters):
+            if launched == s and s + 1 < self.max_iters and s + 1 <= guess - 1:
+                launch(s + 1)
+                launched = s + 1
+            r, sums = self.b.sweep_read(slot=s & 1, want_sums=(s == 0 and want0))
+            if sums is not None:
+                self.entry_sums = sums
+            if not math.isfinite(r):
+                raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
+            if stage_converged(r, r_prev, s, self.eps):
+                self.b.commit(s + 1)
+                self._guess = s + 1
+                # the exchange after sweep s moved U3 ghost-wide: the new u0's halos
+                # (a look-ahead sweep s + 1 writes the other stage set; wait_exchange
+                # orders every later use after the pending exchanges)
+                self.b.u0_halo_ok = True
+                return s + 1, r
+            if finals[s]:
+                launch(s, final=False)  # repeat the missed final sweep with every stage
+                self.b.sweep_read(slot=s & 1, want_sums=False)
+            r_prev = r
+            if launched == s and s + 1 < self.max_iters:
+                launch(s + 1)
+                launched = s + 1
+        raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
+
     def step(self, h: float) -> Tuple[int, int]:
         """One MB4 step with the reference halving policy; returns (sweeps, halvings)."""
         self.entry_sums = None
+        if getattr(self.b, "overlap", False):
+            self.b.wait_exchange()
         last = 0.0
         for hv in range(self.max_halvings + 1):
             sub = 1 << hv
@@ -337,7 +395,10 @@ class CudaBackend:
 
     def __init__(self, dec: Decomposition, V_block: np.ndarray, scheme, gamma: float, cx: float, cy: float,
                  epsilon: float, max_iters: int, neumann_terms: int, device: int,
-                 neumann_first: int = 6):
+                 neumann_first: int = 6, overlap: bool = False, reserve_sms: int = 0):
+        """overlap: sweep the boundary frame first and exchange its halos on a side
+        stream while the interior is swept (the interior launch leaves reserve_sms
+        SMs to the concurrent NCCL kernels)."""
         import torch
 
         self.torch = torch
@@ -367,6 +428,20 @@ class CudaBackend:
         self._saved = None
         self._red = None
         self._scratch = None
+        self.u0_halo_ok = False
+        self.overlap = overlap
+        self._pending = False
+        if overlap:
+            # the context runs on `compute` (made torch's current stream, so NCCL
+            # collectives order after the sweeps); halo exchanges run on `comms`
+            self.compute = torch.cuda.Stream(self.dev)
+            self.comms = torch.cuda.Stream(self.dev)
+            torch.cuda.set_stream(self.compute)
+            self.L.mb4cu_set_stream(self.ctx, C.c_void_p(self.compute.cuda_stream))
+            self._ev_frame = torch.cuda.Event()
+            self._ev_x = torch.cuda.Event()
+            props = torch.cuda.get_device_properties(self.dev)
+            self.grid_cap = 2 * max(1, props.multi_processor_count - reserve_sms) if reserve_sms > 0 else 0
 
     def _chk(self, rc):
         if rc:
@@ -406,12 +481,50 @@ class CudaBackend:
 
     def sweep_read(self, slot=0, want_sums=False):
         """Host read of a launched sweep's reduced [r, sums] (waits for it)."""
-        host = self._red[slot].cpu().numpy()
+        host = self._red_buf(slot).cpu().numpy()
         return float(host[0]), (host[1:6].copy() if want_sums else None)
 
     def sweep_reduce(self, h, s, final, comm, want_sums=False):
         self.sweep_launch(h, s, final, comm, 0, want_sums)
         return self.sweep_read(0, want_sums)
+
+    # ---- halo-exchange overlap (DistributedSession._substep_overlap) -------------
+    def _red_buf(self, slot):
+        if self._red is None:
+            self._red = [self.torch.zeros(6, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
+        return self._red[slot]
+
+    def sweep_frame(self, h, s, final):
+        """Sweep s on the boundary frame (compute stream); marks it for the exchange."""
+        self._chk(self.L.mb4cu_sweep_region(self.ctx, h, s, int(final), 1, 0, None))
+        self._ev_frame.record(self.compute)
+
+    def exchange_async(self, halo, field):
+        """Exchange the frame just swept on the side stream (pack, NCCL, unpack)."""
+        self.comms.wait_event(self._ev_frame)
+        self.L.mb4cu_set_stream(self.ctx, C.c_void_p(self.comms.cuda_stream))
+        try:
+            with self.torch.cuda.stream(self.comms):
+                halo.exchange(field)
+        finally:
+            self.L.mb4cu_set_stream(self.ctx, C.c_void_p(self.compute.cuda_stream))
+        self._ev_x.record(self.comms)
+        self._pending = True
+
+    def wait_exchange(self):
+        if self._pending:
+            self.compute.wait_event(self._ev_x)
+            self._pending = False
+
+    def sweep_interior(self, h, s, final, comm, slot=0, want_sums=False):
+        """Sweep s on the interior (concurrently with the exchange), then the
+        device-side reduction of [r, sums] into slot (compute stream)."""
+        red = self._red_buf(slot)
+        self._chk(self.L.mb4cu_sweep_region(self.ctx, h, s, int(final), 2, self.grid_cap,
+                                            C.c_void_p(red.data_ptr())))
+        comm.allreduce_max_(red[0:1])
+        if want_sums:
+            comm.allreduce_sum_(red[1:6])
 
     def sweep_repeat(self, h, s):
         """Repeat sweep s storing every stage (after a missed final guess)."""
@@ -428,6 +541,9 @@ class CudaBackend:
         return sums
 
     def set_state(self, u_block):
+        self.u0_halo_ok = False
+        if self.overlap:
+            self.wait_exchange()
         u = np.ascontiguousarray(u_block, dtype=np.complex128)
         self._chk(self.L.mb4cu_set_state(self.ctx, _lib.dptr(u)))
 

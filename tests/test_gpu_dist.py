@@ -76,7 +76,7 @@ class LoopbackComm:
         self.h.bar.wait()
 
 
-def _run_decomposed(name, px, py, m, nsteps):
+def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None):
     cfg = configs.CONFIGS[name]
     V, psi = configs.make_inputs(cfg)
     world = px * py
@@ -89,10 +89,14 @@ def _run_decomposed(name, px, py, m, nsteps):
             torch.cuda.set_device(0)
             dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
             be = D.CudaBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon,
-                               cfg.max_iters, m, 0)
+                               cfg.max_iters, m, 0, overlap=overlap)
             be.set_state(dec.block(psi))
             sess = D.DistributedSession(dec, be, LoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon)
-            obs, sweeps = sess.run(cfg.dt, nsteps)
+            if hs is None:
+                obs, sweeps = sess.run(cfg.dt, nsteps)
+            else:
+                sweeps = [sess.step(h)[0] for h in hs]
+                obs = None
             out[rank] = (dec, be.get_state(), obs, sweeps)
             be.close()
         except Exception as exc:  # surface thread failures
@@ -128,3 +132,27 @@ def test_subdomain_path_matches_single_domain(px, py, m):
     H = obs_dec[:, 3]
     assert np.abs(H - obs[:, 3]).max() <= 1e-14 * abs(H[0])
     assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
+
+
+@pytest.mark.parametrize("px,py", [(1, 1), (2, 1), (2, 2)])
+def test_halo_overlap_path_matches_single_domain(px, py):
+    """Boundary frame first, its halo exchange on a side stream while the interior
+    is swept (mb4cu_sweep_region), U3 halos carried into the next step: the same
+    trajectory bit for bit as the single-domain kernel, including a step that misses
+    its predicted final sweep (the longer third step)."""
+    name = "cfg2"
+    cfg = configs.CONFIGS[name]
+    hs = [cfg.dt, cfg.dt, 2 * cfg.dt, cfg.dt]
+    u_dec, _, sweeps_dec = _run_decomposed(name, px, py, 1, len(hs), overlap=True, hs=hs)
+    V, psi = configs.make_inputs(cfg)
+    with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg),
+                       neumann_terms=1) as s:
+        s.set_state(psi)
+        sweeps = []
+        for h in hs:
+            st = nls2d.StepStats()
+            s.step(h, st)
+            sweeps.append(st.newton_iters)
+        u = s.get_state()
+    assert list(sweeps_dec) == sweeps
+    assert np.array_equal(u_dec, u), np.abs(u_dec - u).max()
