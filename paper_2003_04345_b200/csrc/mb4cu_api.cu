@@ -291,7 +291,7 @@ bool stiff_step(const mb4cu_ctx* ctx, double h) {
 // matrix-free GMRES(m) stage solves (restating iterative.cpp:68-153 without the
 // ILU(0) preconditioner); O(N) work on the device, Hessenberg on the host.
 
-constexpr int kKrylovRestart = 50;
+constexpr int kKrylovRestart = 30;  // the Fourier-preconditioned solves converge in < 10 iterations
 constexpr int kKrylovMaxIters = 2000;
 constexpr double kKrylovTol = 1e-13;
 
