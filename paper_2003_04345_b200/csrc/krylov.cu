@@ -29,6 +29,28 @@ struct Nbr {
     size_t c, l, r, d, u;
 };
 
+// Every site: rows round-robin over the blocks, columns over the threads; periodic
+// neighbours by compare-and-select (no integer division in the loop).
+template <class F>
+__device__ __forceinline__ void for_sites(int nx, int ny, const F& f) {
+    for (int j = blockIdx.x; j < ny; j += gridDim.x) {
+        const size_t row = static_cast<size_t>(j) * nx;
+        const size_t dn = static_cast<size_t>(j == 0 ? ny - 1 : j - 1) * nx;
+        const size_t up = static_cast<size_t>(j == ny - 1 ? 0 : j + 1) * nx;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            Nbr q;
+            q.c = row + i;
+            q.l = row + (i == 0 ? nx - 1 : i - 1);
+            q.r = row + (i == nx - 1 ? 0 : i + 1);
+            q.d = dn + i;
+            q.u = up + i;
+            f(q.c, q);
+        }
+    }
+}
+
+int row_blocks(int ny) { return ny < 148 * 8 ? ny : 148 * 8; }
+
 __device__ __forceinline__ Nbr neighbours(size_t k, int nx, int ny) {
     const int j = static_cast<int>(k / nx), i = static_cast<int>(k - static_cast<size_t>(j) * nx);
     Nbr n;
@@ -53,9 +75,7 @@ struct PhiIn {
 
 // b_k = -(T^-1 Phi)_k at every site
 __global__ void __launch_bounds__(kT) phibar_kernel(const PhiIn p, const __grid_constant__ SweepConsts c) {
-    const size_t n = static_cast<size_t>(p.nx) * p.ny;
-    GRID_LOOP(k, n) {
-        const Nbr q = neighbours(k, p.nx, p.ny);
+    for_sites(p.nx, p.ny, [&](size_t k, const Nbr& q) {
         const double2* zp[4] = {p.u0, p.st[0], p.st[1], p.st[2]};
         double2 z[4], w[4];
 #pragma unroll
@@ -68,7 +88,7 @@ __global__ void __launch_bounds__(kT) phibar_kernel(const PhiIn p, const __grid_
         to_eigen(c, phi, pb);
 #pragma unroll
         for (int s = 0; s < 3; ++s) p.b[s][k] = make_double2(-pb[s].x, -pb[s].y);
-    }
+    });
 }
 
 // y = x - hl * J(u0) x
@@ -76,15 +96,13 @@ __global__ void __launch_bounds__(kT) stage_matvec_kernel(const double2* __restr
                                                           const double2* __restrict__ u0, const double* __restrict__ V,
                                                           int nx, int ny, double hl,
                                                           const __grid_constant__ SweepConsts c) {
-    const size_t n = static_cast<size_t>(nx) * ny;
-    GRID_LOOP(k, n) {
-        const Nbr q = neighbours(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nbr& q) {
         const double2 t = x[q.c];
         const double2 a = kv_site(c, V[k], t, x[q.l], x[q.r], x[q.d], x[q.u]);
         const JDiag d = jdiag(u0[k]);
         const double2 jt = j_site(c, d, t, a);
         y[k] = make_double2(fma(-hl, jt.x, t.x), fma(-hl, jt.y, t.y));
-    }
+    });
 }
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -310,13 +328,13 @@ cudaError_t kr_phibar(int nx, int ny, const double2* u0, const double2* const st
         p.st[i] = st[i];
         p.b[i] = b[i];
     }
-    phibar_kernel<<<blocks(static_cast<size_t>(nx) * ny), kT, 0, s>>>(p, c);
+    phibar_kernel<<<row_blocks(ny), kT, 0, s>>>(p, c);
     return cudaGetLastError();
 }
 
 cudaError_t kr_matvec(const double2* x, double2* y, const double2* u0, const double* V, int nx, int ny, double hl,
                       const SweepConsts& c, cudaStream_t s) {
-    stage_matvec_kernel<<<blocks(static_cast<size_t>(nx) * ny), kT, 0, s>>>(x, y, u0, V, nx, ny, hl, c);
+    stage_matvec_kernel<<<row_blocks(ny), kT, 0, s>>>(x, y, u0, V, nx, ny, hl, c);
     return cudaGetLastError();
 }
 

@@ -28,6 +28,25 @@ struct Nb {
     size_t l, r, d, u;
 };
 
+// Every site of the lattice: rows round-robin over the blocks, columns over the
+// threads (coalesced); periodic neighbours by compare-and-select, no division.
+template <class F>
+__device__ __forceinline__ void for_sites(int nx, int ny, const F& f) {
+    for (int j = blockIdx.x; j < ny; j += gridDim.x) {
+        const size_t row = static_cast<size_t>(j) * nx;
+        const size_t dn = static_cast<size_t>(j == 0 ? ny - 1 : j - 1) * nx;
+        const size_t up = static_cast<size_t>(j == ny - 1 ? 0 : j + 1) * nx;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            Nb q;
+            q.l = row + (i == 0 ? nx - 1 : i - 1);
+            q.r = row + (i == nx - 1 ? 0 : i + 1);
+            q.d = dn + i;
+            q.u = up + i;
+            f(row + i, q);
+        }
+    }
+}
+
 __device__ __forceinline__ Nb nbrs(size_t k, int nx, int ny) {
     const int j = static_cast<int>(k / nx), i = static_cast<int>(k - static_cast<size_t>(j) * nx);
     Nb n;
@@ -89,8 +108,7 @@ __global__ void __launch_bounds__(kT) rk4_stage_kernel(int stage, int nx, int ny
                                                        double2* __restrict__ acc, double2* __restrict__ out,
                                                        const MethodConsts c) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    MGRID_LOOP(k, n) {
-        const Nb q = nbrs(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nb& q) {
         const double2 kk = f_at(c, x, V, k, q);
         const double2 u = u0[k];
         if (stage == 1) {
@@ -102,7 +120,7 @@ __global__ void __launch_bounds__(kT) rk4_stage_kernel(int stage, int nx, int ny
         } else {
             out[k] = cadd(u, cscale(c.h / 6.0, cadd(acc[k], kk)));
         }
-    }
+        });
 }
 
 // ---- residuals b = -G of the implicit methods -------------------------------
@@ -111,8 +129,7 @@ __global__ void __launch_bounds__(kT) residual_kernel(int method, int nx, int ny
                                                       const double* __restrict__ V, const double2* __restrict__ unk,
                                                       double2* __restrict__ b, const MethodConsts c) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    MGRID_LOOP(k, n) {
-        const Nb q = nbrs(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nb& q) {
         const double2 z0 = u0[k];
         if (method == kMethodGauss2) {
             // g = u - u0 - (h/2) f(u)   (integrators.cpp:126-128)
@@ -168,7 +185,7 @@ __global__ void __launch_bounds__(kT) residual_kernel(int method, int nx, int ny
                 b[i * n + k] = make_double2(-g.x, -g.y);
             }
         }
-    }
+        });
 }
 
 // ---- Newton matrix applied matrix-free -------------------------------------
@@ -177,8 +194,7 @@ __global__ void __launch_bounds__(kT) newton_matvec_kernel(int s, int nx, int ny
                                                            double2* __restrict__ y, const double2* __restrict__ u0,
                                                            const double* __restrict__ V, const MethodConsts c) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    MGRID_LOOP(k, n) {
-        const Nb q = nbrs(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nb& q) {
         const double2 z = u0[k];
         const double pp = z.x * z.x, qq = z.y * z.y;
         const double al = fma(3.0, pp, qq), be = 2.0 * z.x * z.y, de = fma(3.0, qq, pp);
@@ -197,7 +213,7 @@ __global__ void __launch_bounds__(kT) newton_matvec_kernel(int s, int nx, int ny
             const double2 xi = x[i * n + k];
             y[i * n + k] = make_double2(fma(-c.h, acc.x, xi.x), fma(-c.h, acc.y, xi.y));
         }
-    }
+        });
 }
 
 // unk += x over len complex entries; ||x||_inf over the split reals (bit pattern)
@@ -220,12 +236,11 @@ __global__ void __launch_bounds__(kT) avf4_init_kernel(int nx, int ny, const dou
                                                        const double* __restrict__ V, double2* __restrict__ unk,
                                                        const MethodConsts c) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    MGRID_LOOP(k, n) {
-        const Nb q = nbrs(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nb& q) {
         const double2 z = cscale(c.h, f_at(c, u0, V, k, q));
         unk[k] = z;
         unk[n + k] = z;
-    }
+        });
 }
 
 // final assembly: GAUSS2 u0 + h f(u); GAUSS4 u0 + h (b0 f(u_1) + b1 f(u_2));
@@ -234,8 +249,7 @@ __global__ void __launch_bounds__(kT) final_kernel(int method, int nx, int ny, c
                                                    const double* __restrict__ V, const double2* __restrict__ unk,
                                                    double2* __restrict__ out, const MethodConsts c) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    MGRID_LOOP(k, n) {
-        const Nb q = nbrs(k, nx, ny);
+    for_sites(nx, ny, [&](size_t k, const Nb& q) {
         const double2 z = u0[k];
         if (method == kMethodGauss2) {
             out[k] = cadd(z, cscale(c.h, f_at(c, unk, V, k, q)));
@@ -247,8 +261,10 @@ __global__ void __launch_bounds__(kT) final_kernel(int method, int nx, int ny, c
         } else {
             out[k] = unk[k];
         }
-    }
+        });
 }
+
+int rblocks(int ny) { return ny < 148 * 8 ? ny : 148 * 8; }
 
 int mblocks(size_t n) {
     const size_t b = (n + kT - 1) / kT;
@@ -260,21 +276,21 @@ int mblocks(size_t n) {
 cudaError_t launch_rk4_stage(int stage, int nx, int ny, const double2* x, const double2* u0, const double* V,
                              double2* acc, double2* out, const MethodConsts& c, cudaStream_t s) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    rk4_stage_kernel<<<mblocks(n), kT, 0, s>>>(stage, nx, ny, x, u0, V, acc, out, c);
+    rk4_stage_kernel<<<rblocks(ny), kT, 0, s>>>(stage, nx, ny, x, u0, V, acc, out, c);
     return cudaGetLastError();
 }
 
 cudaError_t launch_method_residual(int method, int nx, int ny, const double2* u0, const double* V,
                                    const double2* unk, double2* b, const MethodConsts& c, cudaStream_t s) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    residual_kernel<<<mblocks(n), kT, 0, s>>>(method, nx, ny, u0, V, unk, b, c);
+    residual_kernel<<<rblocks(ny), kT, 0, s>>>(method, nx, ny, u0, V, unk, b, c);
     return cudaGetLastError();
 }
 
 cudaError_t launch_method_matvec(int stages, int nx, int ny, const double2* x, double2* y, const double2* u0,
                                  const double* V, const MethodConsts& c, cudaStream_t s) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    newton_matvec_kernel<<<mblocks(n), kT, 0, s>>>(stages, nx, ny, x, y, u0, V, c);
+    newton_matvec_kernel<<<rblocks(ny), kT, 0, s>>>(stages, nx, ny, x, y, u0, V, c);
     return cudaGetLastError();
 }
 
@@ -289,14 +305,14 @@ cudaError_t launch_newton_add(double2* unk, const double2* x, size_t len, unsign
 cudaError_t launch_avf4_init(int nx, int ny, const double2* u0, const double* V, double2* unk,
                              const MethodConsts& c, cudaStream_t s) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    avf4_init_kernel<<<mblocks(n), kT, 0, s>>>(nx, ny, u0, V, unk, c);
+    avf4_init_kernel<<<rblocks(ny), kT, 0, s>>>(nx, ny, u0, V, unk, c);
     return cudaGetLastError();
 }
 
 cudaError_t launch_method_final(int method, int nx, int ny, const double2* u0, const double* V,
                                 const double2* unk, double2* out, const MethodConsts& c, cudaStream_t s) {
     const size_t n = static_cast<size_t>(nx) * ny;
-    final_kernel<<<mblocks(n), kT, 0, s>>>(method, nx, ny, u0, V, unk, out, c);
+    final_kernel<<<rblocks(ny), kT, 0, s>>>(method, nx, ny, u0, V, unk, out, c);
     return cudaGetLastError();
 }
 
