@@ -93,7 +93,14 @@ typedef struct {
                                  cheap closed form, so the recursion is one J-chain);
                                  -1 = default (kernel 0: 6; sub-domain mode / tiled: 2).
                                  Kernel 0 pairs (first, terms): (0,0) (1,1) (2,0..2)
-                                 (3,1) (4,1..2) (6,0..2); tiled: equal or (2, <=2).     */
+                                 (3,1) (4,1..2) (5,1..2) (6,0..2); tiled: equal or (2, <=2). */
+    int first_poly;           /* polynomial p_k(J) ~ (I - h lam_k J)^-1 of that first sweep:
+                                 0 = default (2 when H is convex -- V >= 0 and gamma <= 0 --,
+                                 else 1); 1 = the Neumann (Taylor) series; 2 = the Chebyshev
+                                 interpolant on the Gershgorin segment i[-rho, rho] of the
+                                 spectrum of J (residual 2 (|h lam| rho / 2)^(d+1) instead of
+                                 (|h lam| rho)^(d+1)).  Only the split of work
+                                 between sweeps changes: the converged result does not.    */
 } mb4cu_problem;
 
 typedef struct {
@@ -159,6 +166,15 @@ int mb4cu_observables(mb4cu_ctx* ctx, mb4cu_obs* out);
  * NULL restores the context's own (non-blocking) stream.  For the legacy default
  * stream (torch's default stream reports handle 0) pass cudaStreamLegacy. */
 int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
+
+/* Spectral bound rho >= rho(J(u0)) that places the first sweep's Chebyshev polynomial
+ * (first_poly 2): the Gershgorin bound 4cx + 4cy + max|V| + 3|gamma| max|u0|^2 of this
+ * context's owned sites and resident state, rounded up to a power of 2^(1/16).  The
+ * ranks of a decomposed lattice must agree on one bound: all-reduce (max) their
+ * mb4cu_spectral_bound and pass the result to mb4cu_set_spectral_bound (0 restores
+ * the context's own bound). */
+int mb4cu_spectral_bound(mb4cu_ctx* ctx, double* rho);
+int mb4cu_set_spectral_bound(mb4cu_ctx* ctx, double rho);
 
 /* ---- Sub-domain (multi-GPU) stepping, ghost > 0 ---------------------------------
  * The caller owns the decomposition and the exchange (paper_2003_04345_b200/dist.py

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -34,6 +35,9 @@ struct mb4cu_ctx {
     bool m_auto = false;  // neumann_terms = -1 on the production kernel: m adapts in {1, 2}
     int auto_steps = 0;
     int last_sweeps = 0;  // sweeps of the last converged step (predicts the final sweep)
+    int first_poly = 1;   // first-sweep polynomial (resolved): 1 = Neumann (Taylor), 2 = Chebyshev
+    double vmin = 0;      // min V (host, at create)
+    double rho_override = 0;  // > 0: spectral bound set by the caller (decomposed lattices)
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
     size_t alloc_n = 0;        // elements per array (padded in sub-domain mode)
     mb4cu_scheme scheme{};
@@ -145,6 +149,80 @@ int is_default_scheme(const mb4cu_scheme& s) {
                : 0;
 }
 
+// Gershgorin bound of the spectral radius of J(u0): rho <= 4cx + 4cy + max|V| + 3|gamma| max|u0|^2.
+double spectral_bound(const mb4cu_ctx* ctx) {
+    return 4.0 * ctx->cx + 4.0 * ctx->cy + ctx->vmax + 3.0 * std::fabs(ctx->gamma) * ctx->amax2;
+}
+
+// The bound that places the first sweep's Chebyshev polynomial: the context's own
+// Gershgorin bound rounded up to a power of 2^(1/16) (so that last-bit differences of
+// max|u0|^2 between a lattice and its decomposition pick the same polynomial), or
+// the bound a decomposed lattice agreed on (mb4cu_set_spectral_bound).
+double own_first_rho(const mb4cu_ctx* ctx) {
+    const double rho = spectral_bound(ctx);
+    return rho > 0.0 ? std::exp2(std::ceil(16.0 * std::log2(rho)) / 16.0) : 0.0;
+}
+double first_rho(const mb4cu_ctx* ctx) { return ctx->rho_override > 0.0 ? ctx->rho_override : own_first_rho(ctx); }
+
+// Degree-`deg` polynomial p(x) = sum_n out[n] x^n approximating 1/(1 - beta x) on the
+// spectrum of J.  With H(u0) positive semidefinite (K >= 0, V >= 0, defocusing) J = S H
+// has its spectrum on i[-rho, rho]; p interpolates 1/(1 - beta x) at the deg + 1
+// Chebyshev points of that segment, so the residual polynomial 1 - (1 - beta x) p(x)
+// is the scaled Chebyshev polynomial T_{deg+1}: max residual ~ 2 (|beta| rho / 2)^(deg+1)
+// instead of (|beta| rho)^(deg+1) for the Taylor (Neumann) series.  The iteration's
+// fixed point does not depend on p; only how much the first sweep leaves for the next.
+// In t = y / rho, G(t) = 1/(1 - i a t), a = beta rho: Re G = 1/(1 + a^2 t^2) (even),
+// Im G = a t / (1 + a^2 t^2) (odd); interpolated in long double, then mapped back
+// through y = -i x.
+void cheb_first_poly(double beta, double rho, int deg, double* out) {
+    const int n = deg + 1;
+    long double A[8][8], bre[8], bim[8];
+    const long double a = static_cast<long double>(beta) * rho;
+    for (int j = 0; j < n; ++j) {
+        const long double t = std::cos((2.0L * j + 1.0L) * 3.14159265358979323846264338327950288L / (2.0L * n));
+        long double tp = 1.0L;
+        for (int q = 0; q < n; ++q) {
+            A[j][q] = tp;
+            tp *= t;
+        }
+        const long double den = 1.0L + a * a * t * t;
+        bre[j] = 1.0L / den;
+        bim[j] = a * t / den;
+    }
+    // Gaussian elimination with partial pivoting, two right-hand sides
+    for (int col = 0; col < n; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < n; ++r)
+            if (std::fabs(A[r][col]) > std::fabs(A[piv][col])) piv = r;
+        for (int q = 0; q < n; ++q) std::swap(A[col][q], A[piv][q]);
+        std::swap(bre[col], bre[piv]);
+        std::swap(bim[col], bim[piv]);
+        for (int r = col + 1; r < n; ++r) {
+            const long double f = A[r][col] / A[col][col];
+            for (int q = col; q < n; ++q) A[r][q] -= f * A[col][q];
+            bre[r] -= f * bre[col];
+            bim[r] -= f * bim[col];
+        }
+    }
+    for (int r = n - 1; r >= 0; --r) {
+        for (int q = r + 1; q < n; ++q) {
+            bre[r] -= A[r][q] * bre[q];
+            bim[r] -= A[r][q] * bim[q];
+        }
+        bre[r] /= A[r][r];
+        bim[r] /= A[r][r];
+    }
+    // sum_q e_q t^q with t = y / rho and y = -i x: coefficient of x^q is e_q (-i)^q / rho^q,
+    // real by the parity of G (even q: Re part, odd q: Im part)
+    long double rp = 1.0L;
+    for (int q = 0; q <= mb4cu::kMaxNeumannFirst; ++q) {
+        long double v = 0.0L;
+        if (q < n) v = (q % 2 == 0 ? bre[q] : bim[q]) * (((q / 2) % 2) ? -1.0L : 1.0L) / rp;
+        out[q] = static_cast<double>(v);
+        rp *= rho;
+    }
+}
+
 SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
     SweepConsts c{};
     const mb4cu_scheme& s = ctx->scheme;
@@ -180,10 +258,19 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         c.first_ss[k] = cc * c.first_s[k];
         c.first_cs[k] = cc * c.first_c[k];
     }
+    // per-stage polynomial p_k(x) ~ 1/(1 - h lam_k x) of the first sweep, monomial coefficients
+    double pc[3][mb4cu::kMaxNeumannFirst + 1] = {};
+    const double rho = first_rho(ctx);
+    for (int k = 0; k < 3; ++k) {
+        if (ctx->first_poly == 2 && rho > 0.0)
+            cheb_first_poly(c.hlam[k], rho, ctx->mf, pc[k]);
+        else
+            for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) pc[k][n] = std::pow(c.hlam[k], n);
+    }
     for (int i = 0; i < 3; ++i)
         for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) {
             double acc = 0.0;
-            for (int k = 0; k < 3; ++k) acc += s.T[i][k] * c.first_s[k] * std::pow(c.hlam[k], n);
+            for (int k = 0; k < 3; ++k) acc += s.T[i][k] * c.first_s[k] * pc[k][n];
             c.fco[i][n] = -acc * (c.iso ? std::pow(cc, n + 1) : 1.0);
         }
     return c;
@@ -269,7 +356,8 @@ constexpr double kStiffKappa = 0.5;
 // sweep failure, so the estimate only steers the choice of the fast path.
 int refresh_amax2(mb4cu_ctx* ctx) {
     if (ctx->amax2_valid) return MB4CU_OK;
-    MB4_CUDA(ctx, mb4cu::launch_amax2(ctx->u0, ctx->alloc_n, ctx->d_rmax, ctx->stream));
+    const size_t off = static_cast<size_t>(ctx->ghost) * ctx->pitch + ctx->ghost;  // owned sites only
+    MB4_CUDA(ctx, mb4cu::launch_amax2_2d(ctx->u0 + off, ctx->nx, ctx->ny, ctx->pitch, ctx->d_rmax, ctx->stream));
     ctx->prof.other_launches += 1;
     MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                   ctx->stream));
@@ -282,8 +370,7 @@ int refresh_amax2(mb4cu_ctx* ctx) {
 bool stiff_step(const mb4cu_ctx* ctx, double h) {
     const double lam = std::max({std::fabs(ctx->scheme.lam[0]), std::fabs(ctx->scheme.lam[1]),
                                  std::fabs(ctx->scheme.lam[2])});
-    const double rho = 4.0 * ctx->cx + 4.0 * ctx->cy + ctx->vmax + 3.0 * std::fabs(ctx->gamma) * ctx->amax2;
-    return h * lam * rho > kStiffKappa;
+    return h * lam * spectral_bound(ctx) > kStiffKappa;
 }
 
 // ---- Newton-Krylov stage solver (kernel = 3) --------------------------------
@@ -743,6 +830,17 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->alloc_n = static_cast<size_t>(ctx->pitch) * (p->ny + 2 * p->ghost);
     ctx->scheme = *scheme;
     for (size_t k = 0; k < ctx->n; ++k) ctx->vmax = std::max(ctx->vmax, std::fabs(p->V[k]));
+    ctx->vmin = ctx->n ? p->V[0] : 0.0;
+    for (size_t k = 0; k < ctx->n; ++k) ctx->vmin = std::min(ctx->vmin, p->V[k]);
+    // Chebyshev placement needs the spectrum of J = S H(u0) on the imaginary axis, i.e.
+    // H(u0) positive semidefinite: K >= 0 always, V >= 0 and a defocusing cubic term
+    if (p->first_poly < 0 || p->first_poly > 2) {
+        g_create_error = "mb4cu_create: first_poly must be 0 (default), 1 (Neumann) or 2 (Chebyshev)";
+        delete ctx;
+        return MB4CU_INVALID;
+    }
+    ctx->first_poly = p->first_poly != 0 ? p->first_poly : (ctx->vmin >= 0.0 && ctx->gamma <= 0.0 ? 2 : 1);
+    if (p->kernel != 0) ctx->first_poly = 1;  // the cross-check kernels run the per-stage Neumann recursion
 
     auto bail = [&](cudaError_t e, const char* where) {
         g_create_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -843,6 +941,22 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
 }
 
 const char* mb4cu_last_error(const mb4cu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int mb4cu_spectral_bound(mb4cu_ctx* ctx, double* rho) {
+    if (!ctx || !rho) return fail(ctx, MB4CU_INVALID, "spectral_bound: null argument");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    const int rc = refresh_amax2(ctx);
+    if (rc) return rc;
+    *rho = own_first_rho(ctx);
+    return MB4CU_OK;
+}
+
+int mb4cu_set_spectral_bound(mb4cu_ctx* ctx, double rho) {
+    if (!ctx) return MB4CU_INVALID;
+    if (!(rho >= 0.0) || !std::isfinite(rho)) return fail(ctx, MB4CU_INVALID, "set_spectral_bound: rho must be >= 0");
+    ctx->rho_override = rho;
+    return MB4CU_OK;
+}
 
 int mb4cu_set_stream(mb4cu_ctx* ctx, void* s) {
     if (!ctx) return MB4CU_INVALID;

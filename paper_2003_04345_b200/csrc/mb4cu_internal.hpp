@@ -235,6 +235,7 @@ int obs_blocks(int nx, int ny);
 cudaError_t launch_observables(const ObsArgs& a, double* out5, cudaStream_t s);
 // max |u|^2 over n sites, written as the bits of a double to *out (stiffness estimate)
 cudaError_t launch_amax2(const double2* u, size_t n, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_amax2_2d(const double2* u, int nx, int ny, int pitch, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_apply_kv(int nx, int ny, double cx, double cy, const double2* u, const double* V,
                             double gamma, bool rhs, double2* y, cudaStream_t s);
 cudaError_t launch_eval_phi(int nx, int ny, const double2* u0, const double* V,

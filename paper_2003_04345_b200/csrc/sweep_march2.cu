@@ -41,6 +41,10 @@
 #ifndef MB4_UNROLL3
 #define MB4_UNROLL3 1
 #endif
+// threads (= columns) per CTA of the production kernel: one band per CTA
+#ifndef MB4_NT
+#define MB4_NT 128
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -61,7 +65,7 @@ struct Geom3 {
     static constexpr size_t pub_bytes = sizeof(double2) * 2 * 3 * ZW;  // one level, 2 parities
     static constexpr size_t bytes = zu0_bytes + zv_bytes + zU_bytes + M * pub_bytes;
     // CTAs per SM: M <= 1 fits 3 (<= 168 registers, ~70 KB smem), M = 2 fits 2
-    static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
+    static constexpr int MINB = NT >= 256 ? 1 : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
 // The default scheme's tables (alpha1 = -712.5, nodes 1/3, 2/3, 1) as compile-time
@@ -809,7 +813,7 @@ struct KGeom {
     static constexpr size_t first_bytes = MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
                                                   : Geom3<0, NT>::bytes;
     static constexpr size_t bytes = first_bytes > Geom3<M, NT>::bytes ? first_bytes : Geom3<M, NT>::bytes;
-    static constexpr int MINB = M == 2 ? 2 : MB4_MINB_M1;
+    static constexpr int MINB = NT >= 256 ? 1 : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
 template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
@@ -949,24 +953,24 @@ template <int MF, int M>
 cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
     // compile-time scheme tables for the (common) isotropic default-scheme case
     if (a.ghost > 0) {
-        if (c.iso && c.def) return Launcher3<MF, M, 128, true, true, true>::launch(a, c, device, s);
-        return c.iso ? Launcher3<MF, M, 128, true, true, false>::launch(a, c, device, s)
-                     : Launcher3<MF, M, 128, false, true, false>::launch(a, c, device, s);
+        if (c.iso && c.def) return Launcher3<MF, M, MB4_NT, true, true, true>::launch(a, c, device, s);
+        return c.iso ? Launcher3<MF, M, MB4_NT, true, true, false>::launch(a, c, device, s)
+                     : Launcher3<MF, M, MB4_NT, false, true, false>::launch(a, c, device, s);
     }
-    if (c.iso && c.def) return Launcher3<MF, M, 128, true, false, true>::launch(a, c, device, s);
-    return c.iso ? Launcher3<MF, M, 128, true, false, false>::launch(a, c, device, s)
-                 : Launcher3<MF, M, 128, false, false, false>::launch(a, c, device, s);
+    if (c.iso && c.def) return Launcher3<MF, M, MB4_NT, true, false, true>::launch(a, c, device, s);
+    return c.iso ? Launcher3<MF, M, MB4_NT, true, false, false>::launch(a, c, device, s)
+                 : Launcher3<MF, M, MB4_NT, false, false, false>::launch(a, c, device, s);
 }
 
 template <int MF, int M>
 int grid3(int device) {
     int g = 0;
-    const int v[6] = {Launcher3<MF, M, 128, true, false, false>::grid_size(device),
-                      Launcher3<MF, M, 128, false, false, false>::grid_size(device),
-                      Launcher3<MF, M, 128, true, true, false>::grid_size(device),
-                      Launcher3<MF, M, 128, false, true, false>::grid_size(device),
-                      Launcher3<MF, M, 128, true, false, true>::grid_size(device),
-                      Launcher3<MF, M, 128, true, true, true>::grid_size(device)};
+    const int v[6] = {Launcher3<MF, M, MB4_NT, true, false, false>::grid_size(device),
+                      Launcher3<MF, M, MB4_NT, false, false, false>::grid_size(device),
+                      Launcher3<MF, M, MB4_NT, true, true, false>::grid_size(device),
+                      Launcher3<MF, M, MB4_NT, false, true, false>::grid_size(device),
+                      Launcher3<MF, M, MB4_NT, true, false, true>::grid_size(device),
+                      Launcher3<MF, M, MB4_NT, true, true, true>::grid_size(device)};
     for (int x : v) g = x > g ? x : g;
     return g;
 }
@@ -974,7 +978,7 @@ int grid3(int device) {
 }  // namespace
 
 // (first-sweep depth, later-sweep depth) pairs with a compiled kernel
-#define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(6, 1) X(4, 2) X(6, 2) X(6, 0)
+#define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(4, 2) X(5, 2) X(6, 2) X(6, 0)
 
 bool march2_supported(int mf, int m) {
 #define MB4_PAIR_EQ(F, N) if (mf == F && m == N) return true;

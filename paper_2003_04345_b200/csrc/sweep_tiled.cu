@@ -307,11 +307,14 @@ int grid_for(size_t n, int threads) {
 }
 
 // max |u|^2 over n sites as the bit pattern of a non-negative double (atomicMax)
-__global__ void amax2_kernel(const double2* __restrict__ u, size_t n, unsigned long long* out) {
+// max |u|^2 over the nx x ny owned sites of a (possibly ghost-padded) array
+__global__ void amax2_kernel(const double2* __restrict__ u, int nx, size_t n, int pitch,
+                             unsigned long long* out) {
     double m = 0.0;
     for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const double2 z = __ldcs(u + k);
+        const size_t row = k / static_cast<size_t>(nx), col = k - row * nx;
+        const double2 z = __ldcs(u + row * pitch + col);
         m = fmax(m, fma(z.x, z.x, z.y * z.y));
     }
     block_max_to(static_cast<unsigned long long>(__double_as_longlong(m)), out);
@@ -348,10 +351,16 @@ cudaError_t launch_sweep_tiled(int m, bool first, const SweepArgs& a, const Swee
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_amax2_2d(const double2* u, int nx, int ny, int pitch, unsigned long long* out, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(nx) * ny;
+    amax2_kernel<<<grid_for(n, 256), 256, 0, s>>>(u, nx, n, pitch, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_amax2(const double2* u, size_t n, unsigned long long* out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(*out), s);
     if (e != cudaSuccess) return e;
-    amax2_kernel<<<grid_for(n, 256), 256, 0, s>>>(u, n, out);
+    amax2_kernel<<<grid_for(n, 256), 256, 0, s>>>(u, static_cast<int>(n), n, static_cast<int>(n), out);
     return cudaGetLastError();
 }
 

@@ -354,8 +354,18 @@ class DistributedSession:
                 launched = s + 1
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
+    def sync_spectral_bound(self) -> None:
+        """After a state was set: all ranks place the first sweep's Chebyshev polynomial
+        on one interval, the max of the ranks' bounds (mb4cu_spectral_bound), which
+        equals the bound of the whole lattice (the bounds are rounded up to powers of
+        2^(1/16)), so a decomposed run matches the single-domain one."""
+        if getattr(self.b, "bound_dirty", False):
+            self.b.set_spectral_bound(self.comm.allreduce_max(self.b.spectral_bound()))
+            self.b.bound_dirty = False
+
     def step(self, h: float) -> Tuple[int, int]:
         """One MB4 step with the reference halving policy; returns (sweeps, halvings)."""
+        self.sync_spectral_bound()
         self.entry_sums = None
         if getattr(self.b, "overlap", False):
             self.b.wait_exchange()
@@ -412,6 +422,7 @@ class CudaBackend:
         p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, 0
         p.neumann_terms = neumann_terms
         p.neumann_first = neumann_first
+        p.first_poly = 0
         p.device = device
         p.kernel = 0
         p.ghost = max(neumann_terms, neumann_first) + 1
@@ -426,6 +437,7 @@ class CudaBackend:
         self.L.mb4cu_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream or 1))
         self.n = dec.lnx * dec.lny
         self._saved = None
+        self.bound_dirty = False
         self._red = None
         self._scratch = None
         self.u0_halo_ok = False
@@ -546,6 +558,15 @@ class CudaBackend:
             self.wait_exchange()
         u = np.ascontiguousarray(u_block, dtype=np.complex128)
         self._chk(self.L.mb4cu_set_state(self.ctx, _lib.dptr(u)))
+        self.bound_dirty = True
+
+    def spectral_bound(self) -> float:
+        rho = C.c_double(0.0)
+        self._chk(self.L.mb4cu_spectral_bound(self.ctx, C.byref(rho)))
+        return rho.value
+
+    def set_spectral_bound(self, rho: float) -> None:
+        self._chk(self.L.mb4cu_set_spectral_bound(self.ctx, rho))
 
     def get_state(self):
         out = np.empty(self.n, dtype=np.complex128)
@@ -556,7 +577,9 @@ class CudaBackend:
         self._saved = self.get_state()
 
     def restore(self):
+        dirty = getattr(self, "bound_dirty", False)  # an internal restore keeps the step's bound
         self.set_state(self._saved)
+        self.bound_dirty = dirty
 
     def profile(self, on=True):
         self.L.mb4cu_profile_enable(self.ctx, int(on))

@@ -291,7 +291,7 @@ class Session:
     def __init__(self, model: GridModel, scheme: Optional[Mb4Scheme] = None,
                  cfg: Optional[NewtonConfig] = None, neumann_terms: Optional[int] = None,
                  device: int = 0, kernel: int = 0, neumann_first: Optional[int] = None,
-                 method: str = MB4):
+                 method: str = MB4, first_poly: int = 0):
         self._L = _lib.lib()
         if method not in METHODS:
             raise ValueError(f"StepDriver: unknown method {method!r}")
@@ -312,6 +312,7 @@ class Session:
         p.max_step_halvings = self.cfg.max_step_halvings
         p.neumann_terms = -1 if neumann_terms is None else int(neumann_terms)
         p.neumann_first = -1 if neumann_first is None else int(neumann_first)
+        p.first_poly = int(first_poly)  # 0: Chebyshev first sweep when H is convex (mb4cu.h)
         p.ghost = 0
         p.device = device
         p.kernel = kernel

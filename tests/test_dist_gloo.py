@@ -34,6 +34,17 @@ class NumpyBackend:
         self.U = [[z(), z(), z()], [z(), z(), z()]]
         self._in(self.V)[:] = V_block.reshape(dec.lny, dec.lnx)
         self._saved = None
+        # first sweep's polynomial as the library resolves first_poly = 0; the bound is
+        # the one the session all-reduces after set_state (dist.DistributedSession)
+        self.first_poly = SM.first_poly_default(V_block, gamma)
+        self.rho = 0.0
+        self.bound_dirty = False
+
+    def spectral_bound(self):
+        return SM.spectral_bound(self._in(self.u0), self._in(self.V), self.gamma, self.cx, self.cy)
+
+    def set_spectral_bound(self, rho):
+        self.rho = rho
 
     def _in(self, a):
         g = self.g
@@ -87,8 +98,13 @@ class NumpyBackend:
         PY, PX = self.P
         flat = lambda a: a.reshape(-1)  # noqa: E731
         U_in = None if s == 0 else [flat(u) for u in self.U[(s - 1) & 1]]
+        coeffs = None
+        if s == 0 and self.first_poly == 2 and self.mf >= 1:
+            assert self.rho > 0.0, "the session sets the spectral bound before the first sweep"
+            lam = self.scheme.eigenvalues()
+            coeffs = [SM.cheb_coeffs(h * lam[k], self.rho, self.mf) for k in range(3)]
         Un, _ = SM.sweep(flat(self.u0), U_in, flat(self.V), self.gamma, h, self.scheme,
-                         self.mf if s == 0 else self.m, PX, PY, self.cx, self.cy)
+                         self.mf if s == 0 else self.m, PX, PY, self.cx, self.cy, coeffs)
         src = [self.u0] * 3 if s == 0 else self.U[(s - 1) & 1]
         out = self.U[s & 1]
         r = 0.0
@@ -114,6 +130,7 @@ class NumpyBackend:
 
     def set_state(self, u_block):
         self._in(self.u0)[:] = u_block.reshape(self.dec.lny, self.dec.lnx)
+        self.bound_dirty = True
 
     def get_state(self):
         return self._in(self.u0).reshape(-1).copy()
@@ -122,7 +139,9 @@ class NumpyBackend:
         self._saved = self.get_state()
 
     def restore(self):
+        dirty = self.bound_dirty  # an internal restore keeps the step's bound
         self.set_state(self._saved)
+        self.bound_dirty = dirty
 
 
 class NumpyAsyncBackend(NumpyBackend):
@@ -190,8 +209,9 @@ def _reference(m, nsteps):
     V, psi = configs.make_inputs(cfg)
     scheme = nls2d.Mb4Scheme()
     u, its = psi, []
+    rho = SM.spectral_bound(psi, V, cfg.gamma)
     for _ in range(nsteps):
-        u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=2)
+        u, it = SM.step(u, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=2, rho=rho)
         its.append(it)
     return u, its
 
@@ -225,8 +245,9 @@ def test_device_reduction_path_lookahead_and_speculation(tmp_path, px, py):
     V, psi = configs.make_inputs(cfg)
     scheme = nls2d.Mb4Scheme()
     u, its = psi, []
+    rho = SM.spectral_bound(psi, V, cfg.gamma)
     for h in hs:
-        u, it = SM.step(u, V, cfg.gamma, h, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+        u, it = SM.step(u, V, cfg.gamma, h, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6, rho=rho)
         its.append(it)
     glob = np.zeros((cfg.ny, cfg.nx), dtype=np.complex128)
     for r in range(world):

@@ -93,7 +93,8 @@ def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
     scheme = nls2d.Mb4Scheme()
     # default first-sweep depth: 6 on the production kernel, 2 on the tiled one, m on v1
     mf = m if (kernel == 2 or m > 2) else (6 if kernel == 0 else 2)
-    ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=mf)
+    ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=mf,
+                       first_poly=0 if kernel == 0 else 1)
     with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=m, kernel=kernel) as s:
         s.set_state(psi)
         st = nls2d.StepStats()
@@ -174,9 +175,10 @@ def _packet_lattice(nx, ny, lx, ly, seed=3):
     return g, V, psi
 
 
-@pytest.mark.parametrize("mf,m", [(2, 1), (3, 1), (4, 1), (6, 1), (4, 2), (6, 2)])
+@pytest.mark.parametrize("first_poly", [0, 1, 2])
+@pytest.mark.parametrize("mf,m", [(2, 1), (3, 1), (4, 1), (5, 1), (6, 1), (4, 2), (6, 2)])
 @pytest.mark.parametrize("lattice", ["cfg1", "aniso_ragged"])
-def test_deep_first_sweep_matches_numpy_model(mf, m, lattice):
+def test_deep_first_sweep_matches_numpy_model(mf, m, lattice, first_poly):
     """The specialised first sweep at depth mf (one J-chain instead of three stage
     recursions) gives the same sweep count and state as the numpy model, on an
     isotropic lattice (compiled scheme tables) and on an anisotropic one whose
@@ -194,8 +196,9 @@ def test_deep_first_sweep_matches_numpy_model(mf, m, lattice):
         model = nls2d.GridModel(g, 0.7, V)
         h, eps = 0.01, 1e-13
         newton = nls2d.NewtonConfig(eps, 50, 0)
-    ref, its = SM.step(psi, V, model.gamma(), h, scheme, m, nx, ny, eps, mf=mf, cx=model.cx, cy=model.cy)
-    with nls2d.Session(model, scheme, newton, neumann_terms=m, neumann_first=mf) as s:
+    ref, its = SM.step(psi, V, model.gamma(), h, scheme, m, nx, ny, eps, mf=mf, cx=model.cx, cy=model.cy,
+                       first_poly=first_poly)
+    with nls2d.Session(model, scheme, newton, neumann_terms=m, neumann_first=mf, first_poly=first_poly) as s:
         s.set_state(psi)
         st = nls2d.StepStats()
         s.step(h, st)
@@ -204,13 +207,15 @@ def test_deep_first_sweep_matches_numpy_model(mf, m, lattice):
     assert rel(got, ref) <= 1e-13
 
 
+@pytest.mark.parametrize("first_poly", [1, 2])
 @pytest.mark.parametrize("mf", [4, 6])
-def test_deep_first_sweep_ten_steps_match_oracle(mf):
+def test_deep_first_sweep_ten_steps_match_oracle(mf, first_poly):
     cfg = configs.CONFIGS["cfg2"]
     V, psi = configs.make_inputs(cfg)
     ref, ref_obs = _oracle_steps(cfg, V, psi, 10)
     model = configs.model_for(cfg, V)
-    with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg), neumann_terms=1, neumann_first=mf) as s:
+    with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg), neumann_terms=1, neumann_first=mf,
+                       first_poly=first_poly) as s:
         s.set_state(psi)
         obs, _ = s.run(cfg.dt, 10)
         got = s.get_state()
@@ -227,9 +232,10 @@ def test_speculative_final_sweep_miss_is_redone_exactly():
     V, psi = configs.make_inputs(cfg)
     model = configs.model_for(cfg, V)
     scheme = nls2d.Mb4Scheme()
-    u1, it1 = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
-    u2, it2 = SM.step(u1, V, cfg.gamma, 2 * cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
-    u3, it3 = SM.step(u2, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6)
+    rho = SM.spectral_bound(psi, V, cfg.gamma)  # the library's bound is that of the set state
+    u1, it1 = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6, rho=rho)
+    u2, it2 = SM.step(u1, V, cfg.gamma, 2 * cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6, rho=rho)
+    u3, it3 = SM.step(u2, V, cfg.gamma, cfg.dt, scheme, 1, cfg.nx, cfg.ny, cfg.epsilon, mf=6, rho=rho)
     assert it2 > it1
     with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=1, neumann_first=6) as s:
         s.set_state(psi)

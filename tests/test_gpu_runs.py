@@ -97,9 +97,9 @@ def test_large_lattice_properties(name, nx):
     assert np.array_equal(obs_a, obs_b)
     H = obs_a[:, 3]
     assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
-    # the production kernel at the tiled kernel's schedule (first sweep depth 2, m = 1)
-    # takes the same sweeps and agrees to rounding
-    with session(cfg, V, neumann_terms=1, neumann_first=2) as s:
+    # the production kernel at the tiled kernel's schedule (first sweep depth 2 with the
+    # Neumann polynomial, m = 1) takes the same sweeps and agrees to rounding
+    with session(cfg, V, neumann_terms=1, neumann_first=2, first_poly=1) as s:
         s.set_state(psi)
         obs_p, it_p = s.run(cfg.dt, 3)
         up = s.get_state()
