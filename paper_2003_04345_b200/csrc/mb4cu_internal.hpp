@@ -144,6 +144,7 @@ struct StepArgs {
     int obs_accumulate;         // add this launch's energy sums to status->obs
     int grid_cap;               // host side: at most this many CTAs (0 = full occupancy), e.g.
                                 // to leave SMs to NCCL kernels running concurrently
+    int obs_blocks;             // blocks that wrote obs_partial (0: this launch's grid)
 };
 
 // ---- the other integrators (methods.cu) ------------------------------------

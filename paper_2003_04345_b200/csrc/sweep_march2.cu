@@ -45,6 +45,16 @@
 #ifndef MB4_NT
 #define MB4_NT 128
 #endif
+// Split step launches for deep first sweeps (mf >= 4): the first sweep in its own
+// launch (its shared-memory rings allow 2 CTAs/SM), the later sweeps in a second,
+// persistent launch at MB4_MINB_LATER CTAs/SM (depth-1 sweeps fit 3: <= 168
+// registers, 70 KB shared memory) -- more warps to hide the FP64 latency.
+#ifndef MB4_SPLIT
+#define MB4_SPLIT 1
+#endif
+#ifndef MB4_MINB_LATER
+#define MB4_MINB_LATER 3
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -807,17 +817,25 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
 // MF: Neumann depth of the first sweep of a step (whose level 0 is the cheap closed
 // form, so a deeper first sweep costs little and saves one later sweep: measured
 // 5 -> 4 sweeps/step at cfg5 for (MF, M) = (2, 1)); M: depth of the other sweeps.
-template <int MF, int M, int NT>
+// PH: 0 = all sweeps of the (sub)step in one launch; 1 = the first sweep only;
+// 2 = the later sweeps, continuing from a PH = 1 launch (its residual in rmax[0]).
+template <int MF, int M, int NT, int PH = 0>
 struct KGeom {
     // the first sweep runs MarchFirst (MF >= 1) or March3<0>; later sweeps March3<M>
     static constexpr size_t first_bytes = MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
                                                   : Geom3<0, NT>::bytes;
-    static constexpr size_t bytes = first_bytes > Geom3<M, NT>::bytes ? first_bytes : Geom3<M, NT>::bytes;
-    static constexpr int MINB = NT >= 256 ? 1 : (M == 2 ? 2 : MB4_MINB_M1);
+    static constexpr size_t later_bytes = Geom3<M, NT>::bytes;
+    static constexpr size_t bytes = PH == 1   ? first_bytes
+                                    : PH == 2 ? later_bytes
+                                              : (first_bytes > later_bytes ? first_bytes : later_bytes);
+    static constexpr int MINB = NT >= 256 ? 1
+                                : PH == 1 ? 2
+                                : PH == 2 ? (M <= 1 ? MB4_MINB_LATER : 2)
+                                          : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
-template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
-__global__ void __launch_bounds__(NT, (KGeom<MF, M, NT>::MINB))
+template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH>
+__global__ void __launch_bounds__(NT, (KGeom<MF, M, NT, PH>::MINB))
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
@@ -840,20 +858,36 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 #endif
 #ifdef MB4_POISON_SMEM
     // debug builds: stale shared memory must never reach an output
-    for (size_t q = threadIdx.x; q < KGeom<MF, M, NT>::bytes / 8; q += NT)
+    for (size_t q = threadIdx.x; q < KGeom<MF, M, NT, PH>::bytes / 8; q += NT)
         reinterpret_cast<unsigned long long*>(smem)[q] = MB4_POISON_SMEM;
     __syncthreads();
 #endif
     int sweeps = 0, set = 0, converged = 0, redone = 0;
     bool redo = false;  // this pass repeats the missed speculative sweep with all stages
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
     double rlast = 0.0;
-    for (int s = 0; s < a.max_iters; ++s) {
+    int s_begin = 0;
+    if (PH != 2) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
+    } else {
+        // continue the first-sweep launch of this (sub)step: sweep 0 left its residual
+        // in rmax[0]; the same tests as after sweep 0 of the single launch
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[1] = global_timer_ns();
+        rlast = __longlong_as_double(static_cast<long long>(__ldcg(&a.rmax[0])));
+        sweeps = 1;
+        s_begin = 1;
+        if (!isfinite(rlast)) {
+            s_begin = a.max_iters;
+        } else if (stage_converged(rlast, 0.0, 0, a.eps)) {
+            converged = 1;
+            s_begin = a.max_iters;
+        }
+    }
+    for (int s = s_begin; s < a.max_iters; ++s) {
         const int sg = s + a.sweep0;  // global sweep index within the (sub)step
         const int out = sg & 1;
         double2* const uout[3] = {a.U[out][0], a.U[out][1], a.U[out][2]};
         unsigned rmax = 0u;
-        if (sg == 0) {
+        if (PH == 1 || (PH == 0 && sg == 0)) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
             sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
@@ -872,7 +906,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
                     a.obs_partial[blockIdx.x * kObsFields + threadIdx.x] = v;
                 }
             }
-        } else {
+        } else if constexpr (PH != 1) {
             // Speculative final sweep (sg == spec_sweep, predicted by the host from the
             // previous step): only U3 -- the step result -- is stored, saving 32 of the
             // 120 B/site.  If it does not converge, it is redone below with all stages
@@ -881,6 +915,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
             sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc,
                                                        sg == a.spec_sweep && !redo ? 4 : 7);
+        }
+        if constexpr (PH == 1) {  // the later-sweep launch takes it from here
+            block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[0]);
+            return;
         }
         if (redo) {  // same residual as the speculative pass: no new test
             redo = false;
@@ -916,22 +954,24 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
         double v = 0.0;
-        for (int b = 0; b < static_cast<int>(gridDim.x); ++b) v += a.obs_partial[b * kObsFields + threadIdx.x];
+        const int nb = a.obs_blocks > 0 ? a.obs_blocks : static_cast<int>(gridDim.x);
+        for (int b = 0; b < nb; ++b) v += a.obs_partial[b * kObsFields + threadIdx.x];
         a.status->obs[threadIdx.x] = (a.obs_accumulate ? a.status->obs[threadIdx.x] : 0.0) + v;
     }
 }
 
-template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF>
+template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH = 0>
 struct Launcher3 {
     static int grid_size(int device) {
         static std::atomic<int> cached[64];  // per device (0 = not yet computed)
         if (device >= 0 && device < 64 && cached[device].load(std::memory_order_acquire))
             return cached[device].load(std::memory_order_acquire);
-        const size_t smem = KGeom<MF, M, NT>::bytes;
-        cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        const size_t smem = KGeom<MF, M, NT, PH>::bytes;
+        cudaFuncSetAttribute(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF, PH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF, PH>, NT,
+                                                      smem);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int g = per_sm * sms;
@@ -944,13 +984,30 @@ struct Launcher3 {
         if (a.grid_cap > 0 && a.grid_cap < grid) grid = a.grid_cap;
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF>),
-                                           dim3(grid), dim3(NT), params, KGeom<MF, M, NT>::bytes, s);
+        return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF, PH>),
+                                           dim3(grid), dim3(NT), params, KGeom<MF, M, NT, PH>::bytes, s);
     }
 };
 
+// the split pair: first sweep (PH 1), then the later sweeps (PH 2) on the same stream
+template <int MF, int M, int NT, bool ISO, bool DEF>
+cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
+    a.obs_blocks = Launcher3<MF, M, NT, ISO, false, DEF, 1>::grid_size(device);
+    if (a.grid_cap > 0 && a.grid_cap < a.obs_blocks) a.obs_blocks = a.grid_cap;
+    const cudaError_t e = Launcher3<MF, M, NT, ISO, false, DEF, 1>::launch(a, c, device, s);
+    if (e != cudaSuccess) return e;
+    return Launcher3<MF, M, NT, ISO, false, DEF, 2>::launch(a, c, device, s);
+}
+
 template <int MF, int M>
 cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
+    if constexpr (MB4_SPLIT && MF >= 4) {
+        if (a.ghost == 0 && a.sweep0 == 0 && a.max_iters > 1) {
+            if (c.iso && c.def) return launch_split<MF, M, MB4_NT, true, true>(a, c, device, s);
+            return c.iso ? launch_split<MF, M, MB4_NT, true, false>(a, c, device, s)
+                         : launch_split<MF, M, MB4_NT, false, false>(a, c, device, s);
+        }
+    }
     // compile-time scheme tables for the (common) isotropic default-scheme case
     if (a.ghost > 0) {
         if (c.iso && c.def) return Launcher3<MF, M, MB4_NT, true, true, true>::launch(a, c, device, s);
@@ -972,6 +1029,15 @@ int grid3(int device) {
                       Launcher3<MF, M, MB4_NT, true, false, true>::grid_size(device),
                       Launcher3<MF, M, MB4_NT, true, true, true>::grid_size(device)};
     for (int x : v) g = x > g ? x : g;
+    if constexpr (MB4_SPLIT && MF >= 4) {
+        const int w[6] = {Launcher3<MF, M, MB4_NT, true, false, false, 1>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT, false, false, false, 1>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT, true, false, true, 1>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT, true, false, false, 2>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT, false, false, false, 2>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT, true, false, true, 2>::grid_size(device)};
+        for (int x : w) g = x > g ? x : g;
+    }
     return g;
 }
 
