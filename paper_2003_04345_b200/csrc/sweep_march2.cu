@@ -52,6 +52,10 @@
 #ifndef MB4_SPLIT
 #define MB4_SPLIT 1
 #endif
+// first sweeps of depth 3..7: MarchFirst2 (power-of-two rings) instead of MarchFirst
+#ifndef MB4_FIRST_V2
+#define MB4_FIRST_V2 1
+#endif
 #ifndef MB4_MINB_LATER
 #define MB4_MINB_LATER 3
 #endif
@@ -762,6 +766,234 @@ struct MarchFirst {
     }
 };
 
+// First sweep, v2: the MarchFirst algorithm (same per-site arithmetic, bit for bit)
+// with its shared-memory rings laid out for cheap addressing.  v1 spends ~40 % of its
+// instructions on ring-slot and row arithmetic (profiles/): here every ring row is
+// NT double2 = 2 KiB (no halo columns: a band is 2 (MF + 1) columns wider than its
+// output instead of 2 MF + 2 -- lanes 0 and NT-1 read a neighbour's stale column,
+// which only reaches lanes the output masks), every ring depth is a power of two,
+// and one slot offset per ring depth and iteration serves all levels through
+// immediate offsets.  Depth of the history of g_n: 2 for the levels the output reads
+// from registers, else the next power of two >= MF - n + 1 (the output reads g_n
+// written MF - n iterations earlier).
+template <int MF, int NT, bool ISO, bool GHOST>
+struct MarchFirst2 {
+    static_assert(MF >= 3 && MF <= 7, "first-sweep v2 depth");
+    static constexpr int TX = NT - 2 * (MF + 1);  // output columns per band
+    static constexpr int RB = NT * 16;            // bytes of a double2 ring row
+    static_assert((RB & (RB - 1)) == 0, "power-of-two ring rows");
+    static constexpr int SZ = 16;                 // z ring rows
+    static constexpr int BACK = MF + 1;           // level MF reads z row j - (MF + 1)
+    static constexpr int P = SZ - 1 - BACK;       // rows in flight
+    static constexpr int PAD = 16;                // lanes 0 / NT-1 read 16 B beyond a row
+    static constexpr int ZU = PAD;                // u0 ring: SZ rows of RB bytes
+    static constexpr int ZV = ZU + SZ * RB;       // V ring: SZ rows of RB / 2 bytes
+    static constexpr int H0 = ZV + SZ * RB / 2;   // g_n history rings
+    __host__ __device__ static constexpr int pow2ceil(int x) { return x <= 1 ? 1 : 2 * pow2ceil((x + 1) / 2); }
+    __host__ __device__ static constexpr int depth(int n) { return n >= MF - 2 ? 2 : pow2ceil(MF - n + 1); }
+    __host__ __device__ static constexpr int hrow(int n) { return n == 0 ? 0 : hrow(n - 1) + depth(n - 1); }
+    static constexpr size_t bytes = static_cast<size_t>(H0) + static_cast<size_t>(hrow(MF)) * RB + PAD;
+
+    unsigned char* sm;  // dynamic shared memory
+    double2 zw[3];      // own-column u0 of z rows j, j-1, j-2
+    double vw[3];
+    double2 gp[MF][2];  // own-column g_n of the last two iterations (slot = parity)
+
+    __device__ MarchFirst2(unsigned char* smem) : sm(smem) {}
+
+    __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
+        if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
+        return static_cast<size_t>(y) * a.nx + x;
+    }
+    template <class T>
+    __device__ __forceinline__ static T& ref(unsigned char* p) { return *reinterpret_cast<T*>(p); }
+
+    struct Seg {
+        int X0, Y0, R, nzrows, gx, next_row;
+        int xlim;
+        size_t next_off;
+    };
+
+    __device__ __forceinline__ void issue_row(const StepArgs& a, Seg& s, int k) {
+        if (k < s.nzrows) {
+            const size_t rowoff = s.next_off;
+            if (GHOST) {
+                s.next_off += a.pitch;
+            } else if (++s.next_row == a.ny) {
+                s.next_row = 0;
+                s.next_off = 0;
+            } else {
+                s.next_off += a.nx;
+            }
+            const int slot = k & (SZ - 1);
+            const size_t g = rowoff + s.gx;
+            cp_async16(sm + ZU + slot * RB + threadIdx.x * 16, a.u0 + g);
+            cp_async8(sm + ZV + slot * (RB / 2) + threadIdx.x * 8, a.V + g);
+        }
+        cp_async_commit();
+    }
+
+    struct Chain {
+        double2 up, low, mid, u0o;
+    };
+
+    // level N: g_N at row i - N from g_{N-1} rows i-N-1 (register), i-N (ring, previous
+    // iteration), i-N+1 (this iteration, ch.up)
+    template <int N, int PAR>
+    __device__ __forceinline__ void levels(const Coef<ISO>& cf, unsigned char* smt, unsigned char* smv,
+                                           int jrb, int o8, int p8, int o4, int p4, Chain& ch) {
+        if constexpr (N <= MF) {
+            constexpr int n = N - 1;
+            constexpr int D = depth(n);
+            constexpr int HB = H0 + hrow(n) * RB;
+            const int so = D == 2 ? PAR * RB : (D == 8 ? o8 : o4);
+            const int sp = D == 2 ? (PAR ^ 1) * RB : (D == 8 ? p8 : p4);
+            unsigned char* crow = smt + HB + sp;  // g_n, iteration j - 1
+            unsigned char* own = smt + HB + so;   // g_n, iteration j
+            const double2 gc = gp[n][PAR ^ 1];
+            const double2 gd = gp[n][PAR];
+            double2 u0n;
+            double vn;
+            if (N == 1) {
+                u0n = zw[2];
+                vn = vw[2];
+            } else {
+                const int zo = (jrb - (N + 1) * RB) & (SZ * RB - 1);  // z row j - N - 1
+                u0n = ref<double2>(smt + ZU + zo);
+                vn = ref<double>(smv + ZV + (zo >> 1));
+            }
+            const double2 an = cf.kv(cf.dv(vn), gc, ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up);
+            const double2 gn = cf.jt(gc, an, u0n);
+            ref<double2>(own) = ch.up;
+            gp[n][PAR] = ch.up;
+            if (N == MF - 1) ch.low = gd;
+            if (N == MF) {
+                ch.mid = gc;
+                ch.u0o = u0n;
+            }
+            ch.up = gn;
+            levels<N + 1, PAR>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
+        }
+    }
+
+    // own-column g_n(i - MF), n <= MF - 3, written at iteration j - (MF - n)
+    template <int N>
+    __device__ __forceinline__ void gather(unsigned char* smt, int jrb, double2* gout) {
+        if constexpr (N + 3 <= MF) {
+            constexpr int D = depth(N);
+            const int so = (jrb - (MF - N) * RB) & (D * RB - 1);
+            gout[N] = ref<double2>(smt + H0 + hrow(N) * RB + so);
+            gather<N + 1>(smt, jrb, gout);
+        }
+    }
+
+    template <int PAR>  // = j & 1
+    __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3], Seg& s,
+                                         int j, unsigned& rmax, double acc[kObsFields]) {
+        const SweepConsts& c = cf.c;
+        const int t = threadIdx.x, i = j - 2;
+        unsigned char* smt = sm + t * 16;
+        unsigned char* smv = sm + t * 8;
+        cp_async_wait<P - 1>();
+        __syncthreads();
+        issue_row(a, s, j + P);
+
+        const int jrb = j * RB;
+        const int zn = jrb & (SZ * RB - 1);         // z row j
+        const int zc = (jrb - RB) & (SZ * RB - 1);  // z row j - 1
+        const int o8 = jrb & (8 * RB - 1), p8 = (jrb - RB) & (8 * RB - 1);
+        const int o4 = jrb & (4 * RB - 1), p4 = (jrb - RB) & (4 * RB - 1);
+
+        const int yrel = i - 2 * MF;
+        const int xout = s.X0 - MF - 1 + t;
+        const bool lane_ok = t >= MF + 1 && t < NT - MF - 1 && xout < s.xlim;
+        const bool out_ok = lane_ok && yrel >= 0 && yrel < s.R;
+
+        zw[0] = ref<double2>(smt + ZU + zn);
+        vw[0] = ref<double>(smv + ZV + (zn >> 1));
+
+        // ---- level 0 at row i: f(u0) and the energy monitor --------------------
+        const double v = vw[1];
+        const double2 u0c = zw[1];
+        const double2 w0 = cf.kv(cf.dv(v), u0c, ref<double2>(smt + ZU + zc - 16), ref<double2>(smt + ZU + zc + 16),
+                                 zw[2], zw[0]);
+        const double n2 = fma(u0c.x, u0c.x, u0c.y * u0c.y);
+        const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
+        const double gy = fma(-cf.g() * n2, u0c.y, w0.y);
+        const double2 f = make_double2(gy, -gx);
+        if (lane_ok && i >= MF && i < MF + s.R) {
+            const double vn = v * n2;
+            const double sc = ISO ? c.cx : 1.0;
+            acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
+            acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
+            acc[2] += n2;
+            acc[3] += n2 * n2;
+            acc[4] += vn;
+        }
+
+        // ---- levels 1..MF --------------------------------------------------------
+        Chain ch{f, f, f, f};
+        levels<1, PAR>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
+
+        if (out_ok) {
+            double2 gout[MF + 1];
+            gather<0>(smt, jrb, gout);
+            gout[MF - 2] = ch.low;
+            gout[MF - 1] = ch.mid;
+            gout[MF] = ch.up;
+            const double2 u0o = ch.u0o;
+            const size_t gi = at(a, xout, s.Y0 + yrel);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                double rx = c.fco[q][MF] * gout[MF].x, ry = c.fco[q][MF] * gout[MF].y;
+#pragma unroll
+                for (int n = MF - 1; n >= 0; --n) {
+                    rx = fma(c.fco[q][n], gout[n].x, rx);
+                    ry = fma(c.fco[q][n], gout[n].y, ry);
+                }
+                uout[q][gi] = make_double2(u0o.x + rx, u0o.y + ry);
+                March3<MF, NT, true, ISO, GHOST>::track(rmax, make_double2(rx, ry));
+            }
+        }
+        zw[2] = zw[1];
+        zw[1] = zw[0];
+        vw[2] = vw[1];
+        vw[1] = vw[0];
+    }
+
+    __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int X0, int xlim,
+                        int Y0, int R, unsigned& rmax, double acc[kObsFields]) {
+        const Coef<ISO> cf{c};
+        Seg s;
+        s.X0 = X0;
+        s.xlim = xlim;
+        s.Y0 = Y0;
+        s.R = R;
+        s.nzrows = R + 2 * MF + 2;
+        const int yz0 = Y0 - MF - 1, xz = X0 - MF - 1 + static_cast<int>(threadIdx.x);
+        if (GHOST) {
+            s.next_off = static_cast<size_t>(yz0 + a.ghost) * a.pitch;
+            const int last = a.pitch - 1, ca = xz + a.ghost;
+            s.gx = ca < last ? ca : last;
+        } else {
+            s.next_row = wrap_index(yz0, a.ny);
+            s.next_off = static_cast<size_t>(s.next_row) * a.nx;
+            s.gx = wrap_index(xz, a.nx);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) issue_row(a, s, k);
+        const int jend = R + 2 * MF + 2;
+        int j = 0;
+        for (; j + 1 < jend; j += 2) {
+            body<0>(a, cf, uout, s, j, rmax, acc);
+            body<1>(a, cf, uout, s, j + 1, rmax, acc);
+        }
+        if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+};
+
 // Split the band-rows of this launch's output rectangles evenly over the grid and
 // march each segment (a run of rows of one band of one rectangle).
 template <int TX, class Run>
@@ -799,7 +1031,13 @@ template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
                            unsigned& rmax, double acc[kObsFields], int smask = 7) {
-    if constexpr (FIRST && M >= 1) {
+    if constexpr (FIRST && M >= 3 && M <= 7 && MB4_FIRST_V2) {
+        using MFirst = MarchFirst2<M, NT, ISO, GHOST>;
+        MFirst mf(smem);
+        for_segments<MFirst::TX>(a, [&](int X0, int xlim, int Y0, int R) {
+            mf.run(a, c, uout, X0, xlim, Y0, R, rmax, acc);
+        });
+    } else if constexpr (FIRST && M >= 1) {
         using MFirst = MarchFirst<M, NT, ISO, GHOST>;
         MFirst mf(smem);
         for_segments<MFirst::TX>(a, [&](int X0, int xlim, int Y0, int R) {
@@ -822,8 +1060,10 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
 template <int MF, int M, int NT, int PH = 0>
 struct KGeom {
     // the first sweep runs MarchFirst (MF >= 1) or March3<0>; later sweeps March3<M>
-    static constexpr size_t first_bytes = MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
-                                                  : Geom3<0, NT>::bytes;
+    static constexpr size_t first_bytes =
+        MF >= 3 && MF <= 7 && MB4_FIRST_V2 ? MarchFirst2<(MF >= 3 && MF <= 7 ? MF : 3), NT, true, false>::bytes
+        : MF >= 1                         ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
+                                          : Geom3<0, NT>::bytes;
     static constexpr size_t later_bytes = Geom3<M, NT>::bytes;
     static constexpr size_t bytes = PH == 1   ? first_bytes
                                     : PH == 2 ? later_bytes
@@ -845,14 +1085,17 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     // instead of the constant bank (LDCU + uniform-register shuffling), which
     // relieves the register pressure of the two-level kernel (measured: +2 %);
     // for M <= 1 the constant bank is faster (measured: +18 %).
-    __shared__ __align__(16) SweepConsts csm;
-    if (M == 2) {
+    // (not in first-sweep launches: their shared-memory rings need every byte)
+    const SweepConsts* cptr = &c;
+    if constexpr (M == 2 && PH != 1) {
+        __shared__ __align__(16) SweepConsts csm;
         const double* src = reinterpret_cast<const double*>(&c);
         double* dst = reinterpret_cast<double*>(&csm);
         for (int q = threadIdx.x; q < static_cast<int>(sizeof(SweepConsts) / sizeof(double)); q += NT) dst[q] = src[q];
         __syncthreads();
+        cptr = &csm;
     }
-    const SweepConsts& cc = M == 2 ? csm : c;
+    const SweepConsts& cc = *cptr;
 #else
     const SweepConsts& cc = c;
 #endif
