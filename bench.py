@@ -390,6 +390,8 @@ def run_ours(args, d: Dist):
             "kernel": "stage sweep",
             "alg_bytes_per_step": step_alg_bytes,
             "kernel_ms_per_launch": kern_ms / launches,
+            "launches_per_step": launches / max(1, args.steps),
+            "kernel_ms_per_step": kern_ms / max(1, args.steps),
             "sweep_ms_by_index": [round(t / n, 4) for t, n in zip(prof.get("sweep_ms", []), prof.get("sweep_n", []))
                                   if n > 0],
             "step_share": kern_ms / max(1e-9, step_ms_total),

@@ -312,7 +312,8 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         float ms = 0.f;
         MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->pev0, ctx->pev1));
         ctx->prof.kernel_ms += ms;
-        ctx->prof.launches += 1;
+        const bool m2 = ctx->kernel == 0 && mb4cu::march2_supported(ctx->mf, ctx->m);
+        ctx->prof.launches += m2 ? mb4cu::march2_launches(ctx->mf, 0, 0, ctx->max_iters) : 1;
         ctx->prof.sweeps += st.sweeps;
         // U3-only final sweep: 88 instead of 120 B/site (a redone guess is overhead, not counted)
         const bool spec_hit = st.converged && st.sweeps - 1 == spec && spec >= 1;

@@ -198,6 +198,8 @@ cudaError_t launch_step_march(int m, int nx, int ny, const double2* u0, const do
                               int want_obs, const SweepConsts& c, int device, cudaStream_t s);
 int march_grid_size(int m, int device);
 bool march2_supported(int mf, int m);
+// kernel launches of one launch_step_march2 call (2: split first / later sweeps)
+int march2_launches(int mf, int ghost, int sweep0, int max_iters);
 cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0, const double* V,
                                double2* const U[2][3], unsigned long long* rmax,
                                double* obs_partial, void* status, int max_iters, double eps,

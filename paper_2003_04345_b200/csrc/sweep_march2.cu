@@ -56,6 +56,9 @@
 #ifndef MB4_FIRST_V2
 #define MB4_FIRST_V2 1
 #endif
+#ifndef MB4_FIRST_REGZ
+#define MB4_FIRST_REGZ 1
+#endif
 #ifndef MB4_MINB_LATER
 #define MB4_MINB_LATER 3
 #endif
@@ -795,8 +798,13 @@ struct MarchFirst2 {
     static constexpr size_t bytes = static_cast<size_t>(H0) + static_cast<size_t>(hrow(MF)) * RB + PAD;
 
     unsigned char* sm;  // dynamic shared memory
-    double2 zw[3];      // own-column u0 of z rows j, j-1, j-2
-    double vw[3];
+    // own-column u0 / V of z rows j, j-1, ..., j-MF-1: level N reads row j-N-1, which
+    // level N-1 read one iteration earlier, so the rows move down a register pipeline
+    // (one shift per iteration) instead of being re-read from the ring per level
+    // (30 shared-memory wavefronts per warp-row at MF = 6; the sweep is L1-bound)
+    static constexpr int NZW = MB4_FIRST_REGZ ? MF + 2 : 3;
+    double2 zw[NZW];
+    double vw[NZW];
     double2 gp[MF][2];  // own-column g_n of the last two iterations (slot = parity)
 
     __device__ MarchFirst2(unsigned char* smem) : sm(smem) {}
@@ -854,9 +862,9 @@ struct MarchFirst2 {
             const double2 gd = gp[n][PAR];
             double2 u0n;
             double vn;
-            if (N == 1) {
-                u0n = zw[2];
-                vn = vw[2];
+            if (N == 1 || MB4_FIRST_REGZ) {
+                u0n = zw[N + 1];
+                vn = vw[N + 1];
             } else {
                 const int zo = (jrb - (N + 1) * RB) & (SZ * RB - 1);  // z row j - N - 1
                 u0n = ref<double2>(smt + ZU + zo);
@@ -955,10 +963,11 @@ struct MarchFirst2 {
                 March3<MF, NT, true, ISO, GHOST>::track(rmax, make_double2(rx, ry));
             }
         }
-        zw[2] = zw[1];
-        zw[1] = zw[0];
-        vw[2] = vw[1];
-        vw[1] = vw[0];
+#pragma unroll
+        for (int k = NZW - 1; k > 0; --k) {
+            zw[k] = zw[k - 1];
+            vw[k] = vw[k - 1];
+        }
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int X0, int xlim,
@@ -1288,6 +1297,10 @@ int grid3(int device) {
 
 // (first-sweep depth, later-sweep depth) pairs with a compiled kernel
 #define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(4, 2) X(5, 2) X(6, 2) X(6, 0)
+
+int march2_launches(int mf, int ghost, int sweep0, int max_iters) {
+    return MB4_SPLIT && mf >= 4 && ghost == 0 && sweep0 == 0 && max_iters > 1 ? 2 : 1;
+}
 
 bool march2_supported(int mf, int m) {
 #define MB4_PAIR_EQ(F, N) if (mf == F && m == N) return true;

@@ -6,5 +6,5 @@ for lib in "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read())
 r=d['roofline']
-print('$lib', '%.3e'%d['value'], d['sweeps_per_step'], 'ms/launch=%.3f'%r['kernel_ms_per_launch'], r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
+print('$lib', '%.3e'%d['value'], d['sweeps_per_step'], 'ms/step=%.3f'%r.get('kernel_ms_per_step', r['kernel_ms_per_launch']), r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
 done

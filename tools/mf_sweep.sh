@@ -7,5 +7,5 @@ for pair in $1; do
 import json,sys
 d=json.loads(sys.stdin.read())
 r=d['roofline']
-print('$CFG mf=$mf m=$m', '%.3e'%d['value'], 'sweeps=%s'%d['sweeps_per_step'], 'drift=%.2e'%d['energy_drift'], 'frac=%.3f'%r['frac'], 'ms/launch=%.3f'%r['kernel_ms_per_launch'], r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
+print('$CFG mf=$mf m=$m', '%.3e'%d['value'], 'sweeps=%s'%d['sweeps_per_step'], 'drift=%.2e'%d['energy_drift'], 'frac=%.3f'%r['frac'], 'ms/step=%.3f'%r.get('kernel_ms_per_step', r['kernel_ms_per_launch']), r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
 done
