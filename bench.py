@@ -184,7 +184,7 @@ def _traffic_entry(cfg_name: str, schedule: str):
 
 
 def measured_traffic(cfg_name: str, schedule: str):
-    """DRAM bytes per step-kernel launch from the committed ncu capture (profiles/traffic.json)."""
+    """DRAM bytes of one step's kernel launches from the committed ncu capture (profiles/traffic.json)."""
     t = _traffic_entry(cfg_name, schedule)
     return None if t is None else float(t["dram_bytes_per_launch"])
 
@@ -380,7 +380,7 @@ def run_ours(args, d: Dist):
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": measured_traffic(cfg.name, schedule_key(args)),
-            "traffic_source": "ncu --set full, dram__bytes_read+write per launch (profiles/traffic.json)",
+            "traffic_source": "ncu --set full, dram__bytes_read+write of one step's launches (profiles/traffic.json)",
             "limiters": measured_limiters(cfg.name, schedule_key(args)),
             # the same metric against the HBM bound of the stage iteration SURVEY.md 8(d)
             # projected (5 sweeps at cfg5: 72 + 4 x 120 = 552 B/site-step): the deep first

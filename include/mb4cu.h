@@ -99,8 +99,11 @@ typedef struct {
                                  else 1); 1 = the Neumann (Taylor) series; 2 = the Chebyshev
                                  interpolant on the Gershgorin segment i[-rho, rho] of the
                                  spectrum of J (residual 2 (|h lam| rho / 2)^(d+1) instead of
-                                 (|h lam| rho)^(d+1)).  Only the split of work
-                                 between sweeps changes: the converged result does not.    */
+                                 (|h lam| rho)^(d+1)).  With 2 the depth-2 later
+                                 sweeps use the Chebyshev interpolant too (4x the contraction
+                                 of the Neumann series, same cost).  Only the split of work
+                                 between sweeps changes: the converged result does not.
+                                 Kernels 1 / 2 always run the Neumann series.             */
 } mb4cu_problem;
 
 typedef struct {

@@ -267,6 +267,14 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         else
             for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) pc[k][n] = std::pow(c.hlam[k], n);
     }
+    // depth-2 later sweeps: the Chebyshev interpolant at the nodes 0, +-(sqrt(3)/2) rho is
+    // 1 + s (b x + b^2 x^2) -- the Neumann Horner form with the second multiplier scaled
+    // by s (residual (|b| rho)^3 / 4 instead of (|b| rho)^3), at no extra cost
+    for (int k = 0; k < 3; ++k) {
+        const double br = c.hlam[k] * rho;
+        c.hlam2[k] = ctx->first_poly == 2 && rho > 0.0 ? c.hlam[k] / (1.0 + 0.75 * br * br) : c.hlam[k];
+        c.hls2[k] = cc * c.hlam2[k];
+    }
     for (int i = 0; i < 3; ++i)
         for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) {
             double acc = 0.0;
@@ -841,7 +849,9 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         return MB4CU_INVALID;
     }
     ctx->first_poly = p->first_poly != 0 ? p->first_poly : (ctx->vmin >= 0.0 && ctx->gamma <= 0.0 ? 2 : 1);
-    if (p->kernel != 0) ctx->first_poly = 1;  // the cross-check kernels run the per-stage Neumann recursion
+    // the cross-check kernels (and the v1 march the production kernel falls back to for
+    // pairs it does not compile) run the per-stage Neumann recursion
+    if (p->kernel != 0 || !mb4cu::march2_supported(ctx->mf, m)) ctx->first_poly = 1;
 
     auto bail = [&](cudaError_t e, const char* where) {
         g_create_error = std::string(where) + ": " + cudaGetErrorString(e);

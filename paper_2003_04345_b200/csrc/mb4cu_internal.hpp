@@ -41,6 +41,11 @@ struct SweepConsts {
     double first_ss[3]; // c * first_s
     double first_cs[3]; // c * first_c
     double hs;          // c * h (isotropic residual with unscaled E, see defscheme)
+    // multiplier of the second Horner level of a depth-2 later sweep: h lam_k for the
+    // Neumann series, s_k h lam_k (s_k = 1 / (1 + 3/4 (h lam_k rho)^2)) for the Chebyshev
+    // interpolant 1 + s_k (b x + b^2 x^2) on i[-rho, rho] (first_poly 2); c * that if ISO
+    double hlam2[3];
+    double hls2[3];
     int def;            // scheme tables equal the generated default ones (defscheme.inc)
     // First sweep at Neumann depth MF from U = (u0,u0,u0): every phibar_k is a
     // multiple of f(u0), so the recursion needs only g_n = J^n f (n <= MF) once,

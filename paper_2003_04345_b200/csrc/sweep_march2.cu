@@ -62,6 +62,10 @@
 #ifndef MB4_MINB_LATER
 #define MB4_MINB_LATER 3
 #endif
+// threads per CTA of the later-sweep launch (the band width; MINB scales with 128 / NT)
+#ifndef MB4_NT_LATER
+#define MB4_NT_LATER 128
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -130,6 +134,7 @@ struct Coef {
     __device__ __forceinline__ double Ti(int k, int i) const { return DEF ? defscheme::Tinv[k][i] : c.Tinv[k][i]; }
     __device__ __forceinline__ double g() const { return ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double hl(int k) const { return ISO ? c.hls[k] : c.hlam[k]; }
+    __device__ __forceinline__ double hl2(int k) const { return ISO ? c.hls2[k] : c.hlam2[k]; }
     __device__ __forceinline__ double fs(int k) const { return ISO ? c.first_ss[k] : c.first_s[k]; }
     __device__ __forceinline__ double fc(int k) const { return ISO ? c.first_cs[k] : c.first_c[k]; }
     // stencil diagonal incl. potential
@@ -148,6 +153,8 @@ struct Coef {
         return y;
     }
     // b = base + h lam_k J t, with a = kv(...) of t and the J diagonal of u0
+    // (LEV 2: the second Horner level of a depth-2 sweep, multiplier hl2)
+    template <int LEV = 1>
     __device__ __forceinline__ double2 horner(int k, double2 base, double2 t, double2 a, double2 u0) const {
         const double pp = u0.x * u0.x, qq = u0.y * u0.y;
         const double al = fma(3.0, pp, qq), be = 2.0 * u0.x * u0.y, de = fma(3.0, qq, pp);
@@ -155,7 +162,8 @@ struct Coef {
         const double nly = fma(be, t.x, de * t.y);
         const double jx = fma(-g(), nly, a.y);
         const double jy = fma(g(), nlx, -a.x);
-        return make_double2(fma(hl(k), jx, base.x), fma(hl(k), jy, base.y));
+        const double m = LEV == 2 ? hl2(k) : hl(k);
+        return make_double2(fma(m, jx, base.x), fma(m, jy, base.y));
     }
     // J t (isotropic: J t / c) from a = kv(...) of t and u0
     __device__ __forceinline__ double2 jt(double2 t, double2 a, double2 u0) const {
@@ -439,7 +447,7 @@ struct March3 {
                 const double2* prow = pub_row(1, ppar, k);  // b1 row i - 2
                 const double2 tc = prow[cc];
                 const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], b1_m3[k], b1[k]);
-                b2[k] = cf.horner(k, pb_m2[k], tc, ak, u0m);
+                b2[k] = cf.template horner<2>(k, pb_m2[k], tc, ak, u0m);
             }
             double2 tb[3];
             cf.from_eigen(b2, tb);  // r = -T b2
@@ -1079,7 +1087,7 @@ struct KGeom {
                                               : (first_bytes > later_bytes ? first_bytes : later_bytes);
     static constexpr int MINB = NT >= 256 ? 1
                                 : PH == 1 ? 2
-                                : PH == 2 ? (M <= 1 ? MB4_MINB_LATER : 2)
+                                : PH == 2 ? (M <= 1 ? MB4_MINB_LATER : 2) * (128 / NT)
                                           : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
@@ -1248,7 +1256,7 @@ cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStrea
     if (a.grid_cap > 0 && a.grid_cap < a.obs_blocks) a.obs_blocks = a.grid_cap;
     const cudaError_t e = Launcher3<MF, M, NT, ISO, false, DEF, 1>::launch(a, c, device, s);
     if (e != cudaSuccess) return e;
-    return Launcher3<MF, M, NT, ISO, false, DEF, 2>::launch(a, c, device, s);
+    return Launcher3<MF, M, MB4_NT_LATER, ISO, false, DEF, 2>::launch(a, c, device, s);
 }
 
 template <int MF, int M>
@@ -1285,9 +1293,9 @@ int grid3(int device) {
         const int w[6] = {Launcher3<MF, M, MB4_NT, true, false, false, 1>::grid_size(device),
                           Launcher3<MF, M, MB4_NT, false, false, false, 1>::grid_size(device),
                           Launcher3<MF, M, MB4_NT, true, false, true, 1>::grid_size(device),
-                          Launcher3<MF, M, MB4_NT, true, false, false, 2>::grid_size(device),
-                          Launcher3<MF, M, MB4_NT, false, false, false, 2>::grid_size(device),
-                          Launcher3<MF, M, MB4_NT, true, false, true, 2>::grid_size(device)};
+                          Launcher3<MF, M, MB4_NT_LATER, true, false, false, 2>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT_LATER, false, false, false, 2>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT_LATER, true, false, true, 2>::grid_size(device)};
         for (int x : w) g = x > g ? x : g;
     }
     return g;

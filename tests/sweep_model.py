@@ -81,7 +81,7 @@ def step(u0, V, gamma, h, scheme, m, nx, ny, eps, max_iters=50, mf=None, cx=1.0,
     """One step; the first sweep uses depth mf (default m), the others m.  first_poly:
     the first sweep's polynomial as in mb4cu_problem (0 = default, 1 = Neumann, 2 =
     Chebyshev on i[-rho, rho], rho default: spectral_bound of u0); it applies to the
-    production kernel's deep first sweep (mf >= 1)."""
+    production kernel's deep first sweep (mf >= 1) and its depth-2 later sweeps."""
     from paper_2003_04345_b200.dist import stage_converged, widen_residual
 
     if first_poly == 0:
@@ -92,11 +92,16 @@ def step(u0, V, gamma, h, scheme, m, nx, ny, eps, max_iters=50, mf=None, cx=1.0,
         rho = spectral_bound(u0, V, gamma, cx, cy) if rho is None else rho
         lam = np.array(scheme.eigenvalues())
         coeffs = [cheb_coeffs(h * lam[k], rho, d1) for k in range(3)]
+    later = None
+    if first_poly == 2 and m == 2:  # depth-2 later sweeps: Chebyshev multipliers (mb4cu_api.cu hlam2)
+        rho = spectral_bound(u0, V, gamma, cx, cy) if rho is None else rho
+        lam = np.array(scheme.eigenvalues())
+        later = [cheb_coeffs(h * lam[k], rho, 2) for k in range(3)]
     U = None
     r_prev = float("nan")
     for it in range(1, max_iters + 1):
         U, r = sweep(u0, U, V, gamma, h, scheme, m if (it > 1 or mf is None) else mf, nx, ny, cx, cy,
-                     coeffs if it == 1 else None)
+                     coeffs if it == 1 else later)
         r = widen_residual(r)
         if stage_converged(r, r_prev, it - 1, eps):
             return U[2], it

@@ -99,10 +99,11 @@ class NumpyBackend:
         flat = lambda a: a.reshape(-1)  # noqa: E731
         U_in = None if s == 0 else [flat(u) for u in self.U[(s - 1) & 1]]
         coeffs = None
-        if s == 0 and self.first_poly == 2 and self.mf >= 1:
+        d = self.mf if s == 0 else self.m
+        if self.first_poly == 2 and ((s == 0 and d >= 1) or d == 2):
             assert self.rho > 0.0, "the session sets the spectral bound before the first sweep"
             lam = self.scheme.eigenvalues()
-            coeffs = [SM.cheb_coeffs(h * lam[k], self.rho, self.mf) for k in range(3)]
+            coeffs = [SM.cheb_coeffs(h * lam[k], self.rho, d) for k in range(3)]
         Un, _ = SM.sweep(flat(self.u0), U_in, flat(self.V), self.gamma, h, self.scheme,
                          self.mf if s == 0 else self.m, PX, PY, self.cx, self.cy, coeffs)
         src = [self.u0] * 3 if s == 0 else self.U[(s - 1) & 1]

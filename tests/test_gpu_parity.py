@@ -94,7 +94,7 @@ def test_first_step_sweep_count_and_state_match_numpy_model(m, kernel):
     # default first-sweep depth: 6 on the production kernel, 2 on the tiled one, m on v1
     mf = m if (kernel == 2 or m > 2) else (6 if kernel == 0 else 2)
     ref, its = SM.step(psi, V, cfg.gamma, cfg.dt, scheme, m, cfg.nx, cfg.ny, cfg.epsilon, mf=mf,
-                       first_poly=0 if kernel == 0 else 1)
+                       first_poly=0 if (kernel == 0 and m <= 2) else 1)
     with nls2d.Session(model, scheme, configs.newton_for(cfg), neumann_terms=m, kernel=kernel) as s:
         s.set_state(psi)
         st = nls2d.StepStats()

@@ -27,7 +27,7 @@ def mix(rep):
     ist = hdr.index("Warp Stall Sampling (All Samples)")
     cnt, stall = collections.Counter(), collections.Counter()
     for r in rows[2:]:
-        if len(r) <= ix:
+        if len(r) <= ix or not r[ix].strip().isdigit():  # multi-kernel reports repeat the header
             continue
         op = r[isrc].strip().split()
         if not op:
