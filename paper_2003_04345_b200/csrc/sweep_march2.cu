@@ -66,6 +66,10 @@
 #ifndef MB4_NT_LATER
 #define MB4_NT_LATER 128
 #endif
+// threads per CTA of the first-sweep launch
+#ifndef MB4_NT_FIRST
+#define MB4_NT_FIRST 128
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -1252,9 +1256,9 @@ struct Launcher3 {
 // the split pair: first sweep (PH 1), then the later sweeps (PH 2) on the same stream
 template <int MF, int M, int NT, bool ISO, bool DEF>
 cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
-    a.obs_blocks = Launcher3<MF, M, NT, ISO, false, DEF, 1>::grid_size(device);
+    a.obs_blocks = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::grid_size(device);
     if (a.grid_cap > 0 && a.grid_cap < a.obs_blocks) a.obs_blocks = a.grid_cap;
-    const cudaError_t e = Launcher3<MF, M, NT, ISO, false, DEF, 1>::launch(a, c, device, s);
+    const cudaError_t e = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::launch(a, c, device, s);
     if (e != cudaSuccess) return e;
     return Launcher3<MF, M, MB4_NT_LATER, ISO, false, DEF, 2>::launch(a, c, device, s);
 }
@@ -1290,9 +1294,9 @@ int grid3(int device) {
                       Launcher3<MF, M, MB4_NT, true, true, true>::grid_size(device)};
     for (int x : v) g = x > g ? x : g;
     if constexpr (MB4_SPLIT && MF >= 4) {
-        const int w[6] = {Launcher3<MF, M, MB4_NT, true, false, false, 1>::grid_size(device),
-                          Launcher3<MF, M, MB4_NT, false, false, false, 1>::grid_size(device),
-                          Launcher3<MF, M, MB4_NT, true, false, true, 1>::grid_size(device),
+        const int w[6] = {Launcher3<MF, M, MB4_NT_FIRST, true, false, false, 1>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT_FIRST, false, false, false, 1>::grid_size(device),
+                          Launcher3<MF, M, MB4_NT_FIRST, true, false, true, 1>::grid_size(device),
                           Launcher3<MF, M, MB4_NT_LATER, true, false, false, 2>::grid_size(device),
                           Launcher3<MF, M, MB4_NT_LATER, false, false, false, 2>::grid_size(device),
                           Launcher3<MF, M, MB4_NT_LATER, true, false, true, 2>::grid_size(device)};
