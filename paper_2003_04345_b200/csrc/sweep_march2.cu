@@ -1132,9 +1132,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     int s_begin = 0;
     if (PH != 2) {
         if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[0] = global_timer_ns();
-    } else {
+    } else if (a.sweep0 == 0) {
         // continue the first-sweep launch of this (sub)step: sweep 0 left its residual
-        // in rmax[0]; the same tests as after sweep 0 of the single launch
+        // in rmax[0]; the same tests as after sweep 0 of the single launch.  (Sub-domain
+        // sweeps launch one sweep at a time: sweep0 > 0, nothing to continue.)
         if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t[1] = global_timer_ns();
         rlast = __longlong_as_double(static_cast<long long>(__ldcg(&a.rmax[0])));
         sweeps = 1;
@@ -1181,8 +1182,11 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
                                                        sg == a.spec_sweep && !redo ? 4 : 7);
         }
         if constexpr (PH == 1) {  // the later-sweep launch takes it from here
-            block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[0]);
-            return;
+            if (a.max_iters > 1) {   // (a one-sweep launch finishes its status below)
+                block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull,
+                             &a.rmax[0]);
+                return;
+            }
         }
         if (redo) {  // same residual as the speculative pass: no new test
             redo = false;
@@ -1272,6 +1276,20 @@ cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaS
                          : launch_split<MF, M, MB4_NT, false, false>(a, c, device, s);
         }
     }
+    if constexpr (MB4_SPLIT && MF >= 4) {
+        // sub-domain sweeps (one sweep per launch): the first / later sweep kernels with
+        // their own register and shared-memory footprints
+        if (a.ghost > 0 && a.max_iters == 1) {
+            if (a.sweep0 == 0) {
+                if (c.iso && c.def) return Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 1>::launch(a, c, device, s);
+                return c.iso ? Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 1>::launch(a, c, device, s)
+                             : Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 1>::launch(a, c, device, s);
+            }
+            if (c.iso && c.def) return Launcher3<MF, M, MB4_NT_LATER, true, true, true, 2>::launch(a, c, device, s);
+            return c.iso ? Launcher3<MF, M, MB4_NT_LATER, true, true, false, 2>::launch(a, c, device, s)
+                         : Launcher3<MF, M, MB4_NT_LATER, false, true, false, 2>::launch(a, c, device, s);
+        }
+    }
     // compile-time scheme tables for the (common) isotropic default-scheme case
     if (a.ghost > 0) {
         if (c.iso && c.def) return Launcher3<MF, M, MB4_NT, true, true, true>::launch(a, c, device, s);
@@ -1301,6 +1319,13 @@ int grid3(int device) {
                           Launcher3<MF, M, MB4_NT_LATER, false, false, false, 2>::grid_size(device),
                           Launcher3<MF, M, MB4_NT_LATER, true, false, true, 2>::grid_size(device)};
         for (int x : w) g = x > g ? x : g;
+        const int wg[6] = {Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 1>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 1>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 1>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_LATER, true, true, false, 2>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_LATER, false, true, false, 2>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_LATER, true, true, true, 2>::grid_size(device)};
+        for (int x : wg) g = x > g ? x : g;
     }
     return g;
 }
