@@ -36,6 +36,7 @@ struct mb4cu_ctx {
     int auto_steps = 0;
     int last_sweeps = 0;  // sweeps of the last converged step (predicts the final sweep)
     int first_poly = 1;   // first-sweep polynomial (resolved): 1 = Neumann (Taylor), 2 = Chebyshev
+    bool kr_batch = true; // Newton-Krylov: the three stage solves in flight together (krb)
     double vmin = 0;      // min V (host, at create)
     double rho_override = 0;  // > 0: spectral bound set by the caller (decomposed lattices)
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
@@ -83,6 +84,25 @@ struct mb4cu_ctx {
         double* h_partial = nullptr;
         double shift = 0.0;                // mean(V) - 2 gamma mean(|u0|^2) of the current u0
     } fft;
+    // The three decoupled stage solves of a Newton-Krylov iteration in flight at once
+    // (the paper's stage parallelism, on one GPU): one stream, Krylov basis, FFT plan and
+    // reduction buffers per stage system; used while 3 (m + 4) vectors fit kKrBatchBytes.
+    struct {
+        size_t len = 0;
+        int m = 0, nblk = 0;
+        double2* mem = nullptr;  // per system: basis (m + 1), w, y, preconditioner scratch
+        double2** v_dev[3] = {nullptr, nullptr, nullptr};
+        double* partial[3] = {nullptr, nullptr, nullptr};
+        double* h_partial[3] = {nullptr, nullptr, nullptr};
+        double* coef[3] = {nullptr, nullptr, nullptr};
+        double* h_coef[3] = {nullptr, nullptr, nullptr};
+        double* hcol[3] = {nullptr, nullptr, nullptr};
+        double* h_hcol[3] = {nullptr, nullptr, nullptr};
+        cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        cufftHandle plan[3] = {0, 0, 0};
+        bool ready = false;
+    } krb;
     bool profiling = false;
     mb4cu_profile prof{};
     std::string err;
@@ -619,6 +639,252 @@ int kr_gmres_fft(mb4cu_ctx* ctx, int stages, double sigma_or_h, const double C[2
     return fft_apply(ctx, stages, sigma_or_h, C, x);
 }
 
+constexpr size_t kKrBatchBytes = size_t(1) << 31;
+
+void krb_free(mb4cu_ctx* ctx) {
+    auto& B = ctx->krb;
+    for (int q = 0; q < 3; ++q) {
+        cudaFree(B.v_dev[q]);
+        cudaFree(B.partial[q]);
+        cudaFreeHost(B.h_partial[q]);
+        cudaFree(B.coef[q]);
+        cudaFreeHost(B.h_coef[q]);
+        cudaFree(B.hcol[q]);
+        cudaFreeHost(B.h_hcol[q]);
+        if (B.st[q]) cudaStreamDestroy(B.st[q]);
+        if (B.plan[q]) cufftDestroy(B.plan[q]);
+        B.v_dev[q] = nullptr;
+        B.partial[q] = B.h_partial[q] = B.coef[q] = B.h_coef[q] = B.hcol[q] = B.h_hcol[q] = nullptr;
+        B.st[q] = nullptr;
+        B.plan[q] = 0;
+    }
+    for (auto& e : B.ev) {
+        if (e) cudaEventDestroy(e);
+        e = nullptr;
+    }
+    cudaFree(B.mem);
+    B.mem = nullptr;
+    B.ready = false;
+    B.len = 0;
+}
+
+// 1 if the batched stage solves are set up for vectors of len entries
+int krb_alloc(mb4cu_ctx* ctx, size_t len) {
+    auto& B = ctx->krb;
+    if (B.ready && B.len == len) return 1;
+    const int m = kKrylovRestart;
+    const size_t per = static_cast<size_t>(m + 4);
+    // concurrent cooperative Arnoldi launches must fit the device together
+    int cap = mb4cu::arnoldi_grid(size_t(1) << 40);
+    if (3 * per * len * sizeof(double2) > kKrBatchBytes || 3 * mb4cu::krylov_blocks(len) > cap) return 0;
+    if (B.mem) {
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return 0;
+        krb_free(ctx);
+    }
+    B.m = m;
+    B.len = len;
+    B.nblk = mb4cu::krylov_blocks(len);
+    bool ok = cudaMalloc(&B.mem, 3 * per * len * sizeof(double2)) == cudaSuccess;
+    for (int q = 0; q < 3 && ok; ++q) {
+        ok = cudaStreamCreateWithFlags(&B.st[q], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaMalloc(&B.v_dev[q], sizeof(double2*) * (m + 1)) == cudaSuccess &&
+             cudaMalloc(&B.partial[q], sizeof(double) * (m + 1) * B.nblk) == cudaSuccess &&
+             cudaMallocHost(&B.h_partial[q], sizeof(double) * (m + 1) * B.nblk) == cudaSuccess &&
+             cudaMalloc(&B.coef[q], sizeof(double) * (m + 1)) == cudaSuccess &&
+             cudaMallocHost(&B.h_coef[q], sizeof(double) * (m + 1)) == cudaSuccess &&
+             cudaMalloc(&B.hcol[q], sizeof(double) * (m + 2)) == cudaSuccess &&
+             cudaMallocHost(&B.h_hcol[q], sizeof(double) * (m + 2)) == cudaSuccess &&
+             cufftPlan2d(&B.plan[q], ctx->ny, ctx->nx, CUFFT_Z2Z) == CUFFT_SUCCESS &&
+             cufftSetStream(B.plan[q], B.st[q]) == CUFFT_SUCCESS;
+        if (ok) {
+            std::vector<double2*> ptrs(m + 1);
+            for (int i = 0; i <= m; ++i) ptrs[i] = B.mem + (q * per + i) * len;
+            ok = cudaMemcpy(B.v_dev[q], ptrs.data(), sizeof(double2*) * (m + 1), cudaMemcpyHostToDevice) ==
+                 cudaSuccess;
+        }
+    }
+    for (auto& e : B.ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        krb_free(ctx);
+        cudaGetLastError();
+        return 0;
+    }
+    B.ready = true;
+    return 1;
+}
+
+// The three stage systems (I - h lam_k J) x_k = b_k of one Newton iteration, solved
+// together: the same right-preconditioned restarted GMRES(m) as kr_gmres_fft per
+// system (identical arithmetic: the same kernels, host Givens updates and stopping
+// tests), advanced in lockstep, system q on its own stream, so one host round trip
+// per Arnoldi step serves all three and their small kernels run concurrently.
+int kr_gmres_stages(mb4cu_ctx* ctx, const SweepConsts& c, const double2* const b[3], double2* const x[3]) {
+    auto& B = ctx->krb;
+    const size_t n = B.len;
+    const int m = B.m;
+    const size_t per = static_cast<size_t>(m + 4);
+    auto V = [&](int q, int i) { return B.mem + (q * per + i) * n; };
+    auto W = [&](int q) { return V(q, m + 1); };
+    auto Y = [&](int q) { return V(q, m + 2); };
+    auto T = [&](int q) { return V(q, m + 3); };
+    auto& f = ctx->fft;
+    // y = A P^-1 v for system q
+    auto mv = [&](int q, const double2* in, double2* out) -> int {
+        MB4_CUDA(ctx, cudaMemcpyAsync(T(q), in, n * sizeof(double2), cudaMemcpyDeviceToDevice, B.st[q]));
+        auto* z = reinterpret_cast<cufftDoubleComplex*>(T(q));
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, mb4cu::launch_fft_scale1(T(q), ctx->nx, ctx->ny, ctx->cx, ctx->cy, f.shift, c.hlam[q], B.st[q]));
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, mb4cu::kr_matvec(T(q), out, ctx->u0, ctx->V, ctx->nx, ctx->ny, c.hlam[q], c, B.st[q]));
+        ctx->prof.other_launches += 3;
+        return MB4CU_OK;
+    };
+    auto fetch_sum = [&](int q, int nv, double* out) {
+        for (int i = 0; i < nv; ++i) {
+            double sum = 0.0;
+            for (int blk = 0; blk < B.nblk; ++blk) sum += B.h_partial[q][static_cast<size_t>(i) * B.nblk + blk];
+            out[i] = sum;
+        }
+    };
+    auto sync_all = [&](const bool* which) -> int {
+        for (int q = 0; q < 3; ++q)
+            if (which[q]) MB4_CUDA(ctx, cudaStreamSynchronize(B.st[q]));
+        return MB4CU_OK;
+    };
+    // the stage streams start after the right-hand sides (context stream)
+    MB4_CUDA(ctx, cudaEventRecord(B.ev[3], ctx->stream));
+    for (int q = 0; q < 3; ++q) MB4_CUDA(ctx, cudaStreamWaitEvent(B.st[q], B.ev[3], 0));
+
+    std::vector<double> H[3], cs[3], sn[3], g[3], yv[3];
+    double bnorm[3] = {0, 0, 0}, beta[3] = {0, 0, 0};
+    bool active[3] = {true, true, true}, first[3] = {true, true, true}, inner[3] = {false, false, false};
+    int j[3] = {0, 0, 0}, iters[3] = {0, 0, 0};
+    for (int q = 0; q < 3; ++q) {
+        H[q].assign(static_cast<size_t>(m + 1) * m, 0.0);
+        cs[q].assign(m, 0.0);
+        sn[q].assign(m, 0.0);
+        g[q].assign(m + 1, 0.0);
+        yv[q].assign(m, 0.0);
+        MB4_CUDA(ctx, cudaMemsetAsync(x[q], 0, n * sizeof(double2), B.st[q]));
+        MB4_CUDA(ctx, cudaMemsetAsync(Y(q), 0, n * sizeof(double2), B.st[q]));
+        MB4_CUDA(ctx, mb4cu::kr_residual(b[q], Y(q), V(q, 0), n, B.partial[q], B.st[q]));
+        MB4_CUDA(ctx, cudaMemcpyAsync(B.h_partial[q], B.partial[q], sizeof(double) * B.nblk, cudaMemcpyDeviceToHost,
+                                      B.st[q]));
+    }
+    if (int rc = sync_all(active)) return rc;
+    for (int q = 0; q < 3; ++q) {
+        double b2 = 0.0;
+        fetch_sum(q, 1, &b2);
+        bnorm[q] = std::sqrt(b2);
+        if (bnorm[q] == 0.0) active[q] = false;
+    }
+    auto Hat = [&](int q, int i, int jj) -> double& { return H[q][static_cast<size_t>(i) * m + jj]; };
+    for (;;) {
+        bool any = false, need[3] = {false, false, false};
+        // restart: residual of the current x (not for the first cycle: r = b is in v_0)
+        for (int q = 0; q < 3; ++q) {
+            if (!active[q]) continue;
+            any = true;
+            if (first[q]) continue;
+            if (iters[q] >= kKrylovMaxIters) {  // best effort after the cap (iterative.cpp:152)
+                active[q] = false;
+                continue;
+            }
+            need[q] = true;
+            if (int rc = mv(q, x[q], Y(q))) return rc;
+            MB4_CUDA(ctx, mb4cu::kr_residual(b[q], Y(q), V(q, 0), n, B.partial[q], B.st[q]));
+            MB4_CUDA(ctx, cudaMemcpyAsync(B.h_partial[q], B.partial[q], sizeof(double) * B.nblk,
+                                          cudaMemcpyDeviceToHost, B.st[q]));
+        }
+        if (!any) break;
+        if (int rc = sync_all(need)) return rc;
+        for (int q = 0; q < 3; ++q) {
+            if (!active[q]) continue;
+            if (first[q]) {
+                beta[q] = bnorm[q];
+                first[q] = false;
+            } else {
+                double r2 = 0.0;
+                fetch_sum(q, 1, &r2);
+                beta[q] = std::sqrt(r2);
+            }
+            if (beta[q] / bnorm[q] <= kKrylovTol) {
+                active[q] = false;
+                continue;
+            }
+            MB4_CUDA(ctx, mb4cu::kr_scale(V(q, 0), V(q, 0), 1.0 / beta[q], n, B.st[q]));
+            std::fill(g[q].begin(), g[q].end(), 0.0);
+            g[q][0] = beta[q];
+            j[q] = 0;
+            inner[q] = true;
+        }
+        // Arnoldi steps of all systems in the inner cycle, one host round trip each
+        for (;;) {
+            bool step[3] = {false, false, false}, anyin = false;
+            for (int q = 0; q < 3; ++q) {
+                if (!inner[q]) continue;
+                anyin = step[q] = true;
+                if (int rc = mv(q, V(q, j[q]), W(q))) return rc;
+                MB4_CUDA(ctx, mb4cu::kr_arnoldi(W(q), B.v_dev[q], j[q], n, B.partial[q], B.coef[q], B.hcol[q],
+                                                B.st[q]));
+                MB4_CUDA(ctx, cudaMemcpyAsync(B.h_hcol[q], B.hcol[q], sizeof(double) * (j[q] + 2),
+                                              cudaMemcpyDeviceToHost, B.st[q]));
+            }
+            if (!anyin) break;
+            if (int rc = sync_all(step)) return rc;
+            for (int q = 0; q < 3; ++q) {
+                if (!step[q]) continue;
+                const int jj = j[q];
+                for (int i = 0; i <= jj; ++i) Hat(q, i, jj) = B.h_hcol[q][i];
+                const double hn = B.h_hcol[q][jj + 1];
+                Hat(q, jj + 1, jj) = hn;
+                for (int i = 0; i < jj; ++i) {
+                    const double t = cs[q][i] * Hat(q, i, jj) + sn[q][i] * Hat(q, i + 1, jj);
+                    Hat(q, i + 1, jj) = -sn[q][i] * Hat(q, i, jj) + cs[q][i] * Hat(q, i + 1, jj);
+                    Hat(q, i, jj) = t;
+                }
+                const double den = std::hypot(Hat(q, jj, jj), Hat(q, jj + 1, jj));
+                if (den == 0.0) return fail(ctx, MB4CU_NONCONVERGED, "gmres: breakdown");
+                cs[q][jj] = Hat(q, jj, jj) / den;
+                sn[q][jj] = Hat(q, jj + 1, jj) / den;
+                Hat(q, jj, jj) = den;
+                Hat(q, jj + 1, jj) = 0.0;
+                g[q][jj + 1] = -sn[q][jj] * g[q][jj];
+                g[q][jj] = cs[q][jj] * g[q][jj];
+                ++iters[q];
+                j[q] = jj + 1;
+                const bool conv = std::fabs(g[q][jj + 1]) / bnorm[q] <= kKrylovTol || hn == 0.0;
+                if (conv || j[q] == m || iters[q] >= kKrylovMaxIters) {
+                    inner[q] = false;
+                    const int nj = j[q];
+                    ctx->kr.gmres_iters += nj;
+                    ctx->prof.krylov_iters += nj;
+                    for (int i = nj - 1; i >= 0; --i) {
+                        double sum = g[q][i];
+                        for (int k2 = i + 1; k2 < nj; ++k2) sum -= Hat(q, i, k2) * yv[q][k2];
+                        yv[q][i] = sum / Hat(q, i, i);
+                    }
+                    for (int i = 0; i < nj; ++i) B.h_coef[q][i] = yv[q][i];
+                    MB4_CUDA(ctx, cudaMemcpyAsync(B.coef[q], B.h_coef[q], sizeof(double) * nj, cudaMemcpyHostToDevice,
+                                                  B.st[q]));
+                    MB4_CUDA(ctx, mb4cu::kr_combine(x[q], B.v_dev[q], B.coef[q], nj, n, B.st[q]));
+                    if (conv) active[q] = false;
+                }
+            }
+        }
+    }
+    // x = P^-1 x' (right preconditioning), then join the context stream
+    for (int q = 0; q < 3; ++q) {
+        auto* z = reinterpret_cast<cufftDoubleComplex*>(x[q]);
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, mb4cu::launch_fft_scale1(x[q], ctx->nx, ctx->ny, ctx->cx, ctx->cy, f.shift, c.hlam[q], B.st[q]));
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, cudaEventRecord(B.ev[q], B.st[q]));
+        MB4_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, B.ev[q], 0));
+    }
+    return MB4CU_OK;
+}
+
 int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
     if (int rc = kr_alloc(ctx, ctx->n)) return rc;
     const SweepConsts c = make_consts(ctx, h);
@@ -632,15 +898,21 @@ int substep_krylov(mb4cu_ctx* ctx, double h, int* iters, double* last_res) {
     double2* x[3] = {kr_vec(ctx, m + 4), kr_vec(ctx, m + 5), kr_vec(ctx, m + 6)};
     *iters = 0;
     if (int rc = fft_prepare(ctx, 1)) return rc;
+    // the three stage solves in flight together while their Krylov storage is small
+    const bool batch = ctx->kr_batch && krb_alloc(ctx, ctx->n) == 1;
     for (int it = 1; it <= ctx->max_iters; ++it) {
         const double2* cst[3] = {st[0], st[1], st[2]};
         MB4_CUDA(ctx, mb4cu::kr_phibar(ctx->nx, ctx->ny, ctx->u0, cst, ctx->V, b, c, ctx->stream));
-        for (int k = 0; k < 3; ++k) {
-            const double hl = c.hlam[k];
-            auto mv = [&](const double2* xin, double2* yout) {
-                return mb4cu::kr_matvec(xin, yout, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream);
-            };
-            if (int rc = kr_gmres_fft(ctx, 1, hl, nullptr, mv, b[k], x[k])) return rc;
+        if (batch) {
+            if (int rc = kr_gmres_stages(ctx, c, b, x)) return rc;
+        } else {
+            for (int k = 0; k < 3; ++k) {
+                const double hl = c.hlam[k];
+                auto mv = [&](const double2* xin, double2* yout) {
+                    return mb4cu::kr_matvec(xin, yout, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream);
+                };
+                if (int rc = kr_gmres_fft(ctx, 1, hl, nullptr, mv, b[k], x[k])) return rc;
+            }
         }
         MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
         const double2* cx[3] = {x[0], x[1], x[2]};
@@ -848,6 +1120,8 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         delete ctx;
         return MB4CU_INVALID;
     }
+    // cross-check knob: MB4CU_KR_BATCH=0 solves the stage systems one after the other
+    if (const char* kb = std::getenv("MB4CU_KR_BATCH")) ctx->kr_batch = std::atoi(kb) != 0;
     ctx->first_poly = p->first_poly != 0 ? p->first_poly : (ctx->vmin >= 0.0 && ctx->gamma <= 0.0 ? 2 : 1);
     // the cross-check kernels (and the v1 march the production kernel falls back to for
     // pairs it does not compile) run the per-stage Neumann recursion
@@ -938,6 +1212,7 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
     kr_free(ctx);
+    krb_free(ctx);
     if (ctx->fft.have1) cufftDestroy(ctx->fft.plan1);
     if (ctx->fft.have2) cufftDestroy(ctx->fft.plan2);
     cudaFree(ctx->fft.partial);

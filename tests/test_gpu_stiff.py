@@ -100,3 +100,23 @@ def test_newton_krylov_nonconvergence_semantics():
         with pytest.raises(nls2d.NonConvergenceError):
             s.step(0.5)
         assert np.array_equal(s.get_state(), u0)
+
+
+@pytest.mark.parametrize("v0", [0.0, -50.0])
+def test_batched_stage_solves_equal_sequential(monkeypatch, v0):
+    """The three stage systems of a Newton iteration solved together (one stream per
+    system, lockstep GMRES, one host round trip per Arnoldi step) give the same iterates
+    bit for bit as solving them one after the other (MB4CU_KR_BATCH=0)."""
+    g, model = paper_model(n=70 if v0 == 0.0 else 100, v0=v0)
+    u0 = nls2d.initial_condition(g)
+    out = {}
+    for batch in ("1", "0"):
+        monkeypatch.setenv("MB4CU_KR_BATCH", batch)
+        st = nls2d.StepStats()
+        with nls2d.Session(model, nls2d.Mb4Scheme(), nls2d.NewtonConfig(), kernel=NEWTON_KRYLOV) as s:
+            s.set_state(u0)
+            for _ in range(2):
+                s.step(0.01 if v0 == 0.0 else 0.002, st)
+            out[batch] = (s.get_state(), st.newton_iters)
+    assert out["1"][1] == out["0"][1]
+    assert np.array_equal(out["1"][0], out["0"][0])
