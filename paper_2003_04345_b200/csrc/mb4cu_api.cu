@@ -498,6 +498,7 @@ int kr_gmres(mb4cu_ctx* ctx, const MatVec& matvec, const double2* b, double2* x)
     if (int rc = kr_fetch(ctx, 1, &bn2)) return rc;
     const double bnorm = std::sqrt(bn2);
     if (bnorm == 0.0) return MB4CU_OK;
+    if (!std::isfinite(bnorm)) return fail(ctx, MB4CU_NONCONVERGED, "gmres: non-finite right-hand side");
     bool first = true;
     for (int iter = 0; iter < kKrylovMaxIters;) {
         double beta;
@@ -718,7 +719,16 @@ int krb_alloc(mb4cu_ctx* ctx, size_t len) {
 // system (identical arithmetic: the same kernels, host Givens updates and stopping
 // tests), advanced in lockstep, system q on its own stream, so one host round trip
 // per Arnoldi step serves all three and their small kernels run concurrently.
+int kr_gmres_stages_impl(mb4cu_ctx* ctx, const SweepConsts& c, const double2* const b[3], double2* const x[3]);
+
 int kr_gmres_stages(mb4cu_ctx* ctx, const SweepConsts& c, const double2* const b[3], double2* const x[3]) {
+    const int rc = kr_gmres_stages_impl(ctx, c, b, x);
+    if (rc != MB4CU_OK)  // no stage-stream work may outlive a failed solve (the buffers are reused)
+        for (int q = 0; q < 3; ++q) cudaStreamSynchronize(ctx->krb.st[q]);
+    return rc;
+}
+
+int kr_gmres_stages_impl(mb4cu_ctx* ctx, const SweepConsts& c, const double2* const b[3], double2* const x[3]) {
     auto& B = ctx->krb;
     const size_t n = B.len;
     const int m = B.m;
@@ -777,6 +787,7 @@ int kr_gmres_stages(mb4cu_ctx* ctx, const SweepConsts& c, const double2* const b
         fetch_sum(q, 1, &b2);
         bnorm[q] = std::sqrt(b2);
         if (bnorm[q] == 0.0) active[q] = false;
+        if (!std::isfinite(bnorm[q])) return fail(ctx, MB4CU_NONCONVERGED, "gmres: non-finite right-hand side");
     }
     auto Hat = [&](int q, int i, int jj) -> double& { return H[q][static_cast<size_t>(i) * m + jj]; };
     for (;;) {

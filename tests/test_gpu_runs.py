@@ -217,3 +217,36 @@ def test_full_baseline_run_energy_drift(name):
     H = obs[:, 3]
     assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
     assert iters.min() >= 2
+
+
+def test_zero_state_converges_in_the_first_sweep():
+    """u0 = 0 is a fixed point: the first sweep's update is exactly zero, so the step
+    stops after it (the later-sweep launch of the split step only reports), and the
+    state stays exactly zero."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, _ = configs.make_inputs(cfg)
+    zero = np.zeros(cfg.nx * cfg.ny, dtype=np.complex128)
+    with session(cfg, V) as s:
+        s.set_state(zero)
+        st = nls2d.StepStats()
+        s.step(cfg.dt, st)
+        assert st.newton_iters == 1
+        assert not np.any(s.get_state())
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_nonfinite_state_is_reported_and_left_unchanged(kernel):
+    """A NaN in the state makes the first sweep's residual non-finite: the step fails with
+    NonConvergenceError (reference: mb4_integrator.cpp:245-249 finite check) after the
+    halving attempts, and the resident state is the one that was set."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    bad = psi.copy()
+    bad[1234] = np.nan
+    with session(cfg, V, kernel=kernel) as s:
+        s.set_state(bad)
+        with pytest.raises(nls2d.NonConvergenceError):
+            s.step(cfg.dt)
+        got = s.get_state()
+    assert np.array_equal(np.isnan(got), np.isnan(bad))
+    assert np.array_equal(got[~np.isnan(bad)], bad[~np.isnan(bad)])
