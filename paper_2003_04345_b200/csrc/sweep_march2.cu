@@ -70,6 +70,11 @@
 #ifndef MB4_NT_FIRST
 #define MB4_NT_FIRST 128
 #endif
+// later sweeps: the own-column cubic term of a row before the row barrier (measured
+// equal or slower: the later sweeps are FP64-bound, not barrier-bound)
+#ifndef MB4_CUBIC_EARLY
+#define MB4_CUBIC_EARLY 0
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -210,7 +215,7 @@ struct March3 {
         int X0, Y0, R, yz0, nzrows;
         int xlim;        // right edge (exclusive) of the output rectangle
         int smask;       // stages stored (bit q): 7, or 4 = U3 only (speculative final sweep)
-        int gxa, gxb;    // global columns of smem columns t and t + NT (t < 2)
+        int gxa, gxb;    // global columns of smem column t + 1 and of halo column 0 / NT + 1 (t < 2)
         int next_row;    // global (periodic) row of the next z row to issue
         size_t next_off; // its element offset
     };
@@ -233,7 +238,9 @@ struct March3 {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && t >= 2) break;
-                const int col = t + h * NT;
+                // thread t fills its own column t + 1 (so it may read it before the row
+                // barrier); threads 0 / 1 also fill the halo columns 0 / NT + 1
+                const int col = h ? (t == 0 ? 0 : NT + 1) : t + 1;
                 const size_t g = rowoff + (h ? s.gxb : s.gxa);
                 cp_async16(&zu0[slot * G::ZW + col], a.u0 + g);
                 cp_async8(&zv[slot * G::ZW + col], a.V + g);
@@ -254,6 +261,29 @@ struct March3 {
         const unsigned hx = static_cast<unsigned>(__double2hiint(r.x)) & 0x7FFFFFFFu;
         const unsigned hy = static_cast<unsigned>(__double2hiint(r.y)) & 0x7FFFFFFFu;
         rmax = max(rmax, max(hx, hy));
+    }
+
+    // cubic term of Phi at one site: sum_q WA[k][q] |U_q|^2 U_q over the 6 Gauss nodes,
+    // U_q = sum_b L[q][b] z_b
+    __device__ __forceinline__ static void cubic_site(const Coef<ISO, DEF>& cf, const double2 z[4], double2 cub[3]) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) cub[k] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            double ur = cf.Lq(q, 0) * z[0].x, ui = cf.Lq(q, 0) * z[0].y;
+#pragma unroll
+            for (int b = 1; b < 4; ++b) {
+                ur = fma(cf.Lq(q, b), z[b].x, ur);
+                ui = fma(cf.Lq(q, b), z[b].y, ui);
+            }
+            const double n2 = fma(ur, ur, ui * ui);
+            const double gr = n2 * ur, gi = n2 * ui;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                cub[k].x = fma(cf.WAk(k, q), gr, cub[k].x);
+                cub[k].y = fma(cf.WAk(k, q), gi, cub[k].y);
+            }
+        }
     }
 
     // Iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); h3 = 3 * ((j / 3) & 1).
@@ -279,7 +309,20 @@ struct March3 {
         const int slot_new = ring(0);
         const int slot_cen = ring(1);
 
+        // ---- own column, before the row barrier --------------------------------
+        // The new z row j (own column: this thread's own cp.async group) and, for later
+        // sweeps, the cubic term of the centre row (own-column registers only) need no
+        // other thread's data, so a warp that finished the previous row early does this
+        // share (~40 % of the row's FP64 work) while slower warps of the CTA catch up.
         cp_async_wait<G::P - 1>();
+        zw[S_NEW][0] = zu0[slot_new * G::ZW + cc];
+        vw[S_NEW] = zv[slot_new * G::ZW + cc];
+        if (!FIRST) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZW + cc];
+        }
+        double2 cub[3];  // cubic term at the 6 Gauss nodes of the collocation polynomial
+        if (!FIRST && MB4_CUBIC_EARLY) cubic_site(cf, zw[S_CEN], cub);
         __syncthreads();
         issue_row(a, uin, s, j + G::P, ring(-G::P));
 
@@ -287,14 +330,6 @@ struct March3 {
         const int xout = s.X0 - M + t;
         const bool out_ok = yrel >= 0 && yrel < s.R && t >= M && t < NT - M && xout < s.xlim;
         const int par = j & 1, ppar = par ^ 1;
-
-        // ---- own column: new z row j --------------------------------------------
-        zw[S_NEW][0] = zu0[slot_new * G::ZW + cc];
-        vw[S_NEW] = zv[slot_new * G::ZW + cc];
-        if (!FIRST) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZW + cc];
-        }
 
         // own-column level history, read before this iteration overwrites it
         double2 pb_m2[3];  // phibar row i-2 (M == 2)
@@ -355,26 +390,7 @@ struct March3 {
                     z[q] = zw[S_CEN][q];
                     w[q] = cf.kv(d0, z[q], row[cc - 1], row[cc + 1], zw[S_DN][q], zw[S_NEW][q]);
                 }
-                // cubic term at the 6 Gauss nodes of the collocation polynomial
-                double2 cub[3];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) cub[k] = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int q = 0; q < 6; ++q) {
-                    double ur = cf.Lq(q, 0) * z[0].x, ui = cf.Lq(q, 0) * z[0].y;
-#pragma unroll
-                    for (int b = 1; b < 4; ++b) {
-                        ur = fma(cf.Lq(q, b), z[b].x, ur);
-                        ui = fma(cf.Lq(q, b), z[b].y, ui);
-                    }
-                    const double n2 = fma(ur, ur, ui * ui);
-                    const double gr = n2 * ur, gi = n2 * ui;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        cub[k].x = fma(cf.WAk(k, q), gr, cub[k].x);
-                        cub[k].y = fma(cf.WAk(k, q), gi, cub[k].y);
-                    }
-                }
+                if (!MB4_CUBIC_EARLY) cubic_site(cf, z, cub);
                 double2 phi[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -485,17 +501,18 @@ struct March3 {
             s.next_row = wrap_index(s.yz0, a.ny);
             s.next_off = static_cast<size_t>(s.next_row) * a.nx;
         }
-        const int xz0 = s.X0 - M - 1;
+        const int xz0 = s.X0 - M - 1;  // global column of smem column 0
+        const int t = static_cast<int>(threadIdx.x);
+        const int xa = xz0 + t + 1, xb = t == 0 ? xz0 : xz0 + NT + 1;  // see issue_row
         if (GHOST) {
             // padded columns; columns past the right halo only feed masked outputs
             const int last = a.pitch - 1;
-            const int ca = xz0 + static_cast<int>(threadIdx.x) + a.ghost;
-            const int cb = ca + NT;
+            const int ca = xa + a.ghost, cb = xb + a.ghost;
             s.gxa = ca < last ? ca : last;
             s.gxb = cb < last ? cb : last;
         } else {
-            s.gxa = wrap_index(xz0 + static_cast<int>(threadIdx.x), a.nx);
-            s.gxb = wrap_index(xz0 + static_cast<int>(threadIdx.x) + NT, a.nx);
+            s.gxa = wrap_index(xa, a.nx);
+            s.gxb = wrap_index(xb, a.nx);
         }
 #pragma unroll
         for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k, k);
