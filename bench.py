@@ -463,10 +463,10 @@ def run_dist(args, d: Dist):
     total_p = comm.allreduce_sum([psum])[0]
     pb *= 1.0 / math.sqrt(total_p)
     m = args.neumann if args.neumann >= 0 else 1
-    # halo exchange overlapped with the interior sweep; the interior leaves 8 SMs to
+    # halo exchange overlapped with the interior sweep; the interior leaves 2 SMs to
     # NCCL's kernels when there are peers
     be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
-                       overlap=not args.no_overlap, reserve_sms=8 if d.world > 1 else 0)
+                       overlap=not args.no_overlap, reserve_sms=2 if d.world > 1 else 0)
     be.set_state(pb)
     sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon)
     obs_w, _ = sess.run(cfg.dt, args.warmup) if args.warmup > 0 else (None, None)

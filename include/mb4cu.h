@@ -211,7 +211,8 @@ int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* 
 /* Halo-exchange overlap: sweep s in two launches.  region 1 = the boundary frame
  * (the `ghost`-wide strips the neighbours' halos need; run it first, then start
  * exchanging them), region 2 = the interior (needs no halo; launched with at most
- * grid_cap CTAs, 0 = all, to leave SMs to the concurrent NCCL kernels) which then
+ * grid_cap CTAs -- 0 = all, < 0 = all but those of -grid_cap SMs -- to leave SMs to the
+ * concurrent NCCL kernels) which then
  * leaves [||r||_inf over both, energy sums] in dev_out6 like mb4cu_sweep_async.
  * region 0 = the whole sub-domain (= mb4cu_sweep_async). */
 int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,

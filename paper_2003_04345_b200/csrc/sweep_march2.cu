@@ -1266,7 +1266,14 @@ struct Launcher3 {
 
     static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
         int grid = grid_size(device);
-        if (a.grid_cap > 0 && a.grid_cap < grid) grid = a.grid_cap;
+        if (a.grid_cap > 0 && a.grid_cap < grid) {
+            grid = a.grid_cap;
+        } else if (a.grid_cap < 0) {  // leave -grid_cap SMs to concurrent kernels (NCCL)
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+            const int keep = sms + a.grid_cap > 0 ? sms + a.grid_cap : 1;
+            grid = sms > 0 ? grid / sms * keep : grid;
+        }
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
         return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF, PH>),

@@ -452,8 +452,8 @@ class CudaBackend:
             self.L.mb4cu_set_stream(self.ctx, C.c_void_p(self.compute.cuda_stream))
             self._ev_frame = torch.cuda.Event()
             self._ev_x = torch.cuda.Event()
-            props = torch.cuda.get_device_properties(self.dev)
-            self.grid_cap = 2 * max(1, props.multi_processor_count - reserve_sms) if reserve_sms > 0 else 0
+            # negative: the library keeps the kernel's own CTAs-per-SM on all but reserve_sms SMs
+            self.grid_cap = -reserve_sms if reserve_sms > 0 else 0
 
     def _chk(self, rc):
         if rc:

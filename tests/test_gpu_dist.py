@@ -76,7 +76,7 @@ class LoopbackComm:
         self.h.bar.wait()
 
 
-def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None):
+def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None, reserve_sms=0):
     cfg = configs.CONFIGS[name]
     V, psi = configs.make_inputs(cfg)
     world = px * py
@@ -89,7 +89,7 @@ def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None):
             torch.cuda.set_device(0)
             dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
             be = D.CudaBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon,
-                               cfg.max_iters, m, 0, overlap=overlap)
+                               cfg.max_iters, m, 0, overlap=overlap, reserve_sms=reserve_sms)
             be.set_state(dec.block(psi))
             sess = D.DistributedSession(dec, be, LoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon)
             if hs is None:
@@ -134,8 +134,8 @@ def test_subdomain_path_matches_single_domain(px, py, m):
     assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
 
 
-@pytest.mark.parametrize("px,py", [(1, 1), (2, 1), (2, 2)])
-def test_halo_overlap_path_matches_single_domain(px, py):
+@pytest.mark.parametrize("px,py,reserve", [(1, 1, 0), (2, 1, 0), (2, 2, 0), (2, 1, 8)])
+def test_halo_overlap_path_matches_single_domain(px, py, reserve):
     """Boundary frame first, its halo exchange on a side stream while the interior
     is swept (mb4cu_sweep_region), U3 halos carried into the next step: the same
     trajectory bit for bit as the single-domain kernel, including a step that misses
@@ -143,7 +143,8 @@ def test_halo_overlap_path_matches_single_domain(px, py):
     name = "cfg2"
     cfg = configs.CONFIGS[name]
     hs = [cfg.dt, cfg.dt, 2 * cfg.dt, cfg.dt]
-    u_dec, _, sweeps_dec = _run_decomposed(name, px, py, 1, len(hs), overlap=True, hs=hs)
+    # reserve > 0: the interior launches leave that many SMs free (the NCCL overlap setting)
+    u_dec, _, sweeps_dec = _run_decomposed(name, px, py, 1, len(hs), overlap=True, hs=hs, reserve_sms=reserve)
     V, psi = configs.make_inputs(cfg)
     with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg),
                        neumann_terms=1) as s:
