@@ -430,6 +430,26 @@ def run_ours(args, d: Dist):
             "steps": k_e2e,
             "api": "mb4cu_set_state -> mb4cu_step -> mb4cu_get_state (host pinned buffers)",
         }
+        # the reference harness's run() (harness.cpp:64-133) through the same API: the
+        # initial state up, K steps with the per-step energy record read back (its CSV
+        # rows), the final state down -- host copies inside the timed region
+        host.numpy()[:] = psi.view(np.float64)
+        k_run = max(1, args.steps)
+        d.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.mb4cu_set_state(sess._ctx, ptr)
+        rows, _ = sess.run(cfg.dt, k_run)
+        L.mb4cu_get_state(sess._ctx, ptr)
+        run_s = d.max(time.perf_counter() - t0)
+        result["e2e_harness"] = {
+            "value": total_sites * k_run / run_s,
+            "unit": UNIT,
+            "h2d_bytes_per_step": 16 * n / k_run,
+            "d2h_bytes_per_step": 16 * n / k_run + rows.shape[1] * 8,
+            "steps": k_run,
+            "api": "mb4cu_set_state -> mb4cu_run (per-step energy rows to the host) -> mb4cu_get_state",
+        }
         del hv
 
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
