@@ -116,7 +116,8 @@ def test_create_rejects_bad_problems_before_touching_the_gpu():
     L = _lib.lib()
     s = nls2d.Mb4Scheme()
     V = np.zeros(16)
-    for field, val in (("nx", 1), ("epsilon", 0.0), ("max_iters", 0), ("neumann_terms", 7)):
+    for field, val in (("nx", 1), ("epsilon", 0.0), ("max_iters", 0), ("neumann_terms", 7), ("first_poly", 3),
+                       ("first_poly", -1)):
         p = _lib.Problem()
         p.nx = p.ny = 4
         p.cx = p.cy = 1.0
@@ -128,3 +129,12 @@ def test_create_rejects_bad_problems_before_touching_the_gpu():
         rc = L.mb4cu_create(C.byref(p), C.byref(s.raw), C.byref(ctx))
         assert rc == _lib.MB4CU_INVALID
         assert L.mb4cu_create_error().decode()
+
+
+def test_abi_null_and_range_checks_without_a_gpu():
+    """Entry points validate their arguments before any device work (status codes of
+    include/mb4cu.h); the spectral-bound setter rejects negative / non-finite bounds."""
+    L = _lib.lib()
+    assert L.mb4cu_spectral_bound(None, None) == _lib.MB4CU_INVALID
+    assert L.mb4cu_set_spectral_bound(None, 1.0) == _lib.MB4CU_INVALID
+    assert L.mb4cu_step(None, 0.01, None) == _lib.MB4CU_INVALID

@@ -272,3 +272,31 @@ def test_ragged_lattices_default_path_match_oracle(nx, ny, lx, ly):
         got = s.get_state()
     assert rel(got, ref) <= 1e-10
     assert np.abs(obs[:, 3] - ref_obs[:, 3]).max() <= 1e-13 * max(1.0, abs(ref_obs[0, 3]))
+
+
+def test_spectral_bound_abi():
+    """mb4cu_spectral_bound is the Gershgorin bound of the resident state rounded up to a
+    power of 2^(1/16) (the numpy model's value); an agreed bound set by the caller changes
+    the first sweep's polynomial but not the converged step (within the stopping rule)."""
+    import ctypes as C
+
+    from paper_2003_04345_b200 import _lib
+
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    model = configs.model_for(cfg, V)
+    L = _lib.lib()
+    with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg)) as s:
+        s.set_state(psi)
+        rho = C.c_double(0.0)
+        assert L.mb4cu_spectral_bound(s._ctx, C.byref(rho)) == 0
+        assert rho.value == pytest.approx(SM.spectral_bound(psi, V, cfg.gamma), rel=1e-14)
+        assert L.mb4cu_set_spectral_bound(s._ctx, -1.0) == _lib.MB4CU_INVALID
+        assert L.mb4cu_set_spectral_bound(s._ctx, float("nan")) == _lib.MB4CU_INVALID
+        s.step(cfg.dt)
+        u_own = s.get_state()
+        s.set_state(psi)
+        assert L.mb4cu_set_spectral_bound(s._ctx, 2.0 * rho.value) == 0
+        s.step(cfg.dt)
+        u_wide = s.get_state()
+    assert rel(u_own, u_wide) <= 1e-13
