@@ -386,6 +386,10 @@ def run_ours(args, d: Dist):
             # projected (5 sweeps at cfg5: 72 + 4 x 120 = 552 B/site-step): the deep first
             # sweep and the U3-only final sweep remove bytes, so frac above understates it
             "vs_hbm_bound_of_5_sweep_schedule": (value / d.world / (peak * 1e9 / 552.0)) if cfg.name == "cfg5" else None,
+            # SURVEY.md 8(d)'s formula bytes(step) = N (72 + 120 (S - 1)) counts the U3-only final
+            # sweep at 120 B/site; `frac` above uses the 88 B it moves
+            "frac_survey_8d": (n * (72.0 * args.steps + 120.0 * (prof["sweeps"] - args.steps))
+                               / (kern_ms * 1e-3) / 1e9 / peak) if kern_ms > 0 else None,
             "peak_kind": peak_kind,
             "kernel": "stage sweep",
             "alg_bytes_per_step": step_alg_bytes,
