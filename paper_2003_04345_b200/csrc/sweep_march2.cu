@@ -1094,7 +1094,9 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
 // form, so a deeper first sweep costs little and saves one later sweep: measured
 // 5 -> 4 sweeps/step at cfg5 for (MF, M) = (2, 1)); M: depth of the other sweeps.
 // PH: 0 = all sweeps of the (sub)step in one launch; 1 = the first sweep only;
-// 2 = the later sweeps, continuing from a PH = 1 launch (its residual in rmax[0]).
+// 2 = the later sweeps, continuing from a PH = 1 launch (its residual in rmax[0]);
+// 3 = the first sweep as a one-sweep launch with its status (sub-domain sweeps).
+// (PH 1 is kept free of the status path: a runtime switch costs it registers.)
 template <int MF, int M, int NT, int PH = 0>
 struct KGeom {
     // the first sweep runs MarchFirst (MF >= 1) or March3<0>; later sweeps March3<M>
@@ -1103,11 +1105,11 @@ struct KGeom {
         : MF >= 1                         ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
                                           : Geom3<0, NT>::bytes;
     static constexpr size_t later_bytes = Geom3<M, NT>::bytes;
-    static constexpr size_t bytes = PH == 1   ? first_bytes
+    static constexpr size_t bytes = PH == 1 || PH == 3 ? first_bytes
                                     : PH == 2 ? later_bytes
                                               : (first_bytes > later_bytes ? first_bytes : later_bytes);
     static constexpr int MINB = NT >= 256 ? 1
-                                : PH == 1 ? 2
+                                : PH == 1 || PH == 3 ? 2
                                 : PH == 2 ? (M <= 1 ? MB4_MINB_LATER : 2) * (128 / NT)
                                           : (M == 2 ? 2 : MB4_MINB_M1);
 };
@@ -1125,7 +1127,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     // for M <= 1 the constant bank is faster (measured: +18 %).
     // (not in first-sweep launches: their shared-memory rings need every byte)
     const SweepConsts* cptr = &c;
-    if constexpr (M == 2 && PH != 1) {
+    if constexpr (M == 2 && PH != 1 && PH != 3) {
         __shared__ __align__(16) SweepConsts csm;
         const double* src = reinterpret_cast<const double*>(&c);
         double* dst = reinterpret_cast<double*>(&csm);
@@ -1169,7 +1171,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         const int out = sg & 1;
         double2* const uout[3] = {a.U[out][0], a.U[out][1], a.U[out][2]};
         unsigned rmax = 0u;
-        if (PH == 1 || (PH == 0 && sg == 0)) {
+        if (PH == 1 || PH == 3 || (PH == 0 && sg == 0)) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
             sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
@@ -1188,7 +1190,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
                     a.obs_partial[blockIdx.x * kObsFields + threadIdx.x] = v;
                 }
             }
-        } else if constexpr (PH != 1) {
+        } else if constexpr (PH != 1 && PH != 3) {
             // Speculative final sweep (sg == spec_sweep, predicted by the host from the
             // previous step): only U3 -- the step result -- is stored, saving 32 of the
             // 120 B/site.  If it does not converge, it is redone below with all stages
@@ -1199,11 +1201,8 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
                                                        sg == a.spec_sweep && !redo ? 4 : 7);
         }
         if constexpr (PH == 1) {  // the later-sweep launch takes it from here
-            if (a.max_iters > 1) {   // (a one-sweep launch finishes its status below)
-                block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull,
-                             &a.rmax[0]);
-                return;
-            }
+            block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[0]);
+            return;
         }
         if (redo) {  // same residual as the speculative pass: no new test
             redo = false;
@@ -1305,9 +1304,9 @@ cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaS
         // their own register and shared-memory footprints
         if (a.ghost > 0 && a.max_iters == 1) {
             if (a.sweep0 == 0) {
-                if (c.iso && c.def) return Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 1>::launch(a, c, device, s);
-                return c.iso ? Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 1>::launch(a, c, device, s)
-                             : Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 1>::launch(a, c, device, s);
+                if (c.iso && c.def) return Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 3>::launch(a, c, device, s);
+                return c.iso ? Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 3>::launch(a, c, device, s)
+                             : Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 3>::launch(a, c, device, s);
             }
             if (c.iso && c.def) return Launcher3<MF, M, MB4_NT_LATER, true, true, true, 2>::launch(a, c, device, s);
             return c.iso ? Launcher3<MF, M, MB4_NT_LATER, true, true, false, 2>::launch(a, c, device, s)
@@ -1343,9 +1342,9 @@ int grid3(int device) {
                           Launcher3<MF, M, MB4_NT_LATER, false, false, false, 2>::grid_size(device),
                           Launcher3<MF, M, MB4_NT_LATER, true, false, true, 2>::grid_size(device)};
         for (int x : w) g = x > g ? x : g;
-        const int wg[6] = {Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 1>::grid_size(device),
-                           Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 1>::grid_size(device),
-                           Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 1>::grid_size(device),
+        const int wg[6] = {Launcher3<MF, M, MB4_NT_FIRST, true, true, false, 3>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_FIRST, false, true, false, 3>::grid_size(device),
+                           Launcher3<MF, M, MB4_NT_FIRST, true, true, true, 3>::grid_size(device),
                            Launcher3<MF, M, MB4_NT_LATER, true, true, false, 2>::grid_size(device),
                            Launcher3<MF, M, MB4_NT_LATER, false, true, false, 2>::grid_size(device),
                            Launcher3<MF, M, MB4_NT_LATER, true, true, true, 2>::grid_size(device)};
