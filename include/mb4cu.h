@@ -218,6 +218,26 @@ int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* 
 int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
                        double* dev_out6);
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
+
+/* ---- Stage-split Newton-Krylov (the paper's 3-way stage partition) ---------------
+ * The simplified Newton iteration of the stiff-regime solver (mb4_integrator.cpp:194-255
+ * with matrix-free, Fourier-preconditioned GMRES stage solves), opened up so that the
+ * three decoupled stage systems (I - h lam_k J) x_k = b_k of an iteration can be solved
+ * on different GPUs -- the partition the paper parallelises over nodes
+ * (paper_2003_04345_b200/dist.py StageSplitSession).  Every rank holds the whole lattice:
+ *   mb4cu_ns_begin(ctx, h);
+ *   repeat: mb4cu_ns_phibar(ctx);  mb4cu_ns_solve(ctx, k) for the owned k;
+ *           exchange x_k (mb4cu_ns_get_correction / mb4cu_ns_set_correction, 2N doubles
+ *           of device memory);  mb4cu_ns_update(ctx, &r);  until r <= epsilon;
+ *   mb4cu_ns_commit(ctx);
+ * A context that solves all three systems reproduces kernel 3's step bit for bit. */
+int mb4cu_ns_begin(mb4cu_ctx* ctx, double h);
+int mb4cu_ns_phibar(mb4cu_ctx* ctx);
+int mb4cu_ns_solve(mb4cu_ctx* ctx, int k);
+int mb4cu_ns_get_correction(mb4cu_ctx* ctx, int k, double* dev_out);
+int mb4cu_ns_set_correction(mb4cu_ctx* ctx, int k, const double* dev_in);
+int mb4cu_ns_update(mb4cu_ctx* ctx, double* rmax);
+int mb4cu_ns_commit(mb4cu_ctx* ctx);
 /* Local energy sums of the resident state (ghosts of u0 must be current). */
 int mb4cu_observables_sums(mb4cu_ctx* ctx, double* local_sums5);
 

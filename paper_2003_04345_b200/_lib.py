@@ -156,6 +156,13 @@ def lib() -> C.CDLL:
         "mb4cu_sweep_region": (I, [P, D, I, I, I, I, P]),
         "mb4cu_commit_step": (I, [P, I]),
         "mb4cu_observables_sums": (I, [P, DP]),
+        "mb4cu_ns_begin": (I, [P, D]),
+        "mb4cu_ns_phibar": (I, [P]),
+        "mb4cu_ns_solve": (I, [P, I]),
+        "mb4cu_ns_get_correction": (I, [P, I, P]),
+        "mb4cu_ns_set_correction": (I, [P, I, P]),
+        "mb4cu_ns_update": (I, [P, DP]),
+        "mb4cu_ns_commit": (I, [P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -180,4 +187,6 @@ EXPORTED = [
     "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
     "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",
     "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_sweep_region", "mb4cu_commit_step", "mb4cu_observables_sums",
+    "mb4cu_ns_begin", "mb4cu_ns_phibar", "mb4cu_ns_solve", "mb4cu_ns_get_correction", "mb4cu_ns_set_correction",
+    "mb4cu_ns_update", "mb4cu_ns_commit",
 ]

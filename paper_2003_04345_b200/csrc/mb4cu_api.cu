@@ -37,6 +37,10 @@ struct mb4cu_ctx {
     int last_sweeps = 0;  // sweeps of the last converged step (predicts the final sweep)
     int first_poly = 1;   // first-sweep polynomial (resolved): 1 = Neumann (Taylor), 2 = Chebyshev
     bool kr_batch = true; // Newton-Krylov: the three stage solves in flight together (krb)
+    // stage-split Newton-Krylov (mb4cu_ns_*): the step size and constants of the open step
+    bool ns_open = false;
+    double ns_h = 0.0;
+    SweepConsts ns_c{};
     double vmin = 0;      // min V (host, at create)
     double rho_override = 0;  // > 0: spectral bound set by the caller (decomposed lattices)
     int ghost = 0, pitch = 0;  // sub-domain mode: halo width and padded row pitch
@@ -1895,6 +1899,89 @@ int mb4cu_eval_phi(mb4cu_ctx* ctx, const double* u0, const double* s1, const dou
     for (int i = 0; i < 3; ++i)
         MB4_CUDA(ctx, cudaMemcpyAsync(hout[i], ph[i], sb, cudaMemcpyDeviceToHost, ctx->stream));
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+
+// ---- Stage-split Newton-Krylov (the paper's 3-way stage partition) --------------
+// The simplified Newton iteration of substep_krylov, opened up so that the three
+// decoupled stage solves of an iteration can run on different devices / processes:
+//   ns_begin(h); repeat { ns_phibar; ns_solve(k) for the owned k; exchange the
+//   corrections (ns_get/set_correction); ns_update -> ||r||_inf } until r <= eps;
+//   ns_commit.  The same kernels and GMRES as substep_krylov: a context that solves all
+//   three systems itself reproduces it bit for bit.
+static double2* ns_b(mb4cu_ctx* ctx, int k) { return kr_vec(ctx, ctx->kr.m + 1 + k); }
+static double2* ns_x(mb4cu_ctx* ctx, int k) { return kr_vec(ctx, ctx->kr.m + 4 + k); }
+
+int mb4cu_ns_begin(mb4cu_ctx* ctx, double h) {
+    if (!ctx) return MB4CU_INVALID;
+    if (!(h > 0.0)) return fail(ctx, MB4CU_INVALID, "ns_begin: h must be positive");
+    if (ctx->ghost > 0) return fail(ctx, MB4CU_INVALID, "ns_begin: needs a whole-lattice context");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (int rc = refresh_amax2(ctx)) return rc;
+    if (int rc = kr_alloc(ctx, ctx->n)) return rc;
+    ctx->ns_c = make_consts(ctx, h);
+    ctx->ns_h = h;
+    const size_t sb = ctx->n * sizeof(double2);
+    for (int i = 0; i < 3; ++i)
+        MB4_CUDA(ctx, cudaMemcpyAsync(ctx->U[0][i], ctx->u0, sb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (int rc = fft_prepare(ctx, 1)) return rc;
+    ctx->ns_open = true;
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_phibar(mb4cu_ctx* ctx) {
+    if (!ctx || !ctx->ns_open) return fail(ctx, MB4CU_INVALID, "ns_phibar: no open step (ns_begin)");
+    const double2* cst[3] = {ctx->U[0][0], ctx->U[0][1], ctx->U[0][2]};
+    double2* b[3] = {ns_b(ctx, 0), ns_b(ctx, 1), ns_b(ctx, 2)};
+    MB4_CUDA(ctx, mb4cu::kr_phibar(ctx->nx, ctx->ny, ctx->u0, cst, ctx->V, b, ctx->ns_c, ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_solve(mb4cu_ctx* ctx, int k) {
+    if (!ctx || !ctx->ns_open || k < 0 || k > 2) return fail(ctx, MB4CU_INVALID, "ns_solve: open step, k in 0..2");
+    const SweepConsts& c = ctx->ns_c;
+    const double hl = c.hlam[k];
+    auto mv = [&](const double2* xin, double2* yout) {
+        return mb4cu::kr_matvec(xin, yout, ctx->u0, ctx->V, ctx->nx, ctx->ny, hl, c, ctx->stream);
+    };
+    return kr_gmres_fft(ctx, 1, hl, nullptr, mv, ns_b(ctx, k), ns_x(ctx, k));
+}
+
+int mb4cu_ns_get_correction(mb4cu_ctx* ctx, int k, double* dev_out) {
+    if (!ctx || !ctx->ns_open || k < 0 || k > 2 || !dev_out)
+        return fail(ctx, MB4CU_INVALID, "ns_get_correction: open step, k in 0..2, buffer");
+    MB4_CUDA(ctx, cudaMemcpyAsync(dev_out, ns_x(ctx, k), ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_set_correction(mb4cu_ctx* ctx, int k, const double* dev_in) {
+    if (!ctx || !ctx->ns_open || k < 0 || k > 2 || !dev_in)
+        return fail(ctx, MB4CU_INVALID, "ns_set_correction: open step, k in 0..2, buffer");
+    MB4_CUDA(ctx, cudaMemcpyAsync(ns_x(ctx, k), dev_in, ctx->n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_update(mb4cu_ctx* ctx, double* rmax) {
+    if (!ctx || !ctx->ns_open || !rmax) return fail(ctx, MB4CU_INVALID, "ns_update: open step, output");
+    double2* st[3] = {ctx->U[0][0], ctx->U[0][1], ctx->U[0][2]};
+    const double2* cx[3] = {ns_x(ctx, 0), ns_x(ctx, 1), ns_x(ctx, 2)};
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), ctx->stream));
+    MB4_CUDA(ctx, mb4cu::kr_update(st, cx, ctx->n, ctx->d_rmax, ctx->ns_c, ctx->stream));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *rmax = decode_bits(*ctx->h_rmax);
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_commit(mb4cu_ctx* ctx) {
+    if (!ctx || !ctx->ns_open) return fail(ctx, MB4CU_INVALID, "ns_commit: no open step");
+    std::swap(ctx->u0, ctx->U[0][2]);
+    ctx->obs_cached = false;
+    ctx->ns_open = false;
     return MB4CU_OK;
 }
 

@@ -155,6 +155,10 @@ class Comm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return t.cpu().numpy()
 
+    def broadcast_(self, t, src: int) -> None:
+        """In-place broadcast of a device tensor from rank src."""
+        self.dist.broadcast(t, src=src)
+
     def exchange(self, pairs):
         """pairs: list of (send_tensor, dst, recv_tensor, src); all posted at once."""
         ops = []
@@ -588,3 +592,64 @@ class CudaBackend:
         if self.ctx:
             self.L.mb4cu_destroy(self.ctx)
             self.ctx = None
+
+
+class StageSplitSession:
+    """The paper's stage partition on GPUs: every rank holds the
+    whole lattice in its own context, and the three decoupled stage systems
+    (I - h lam_k J) x_k = b_k of each simplified-Newton iteration (the reference's
+    WorkerPool tasks, mb4_integrator.cpp:221-229; the paper's per-node solves) are solved
+    on different ranks: rank r owns the systems k with k % world == r.  The corrections
+    are broadcast from their owners and every rank applies the same update, so all ranks
+    hold the same iterate -- bit-identical to the single-context Newton-Krylov step
+    (kernel 3).  This is the stiff-regime (paper-scale) partition; the matrix-free sweep
+    path shards the lattice instead (DistributedSession).  No step halving: a step that
+    does not converge raises NonConvergence with the state unchanged."""
+
+    def __init__(self, session, comm, rank: int, world: int, epsilon: float, max_iters: int = 50,
+                 lib=None, device=None):
+        """lib / device: injection points for the CPU tests (a numpy stand-in of the
+        mb4cu_ns_* entry points and host buffers)."""
+        import torch
+
+        self.s, self.comm, self.rank, self.world = session, comm, rank, world
+        self.eps, self.max_iters = epsilon, max_iters
+        self.L = lib if lib is not None else _lib.lib()
+        self.torch = torch
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.type == "cuda":
+            # the context runs on torch's stream so the collectives order after its kernels
+            self.L.mb4cu_set_stream(session._ctx, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1))
+        self.buf = [torch.empty(2 * session.n, dtype=torch.float64, device=dev) for _ in range(3)]
+
+    def _chk(self, rc):
+        if rc:
+            raise RuntimeError(f"mb4cu status {rc}: {self.L.mb4cu_last_error(self.s._ctx).decode()}")
+
+    def owner(self, k: int) -> int:
+        return k % self.world
+
+    def step(self, h: float) -> int:
+        """One MB4 step; returns the Newton iterations."""
+        ctx = self.s._ctx
+        self._chk(self.L.mb4cu_ns_begin(ctx, h))
+        r = math.inf
+        for it in range(1, self.max_iters + 1):
+            self._chk(self.L.mb4cu_ns_phibar(ctx))
+            for k in range(3):
+                if self.owner(k) == self.rank:
+                    self._chk(self.L.mb4cu_ns_solve(ctx, k))
+                    self._chk(self.L.mb4cu_ns_get_correction(ctx, k, C.c_void_p(self.buf[k].data_ptr())))
+            for k in range(3):
+                self.comm.broadcast_(self.buf[k], self.owner(k))
+                if self.owner(k) != self.rank:
+                    self._chk(self.L.mb4cu_ns_set_correction(ctx, k, C.c_void_p(self.buf[k].data_ptr())))
+            rv = C.c_double(0.0)
+            self._chk(self.L.mb4cu_ns_update(ctx, C.byref(rv)))
+            r = rv.value
+            if not math.isfinite(r):
+                raise NonConvergence("newton_solve: iteration diverged (non-finite update)", math.inf)
+            if r <= self.eps:  # the reference test (mb4_integrator.cpp:250)
+                self._chk(self.L.mb4cu_ns_commit(ctx))
+                return it
+        raise NonConvergence(f"newton_solve: no convergence after {self.max_iters} iterations", r)

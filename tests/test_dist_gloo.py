@@ -7,6 +7,7 @@ halo rectangles, sweep s / commit).  World sizes 2 and 4 must reproduce the
 single-domain matrix-free iteration bit for bit, and the reference oracle within
 the parity bound.
 """
+import ctypes as C
 import os
 import socket
 
@@ -296,3 +297,97 @@ def test_choose_grid_and_neighbours():
     assert (dec.rx, dec.ry, dec.lnx, dec.lny) == (1, 2, 8192, 8192)
     assert dec.neighbor(D.EAST) == 4 and dec.neighbor(D.WEST) == 4
     assert dec.neighbor(D.NORTH) == 7 and dec.neighbor(D.SOUTH) == 3
+
+
+# ----------------------------------------------------------------------------- stage split
+
+
+class FakeNsLib:
+    """Numpy stand-in of the mb4cu_ns_* entry points (test infrastructure): a contracting
+    linear 'Newton iteration' on three stage vectors whose stage solves depend only on the
+    current stages -- so a rank that did not solve system k must receive its correction."""
+
+    def __init__(self, n):
+        self.n = n
+        rng = np.random.default_rng(5)
+        self.u0 = rng.standard_normal(2 * n)
+        self.A = [0.3 + 0.1 * k for k in range(3)]
+        self.solved = []
+
+    def mb4cu_ns_begin(self, ctx, h):
+        self.h = h
+        self.st = [self.u0.copy() for _ in range(3)]
+        self.x = [np.full(2 * self.n, np.nan) for _ in range(3)]
+        return 0
+
+    def mb4cu_ns_phibar(self, ctx):
+        self.b = [self.A[k] * (self.st[k] - self.u0 * (1.0 + self.h * (k + 1))) for k in range(3)]
+        return 0
+
+    def mb4cu_ns_solve(self, ctx, k):
+        self.x[k] = -self.b[k] / (1.0 + self.A[k])
+        self.solved.append(k)
+        return 0
+
+    def mb4cu_ns_get_correction(self, ctx, k, ptr):
+        C.memmove(ptr.value, self.x[k].ctypes.data, self.x[k].nbytes)
+        return 0
+
+    def mb4cu_ns_set_correction(self, ctx, k, ptr):
+        C.memmove(self.x[k].ctypes.data, ptr.value, self.x[k].nbytes)
+        return 0
+
+    def mb4cu_ns_update(self, ctx, rref):
+        for k in range(3):
+            self.st[k] = self.st[k] + self.x[k]
+        rref._obj.value = float(max(np.abs(x).max() for x in self.x))
+        return 0
+
+    def mb4cu_ns_commit(self, ctx):
+        self.u0 = self.st[2].copy()
+        return 0
+
+    def mb4cu_last_error(self, ctx):
+        return b""
+
+
+class _Sess:
+    _ctx = None
+
+    def __init__(self, n):
+        self.n = n
+
+
+class _GlooBroadcast:
+    def broadcast_(self, t, src):
+        dist.broadcast(t, src=src)
+
+
+def _worker_split(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lib = FakeNsLib(64)
+        sess = D.StageSplitSession(_Sess(64), _GlooBroadcast(), rank, world, 1e-14, 200, lib=lib,
+                                   device=torch.device("cpu"))
+        its = [sess.step(0.01) for _ in range(3)]
+        np.savez(os.path.join(out_dir, f"s{rank}.npz"), u=lib.u0, its=its, solved=np.array(lib.solved))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stage_split_control_flow_gloo(tmp_path, world):
+    """dist.StageSplitSession across processes (gloo): each rank solves only the stage
+    systems it owns (k % world == rank), receives the others by broadcast, and every rank
+    ends every step with the same state and iteration count as one rank solving all three."""
+    mp.spawn(_worker_split, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    lib = FakeNsLib(64)
+    sess = D.StageSplitSession(_Sess(64), None, 0, 1, 1e-14, 200, lib=lib, device=torch.device("cpu"))
+    sess.comm = type("NoComm", (), {"broadcast_": lambda self, t, src: None})()
+    its = [sess.step(0.01) for _ in range(3)]
+    for r in range(world):
+        d = np.load(tmp_path / f"s{r}.npz")
+        assert list(d["its"]) == its
+        assert np.array_equal(d["u"], lib.u0)
+        assert set(d["solved"].tolist()) == {k for k in range(3) if k % world == r}

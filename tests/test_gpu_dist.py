@@ -157,3 +157,59 @@ def test_halo_overlap_path_matches_single_domain(px, py, reserve):
         u = s.get_state()
     assert list(sweeps_dec) == sweeps
     assert np.array_equal(u_dec, u), np.abs(u_dec - u).max()
+
+
+class LoopbackBroadcast(LoopbackComm):
+    def broadcast_(self, t, src):
+        torch.cuda.synchronize()
+        vals = self._gather(t.cpu().clone() if self.rank == src else None)
+        t.copy_(vals[src].to(t.device))
+        torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_stage_split_matches_single_context_newton_krylov(world):
+    """The paper's stage partition (dist.StageSplitSession): each rank solves the stage
+    systems it owns and the corrections are broadcast -- here `world` thread-loopback ranks,
+    each with its own context on one GPU -- reproduces the single-context Newton-Krylov step
+    (kernel 3) bit for bit, with the same Newton iteration counts."""
+    n, gamma = 70, 0.1
+    g = nls2d.GridSpec(n, n, 2 * np.pi, 2 * np.pi)
+    model = nls2d.GridModel(g, gamma)
+    u0 = nls2d.initial_condition(g)
+    cfg = nls2d.NewtonConfig()
+    hs = [0.01, 0.01]
+    with nls2d.Session(model, nls2d.Mb4Scheme(), cfg, kernel=3) as s:
+        s.set_state(u0)
+        its = []
+        for h in hs:
+            st = nls2d.StepStats()
+            s.step(h, st)
+            its.append(st.newton_iters)
+        ref = s.get_state()
+    hub = Hub(world)
+    out = [None] * world
+    errs = []
+
+    def work(rank):
+        try:
+            torch.cuda.set_device(0)
+            with nls2d.Session(model, nls2d.Mb4Scheme(), cfg, kernel=3) as s:
+                s.set_state(u0)
+                sess = D.StageSplitSession(s, LoopbackBroadcast(hub, rank), rank, world, cfg.epsilon, cfg.max_iters)
+                got_its = [sess.step(h) for h in hs]
+                out[rank] = (s.get_state(), got_its)
+        except Exception as exc:
+            errs.append(exc)
+            hub.bar.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    for u, got_its in out:
+        assert got_its == its
+        assert np.array_equal(u, ref)
