@@ -75,6 +75,10 @@
 #ifndef MB4_CUBIC_EARLY
 #define MB4_CUBIC_EARLY 0
 #endif
+// default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
+#ifndef MB4_SYM_PAIRS
+#define MB4_SYM_PAIRS 1
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -268,6 +272,34 @@ struct March3 {
     __device__ __forceinline__ static void cubic_site(const Coef<ISO, DEF>& cf, const double2 z[4], double2 cub[3]) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) cub[k] = make_double2(0.0, 0.0);
+        if constexpr (DEF && MB4_SYM_PAIRS) {
+            // default scheme: symmetric node pairs q, 5 - q (defscheme LS / LD):
+            // U_q = E + O, U_{5-q} = E - O -- 12 instead of 24 node weights, 4 fewer FP64 ops
+            const double2 s03 = make_double2(z[0].x + z[3].x, z[0].y + z[3].y);
+            const double2 d03 = make_double2(z[0].x - z[3].x, z[0].y - z[3].y);
+            const double2 s12 = make_double2(z[1].x + z[2].x, z[1].y + z[2].y);
+            const double2 d12 = make_double2(z[1].x - z[2].x, z[1].y - z[2].y);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double ex = fma(defscheme::LS[q][1], s12.x, defscheme::LS[q][0] * s03.x);
+                const double ey = fma(defscheme::LS[q][1], s12.y, defscheme::LS[q][0] * s03.y);
+                const double ox = fma(defscheme::LD[q][1], d12.x, defscheme::LD[q][0] * d03.x);
+                const double oy = fma(defscheme::LD[q][1], d12.y, defscheme::LD[q][0] * d03.y);
+#pragma unroll
+                for (int side = 0; side < 2; ++side) {
+                    const int qq = side ? 5 - q : q;
+                    const double ur = side ? ex - ox : ex + ox, ui = side ? ey - oy : ey + oy;
+                    const double n2 = fma(ur, ur, ui * ui);
+                    const double gr = n2 * ur, gi = n2 * ui;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        cub[k].x = fma(cf.WAk(k, qq), gr, cub[k].x);
+                        cub[k].y = fma(cf.WAk(k, qq), gi, cub[k].y);
+                    }
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             double ur = cf.Lq(q, 0) * z[0].x, ui = cf.Lq(q, 0) * z[0].y;
