@@ -475,11 +475,16 @@ def run_dist(args, d: Dist):
 
     from paper_2003_04345_b200 import configs, dist as D, nls2d
 
-    if args.config != "cfg5":
-        raise SystemExit("multi-GPU runs use the cfg5 weak-scaling workload")
+    if args.config not in ("cfg3", "cfg4", "cfg5"):
+        raise SystemExit("multi-GPU runs: cfg5 (weak scaling) or cfg3 / cfg4 (strong scaling)")
     torch.cuda.set_device(d.local)
-    gnx, gny = configs.cfg5_lattice(d.world)
-    cfg = configs.CONFIGS["cfg5"].with_lattice(gnx, gny)
+    weak = args.config == "cfg5"
+    if weak:  # BASELINE configs[4]: 8192^2 sites per GPU
+        gnx, gny = configs.cfg5_lattice(d.world)
+        cfg = configs.CONFIGS["cfg5"].with_lattice(gnx, gny)
+    else:  # BASELINE configs[2] / [3]: the fixed lattice split over the GPUs
+        cfg = configs.CONFIGS[args.config]
+        gnx, gny = cfg.nx, cfg.ny
     px, py = D.choose_grid(d.world, gnx, gny)
     dec = D.Decomposition(gnx, gny, px, py, d.rank)
     Vb, pb, psum = configs.make_block(cfg, dec.x0, dec.y0, dec.lnx, dec.lny)
@@ -521,16 +526,18 @@ def run_dist(args, d: Dist):
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded defects + Gaussian packets, configs.py)",
-        "config": {"workload": f"cfg5 weak scaling: {gnx}x{gny} lattice, {dec.lnx}x{dec.lny} sites per GPU, "
-                               f"dt={cfg.dt}, g={cfg.g}, eps={cfg.epsilon}",
+        "config": {"workload": f"{args.config} {'weak' if weak else 'strong'} scaling: {gnx}x{gny} lattice, "
+                               f"{dec.lnx}x{dec.lny} sites per GPU, dt={cfg.dt}, g={cfg.g}, eps={cfg.epsilon}",
                    "lattice": [gnx, gny], "sites_per_gpu": n_local, "neumann_terms": m,
                    "process_grid": [px, py], "parallelism": f"2-D domain decomposition {px}x{py}",
                    "halo_exchange": ("between sweeps" if args.no_overlap else
                                      "overlapped: boundary frame swept first, its NCCL exchange on a side "
                                      "stream while the interior is swept"),
-                   "l2": "inputs larger than L2 (state+stages >= 3 GiB per GPU)"},
+                   "l2": (f"working set {dec.lnx * dec.lny * 120 / 2**20:.0f} MiB per GPU "
+                          + ("> L2 (126 MB)" if dec.lnx * dec.lny * 120 > 126e6 else
+                             "<= L2 (126 MB): not flushed between steps, strong-scaling reference only"))},
         "sweeps_per_step": float(np.mean(sweeps)),
         "energy_drift": d.max(drift),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
