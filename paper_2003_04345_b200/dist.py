@@ -59,26 +59,31 @@ def stage_converged(r: float, r_prev: float, s: int, eps: float) -> bool:
 
 
 def choose_grid(n: int, gnx: int, gny: int) -> Tuple[int, int]:
-    """px * py = n minimising the halo perimeter per rank (ties: squarest blocks)."""
+    """px * py = n minimising the halo perimeter per rank (ties: squarest blocks, then
+    even splits).  Uneven splits are allowed (blocks differ by at most one column / row)."""
     best = None
     for px in range(1, n + 1):
         if n % px:
             continue
         py = n // px
-        if gnx % px or gny % py:
+        if px > gnx or py > gny:
             continue
-        lnx, lny = gnx // px, gny // py
+        lnx, lny = -(-gnx // px), -(-gny // py)  # the largest block
         cost = (lny if px > 1 else 0) + (lnx if py > 1 else 0)
-        key = (cost, abs(lnx - lny), px)
+        key = (cost, abs(lnx - lny), int(gnx % px != 0) + int(gny % py != 0), px)
         if best is None or key < best[0]:
             best = (key, (px, py))
     if best is None:
-        raise ValueError(f"cannot split {gnx}x{gny} over {n} ranks evenly")
+        raise ValueError(f"cannot split {gnx}x{gny} over {n} ranks")
     return best[1]
 
 
 @dataclass
 class Decomposition:
+    """Tensor-product block split of the periodic gnx x gny lattice over a px x py torus:
+    process column rx owns columns [rx gnx / px, (rx + 1) gnx / px), process row ry the
+    rows [ry gny / py, (ry + 1) gny / py) -- so ranks in one process row share the block
+    height and ranks in one process column the block width (what the halo strips need)."""
     gnx: int
     gny: int
     px: int
@@ -86,8 +91,8 @@ class Decomposition:
     rank: int
 
     def __post_init__(self):
-        if self.gnx % self.px or self.gny % self.py:
-            raise ValueError("lattice must split evenly over the process grid")
+        if not (1 <= self.px <= self.gnx and 1 <= self.py <= self.gny):
+            raise ValueError("process grid larger than the lattice")
         if not 0 <= self.rank < self.px * self.py:
             raise ValueError("rank out of range")
 
@@ -100,20 +105,20 @@ class Decomposition:
         return self.rank // self.px
 
     @property
-    def lnx(self) -> int:
-        return self.gnx // self.px
-
-    @property
-    def lny(self) -> int:
-        return self.gny // self.py
-
-    @property
     def x0(self) -> int:
-        return self.rx * self.lnx
+        return self.rx * self.gnx // self.px
 
     @property
     def y0(self) -> int:
-        return self.ry * self.lny
+        return self.ry * self.gny // self.py
+
+    @property
+    def lnx(self) -> int:
+        return (self.rx + 1) * self.gnx // self.px - self.x0
+
+    @property
+    def lny(self) -> int:
+        return (self.ry + 1) * self.gny // self.py - self.y0
 
     def rank_of(self, rx: int, ry: int) -> int:
         return (ry % self.py) * self.px + (rx % self.px)

@@ -261,7 +261,7 @@ def test_device_reduction_path_lookahead_and_speculation(tmp_path, px, py):
     assert np.array_equal(glob.reshape(-1), u)
 
 
-@pytest.mark.parametrize("px,py,m", [(2, 1, 1), (1, 2, 2), (2, 2, 1)])
+@pytest.mark.parametrize("px,py,m", [(2, 1, 1), (1, 2, 2), (2, 2, 1), (3, 1, 1), (1, 3, 2)])
 def test_decomposed_run_reproduces_single_domain(tmp_path, px, py, m):
     world, nsteps = px * py, 3
     mp.spawn(_worker, args=(world, _free_port(), px, py, m, nsteps, str(tmp_path)), nprocs=world, join=True)

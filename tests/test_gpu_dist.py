@@ -116,7 +116,7 @@ def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None, reserve_sms
     return glob.reshape(-1), out[0][2], out[0][3]
 
 
-@pytest.mark.parametrize("px,py,m", [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1), (2, 2, 2)])
+@pytest.mark.parametrize("px,py,m", [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1), (2, 2, 2), (3, 1, 1), (1, 3, 2)])
 def test_subdomain_path_matches_single_domain(px, py, m):
     name, nsteps = "cfg2", 4
     cfg = configs.CONFIGS[name]
