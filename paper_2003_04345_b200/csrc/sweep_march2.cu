@@ -1,28 +1,36 @@
-// Production stage-sweep kernel (v3): one persistent cooperative launch per MB4
-// step, marching column bands; vertical neighbours in registers / own-column
-// smem history, horizontal neighbours through shared-memory rows.
+// Production stage-sweep kernels: the MB4 step as column-band marches; vertical
+// neighbours in registers / own-column smem history, horizontal neighbours through
+// shared-memory rows.  Default schedule (launch_split): two launches per (sub)step,
+//   PH 1  the first sweep (MarchFirst2: depth-6 J-chain, Chebyshev-placed, fused energy
+//         monitor; 2 CTAs/SM, bound by the shared-memory data pipe), then
+//   PH 2  a persistent cooperative launch for the later sweeps (March3: grid barrier
+//         between sweeps, in-kernel convergence test, speculative U3-only final sweep;
+//         3 CTAs/SM at depth 1, bound by the FP64 pipe).
+// PH 0 runs both in one launch (shallow first sweeps); PH 3 is the first sweep as a
+// one-sweep launch with its status (sub-domain sweeps of the multi-GPU path).
 //
 // Same algorithm as sweep_march.cu and sweep_tiled.cu (Phi -> T^-1 -> M-term
 // Neumann (I - h lam_k J)^-1 -> T -> update -> ||r||_inf; site_math.cuh) and
 // the same band / work split.  Organised around the measured limits of the
 // earlier versions (profiles/r01_*): shared-memory wavefronts, FP64 latency
-// with 8 warps/SM, and integer overhead.
+// and integer overhead.
 //  - Each thread keeps a 3-row register window of its own column of
-//    z = (u0, U1..U3).  z rows arrive by cp.async in a 6-row ring; only the
-//    centre row's left/right neighbours and the new own-column row are read
-//    from it.
+//    z = (u0, U1..U3).  z rows arrive by cp.async in a 6-row ring (each thread fills
+//    its own column); only the centre row's left/right neighbours are read from it
+//    after the row barrier.
 //  - Neumann level n works on row i - n at iteration i.  Every level publishes
 //    its row into a double-buffered smem row; the neighbours read it one
 //    iteration later, and the publishing thread reads its own column two rows
-//    back from the same buffers, so one __syncthreads per row suffices and no
-//    level history lives in registers.
+//    back from the same buffers, so one __syncthreads per row suffices.
 //  - The Jacobian diagonal is recomputed from u0 where it is needed.
 //  - Isotropic lattices (cx == cy, all BASELINE configs) evaluate the unit
-//    stencil and fold c into pre-scaled coefficients (SweepConsts::Es, gs, hls).
+//    stencil and fold c into pre-scaled coefficients (SweepConsts::Es, gs, hls);
+//    the default scheme's tables are compile-time immediates (defscheme.inc).
 //  - The first sweep of a step (U = (u0,u0,u0)) uses the closed form
 //    Phi_i = -h c_i f(u0), c_i = sum_j E[i][j].
-//  - The iteration loop is unrolled by 3 so register-window slots are static.
-// HBM traffic per sweep: 120 B/site (72 B/site for the first sweep).
+//  - The later-sweep loop is unrolled by 3 so register-window slots are static.
+// HBM traffic per sweep: 120 B/site (72 B/site for the first sweep, 88 for a
+// U3-only final sweep).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
