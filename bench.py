@@ -642,6 +642,7 @@ def main():
         if rank != 0:
             return 0
         res = run_reference(args, Dist(1, 0, 0))
+        res["n_gpus"] = world  # the launch's N (the CPU path itself runs on rank 0's host cores)
         print(json.dumps(res))
         return 0
     d = Dist(world, rank, local)
