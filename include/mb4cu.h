@@ -5,7 +5,7 @@
  * (/root/reference/proj/include/nls2d/mb4_integrator.hpp:107-110 `mb4_step`,
  *  integrators.hpp:51 `StepDriver::advance`, lattice.hpp:88 `observables`).
  * The reference has no FFI layer; its boundary is the C++ API in
- * proj/include/nls2d.  The C++ mirror of that API (include/nls2d/*.hpp) calls
+ * proj/include/nls2d.  The C++ mirror of that API (the headers in include/nls2d/) calls
  * these entry points, and so do the Python tests (ctypes) and bench.py.
  *
  * Conventions
