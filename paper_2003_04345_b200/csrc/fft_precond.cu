@@ -32,7 +32,8 @@ __device__ __forceinline__ double mode_mu(int kx, int ky, int nx, int ny, double
 
 // one stage: y_k *= 1 / ((1 + i sigma (mu_k + s)) N)
 __global__ void __launch_bounds__(kT) scale1_kernel(double2* __restrict__ y, int nx, int ny, double cx, double cy,
-                                                    double shift, double sigma) {
+                                                    double shift_arg, double sigma, const double* __restrict__ shift_dev) {
+    const double shift = shift_dev ? *shift_dev : shift_arg;  // device copy: graph-invariant
     const size_t n = static_cast<size_t>(nx) * ny;
     const double inv_n = 1.0 / static_cast<double>(n);
     for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
@@ -120,8 +121,8 @@ cudaError_t launch_fft_shift_partials(const double2* u0, const double* V, size_t
 }
 
 cudaError_t launch_fft_scale1(double2* y, int nx, int ny, double cx, double cy, double shift, double sigma,
-                              cudaStream_t s) {
-    scale1_kernel<<<pblocks(static_cast<size_t>(nx) * ny), kT, 0, s>>>(y, nx, ny, cx, cy, shift, sigma);
+                              cudaStream_t s, const double* shift_dev) {
+    scale1_kernel<<<pblocks(static_cast<size_t>(nx) * ny), kT, 0, s>>>(y, nx, ny, cx, cy, shift, sigma, shift_dev);
     return cudaGetLastError();
 }
 

@@ -228,12 +228,16 @@ int blocks(size_t n) {
 // hcol[i] = h_ij (both passes), hcol[j+1] = ||w||, v_{j+1} = w / ||w||.  Dot
 // products are block partials summed by block 0 in a fixed order (bit-
 // reproducible; the same grid as the other Krylov kernels).
-__global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, double2* const* __restrict__ v, int j,
+__global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, double2* const* __restrict__ v, int j_arg,
                                                      size_t n, double* __restrict__ partial,
-                                                     double* __restrict__ hbuf, double* __restrict__ hcol) {
+                                                     double* __restrict__ hbuf, double* __restrict__ hcol,
+                                                     int* __restrict__ jdev) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     const int G = gridDim.x;
+    // jdev != nullptr: the step index lives in device memory and advances here, so one
+    // captured graph serves every step of a cycle (kr_gmres_stages)
+    const int j = jdev ? *jdev : j_arg;
     for (int pass = 0; pass < 2; ++pass) {
         for (int i = 0; i <= j; ++i) {
             const double2* vi = v[i];
@@ -288,6 +292,14 @@ __global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, do
             vn[k] = make_double2(inv * a.x, inv * a.y);
         }
     }
+    if (jdev && blockIdx.x == 0 && threadIdx.x == 0) *jdev = j + 1;  // every block read *jdev before the syncs
+}
+
+// y = v[*jdev] (the basis vector of the current Arnoldi step, index in device memory)
+__global__ void gather_basis_kernel(double2* __restrict__ y, double2* const* __restrict__ v, const int* __restrict__ jdev,
+                                    size_t n) {
+    const double2* src = v[*jdev];
+    GRID_LOOP(k, n) y[k] = src[k];
 }
 
 }  // namespace
@@ -309,10 +321,15 @@ int arnoldi_grid(size_t n) {
 }
 
 cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,
-                       double* hcol, cudaStream_t s) {
+                       double* hcol, cudaStream_t s, int* jdev) {
     const int g = arnoldi_grid(n);
-    void* args[] = {&w, const_cast<double2***>(&v_dev), &j, &n, &partial, &hbuf, &hcol};
+    void* args[] = {&w, const_cast<double2***>(&v_dev), &j, &n, &partial, &hbuf, &hcol, &jdev};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(g), dim3(kT), args, 0, s);
+}
+
+cudaError_t kr_gather_basis(double2* y, double2* const* v_dev, const int* jdev, size_t n, cudaStream_t s) {
+    gather_basis_kernel<<<blocks(n), kT, 0, s>>>(y, v_dev, jdev, n);
+    return cudaGetLastError();
 }
 
 int krylov_blocks(size_t n) { return blocks(n); }

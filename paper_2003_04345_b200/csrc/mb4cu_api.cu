@@ -87,6 +87,8 @@ struct mb4cu_ctx {
         double* partial = nullptr;         // shift partial sums [blocks][2]
         double* h_partial = nullptr;
         double shift = 0.0;                // mean(V) - 2 gamma mean(|u0|^2) of the current u0
+        double* shift_dev = nullptr;       // its device copy (read by graph-captured steps)
+        double* h_shift = nullptr;         // pinned staging
     } fft;
     // The three decoupled stage solves of a Newton-Krylov iteration in flight at once
     // (the paper's stage parallelism, on one GPU): one stream, Krylov basis, FFT plan and
@@ -106,6 +108,17 @@ struct mb4cu_ctx {
         cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
         cufftHandle plan[3] = {0, 0, 0};
         bool ready = false;
+        // one Arnoldi step of system q as a CUDA graph (gather v_j, preconditioner, matvec,
+        // CGS2, Hessenberg column to the host), j in device memory (jd[q]); captured once per
+        // (u0, h, shift) and relaunched for every step of every cycle
+        int* jd = nullptr;
+        struct Slot {
+            const void* u0 = nullptr;  // the Newton-Krylov commit alternates u0 between two buffers
+            double h = 0.0;
+            cudaGraphExec_t g[3] = {nullptr, nullptr, nullptr};
+        } slot[2];
+        int next_slot = 0;
+        bool use_graphs = true;
     } krb;
     bool profiling = false;
     mb4cu_profile prof{};
@@ -603,6 +616,13 @@ int fft_prepare(mb4cu_ctx* ctx, int stages) {
     }
     const double n = static_cast<double>(ctx->n);
     f.shift = sv / n - 2.0 * ctx->gamma * (su / n);
+    if (!f.shift_dev) {
+        MB4_CUDA(ctx, cudaMalloc(&f.shift_dev, sizeof(double)));
+        MB4_CUDA(ctx, cudaMallocHost(&f.h_shift, sizeof(double)));
+    }
+    *f.h_shift = f.shift;
+    MB4_CUDA(ctx, cudaMemcpyAsync(f.shift_dev, f.h_shift, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // the pinned staging is reused
     return MB4CU_OK;
 }
 
@@ -667,6 +687,15 @@ void krb_free(mb4cu_ctx* ctx) {
         if (e) cudaEventDestroy(e);
         e = nullptr;
     }
+    for (auto& sl : B.slot) {
+        for (auto& g : sl.g) {
+            if (g) cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+        sl.u0 = nullptr;
+    }
+    cudaFree(B.jd);
+    B.jd = nullptr;
     cudaFree(B.mem);
     B.mem = nullptr;
     B.ready = false;
@@ -709,6 +738,7 @@ int krb_alloc(mb4cu_ctx* ctx, size_t len) {
         }
     }
     for (auto& e : B.ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaMalloc(&B.jd, 3 * sizeof(int)) == cudaSuccess;
     if (!ok) {
         krb_free(ctx);
         cudaGetLastError();
@@ -753,6 +783,58 @@ int kr_gmres_stages_impl(mb4cu_ctx* ctx, const SweepConsts& c, const double2* co
         ctx->prof.other_launches += 3;
         return MB4CU_OK;
     };
+    // one Arnoldi step of system q on its stream (the body of the captured graph)
+    auto arnoldi_step = [&](int q) -> int {
+        MB4_CUDA(ctx, mb4cu::kr_gather_basis(T(q), B.v_dev[q], B.jd + q, n, B.st[q]));
+        auto* z = reinterpret_cast<cufftDoubleComplex*>(T(q));
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, mb4cu::launch_fft_scale1(T(q), ctx->nx, ctx->ny, ctx->cx, ctx->cy, f.shift, c.hlam[q], B.st[q],
+                                               f.shift_dev));
+        if (cufftExecZ2Z(B.plan[q], z, z, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(ctx, MB4CU_CUDA_ERROR, "cufft");
+        MB4_CUDA(ctx, mb4cu::kr_matvec(T(q), W(q), ctx->u0, ctx->V, ctx->nx, ctx->ny, c.hlam[q], c, B.st[q]));
+        MB4_CUDA(ctx, mb4cu::kr_arnoldi(W(q), B.v_dev[q], 0, n, B.partial[q], B.coef[q], B.hcol[q], B.st[q],
+                                        B.jd + q));
+        MB4_CUDA(ctx, cudaMemcpyAsync(B.h_hcol[q], B.hcol[q], sizeof(double) * (m + 2), cudaMemcpyDeviceToHost,
+                                      B.st[q]));
+        return MB4CU_OK;
+    };
+    // the three step graphs for this (u0, h): cached in two slots (the commit alternates u0
+    // between two buffers; the preconditioner shift is read from device memory)
+    cudaGraphExec_t* gx = nullptr;
+    if (B.use_graphs) {
+        for (auto& sl : B.slot)
+            if (sl.u0 == ctx->u0 && sl.h == c.h && sl.g[0]) gx = sl.g;
+        if (!gx) {
+            auto& sl = B.slot[B.next_slot];
+            B.next_slot ^= 1;
+            for (auto& g : sl.g) {
+                if (g) cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
+            sl.u0 = nullptr;
+            bool ok = true;
+            for (int q = 0; q < 3 && ok; ++q) {
+                cudaGraph_t graph = nullptr;
+                ok = cudaStreamBeginCapture(B.st[q], cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                const int rc = ok ? arnoldi_step(q) : MB4CU_CUDA_ERROR;
+                ok = cudaStreamEndCapture(B.st[q], &graph) == cudaSuccess && ok && rc == MB4CU_OK;
+                ok = ok && cudaGraphInstantiate(&sl.g[q], graph, 0) == cudaSuccess;
+                if (graph) cudaGraphDestroy(graph);
+            }
+            if (ok) {
+                sl.u0 = ctx->u0;
+                sl.h = c.h;
+                gx = sl.g;
+            } else {  // capture unsupported here: launch the steps one by one
+                cudaGetLastError();
+                for (auto& g : sl.g) {
+                    if (g) cudaGraphExecDestroy(g);
+                    g = nullptr;
+                }
+                B.use_graphs = false;
+            }
+        }
+    }
     auto fetch_sum = [&](int q, int nv, double* out) {
         for (int i = 0; i < nv; ++i) {
             double sum = 0.0;
@@ -828,6 +910,7 @@ int kr_gmres_stages_impl(mb4cu_ctx* ctx, const SweepConsts& c, const double2* co
                 continue;
             }
             MB4_CUDA(ctx, mb4cu::kr_scale(V(q, 0), V(q, 0), 1.0 / beta[q], n, B.st[q]));
+            MB4_CUDA(ctx, cudaMemsetAsync(B.jd + q, 0, sizeof(int), B.st[q]));  // step index of the cycle
             std::fill(g[q].begin(), g[q].end(), 0.0);
             g[q][0] = beta[q];
             j[q] = 0;
@@ -839,11 +922,12 @@ int kr_gmres_stages_impl(mb4cu_ctx* ctx, const SweepConsts& c, const double2* co
             for (int q = 0; q < 3; ++q) {
                 if (!inner[q]) continue;
                 anyin = step[q] = true;
-                if (int rc = mv(q, V(q, j[q]), W(q))) return rc;
-                MB4_CUDA(ctx, mb4cu::kr_arnoldi(W(q), B.v_dev[q], j[q], n, B.partial[q], B.coef[q], B.hcol[q],
-                                                B.st[q]));
-                MB4_CUDA(ctx, cudaMemcpyAsync(B.h_hcol[q], B.hcol[q], sizeof(double) * (j[q] + 2),
-                                              cudaMemcpyDeviceToHost, B.st[q]));
+                if (gx) {
+                    MB4_CUDA(ctx, cudaGraphLaunch(gx[q], B.st[q]));
+                    ctx->prof.other_launches += 6;
+                } else if (int rc = arnoldi_step(q)) {
+                    return rc;
+                }
             }
             if (!anyin) break;
             if (int rc = sync_all(step)) return rc;
@@ -1232,6 +1316,8 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     if (ctx->fft.have2) cufftDestroy(ctx->fft.plan2);
     cudaFree(ctx->fft.partial);
     cudaFreeHost(ctx->fft.h_partial);
+    cudaFree(ctx->fft.shift_dev);
+    cudaFreeHost(ctx->fft.h_shift);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->pev0) cudaEventDestroy(ctx->pev0);

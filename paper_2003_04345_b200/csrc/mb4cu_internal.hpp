@@ -185,14 +185,17 @@ void avf4_coupling(double mt[2][2]);
 // (j+1) * arnoldi_grid(n) doubles, hbuf j+1, hcol j+2 (device)
 int arnoldi_grid(size_t n);
 cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,
-                       double* hcol, cudaStream_t s);
+                       double* hcol, cudaStream_t s, int* jdev = nullptr);
+// y = v[*jdev] (device-indexed basis vector, for graph-captured Arnoldi steps)
+cudaError_t kr_gather_basis(double2* y, double2* const* v_dev, const int* jdev, size_t n, cudaStream_t s);
 
 // Fourier preconditioner of the Krylov solves (fft_precond.cu)
 int fft_shift_blocks(size_t n);
 cudaError_t launch_fft_shift_partials(const double2* u0, const double* V, size_t n, double* partial,
                                       cudaStream_t s);
 cudaError_t launch_fft_scale1(double2* y, int nx, int ny, double cx, double cy, double shift, double sigma,
-                              cudaStream_t s);
+                              cudaStream_t s,
+                              const double* shift_dev = nullptr);
 cudaError_t launch_fft_scale2(double2* y0, double2* y1, int nx, int ny, double cx, double cy, double shift,
                               double h, const double C[2][2], cudaStream_t s);
 
