@@ -78,6 +78,11 @@
 #ifndef MB4_NT_FIRST
 #define MB4_NT_FIRST 128
 #endif
+// band-rows per CTA at least (small lattices): 1 = no idle CTAs; larger values trade CTAs
+// for rows marched in sequence (measured slower at 32: the row march is latency-bound)
+#ifndef MB4_MIN_ROWS_PER_CTA
+#define MB4_MIN_ROWS_PER_CTA 1
+#endif
 // later sweeps: the own-column cubic term of a row before the row barrier (measured
 // equal or slower: the later sweeps are FP64-bound, not barrier-bound)
 #ifndef MB4_CUBIC_EARLY
@@ -1303,7 +1308,18 @@ struct Launcher3 {
         return g;
     }
 
-    static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
+    // output columns per band of this launch's sweeps (the smaller one if it runs both kinds)
+    static constexpr int TX_FIRST = MF >= 3 && MF <= 7 && MB4_FIRST_V2
+                                        ? MarchFirst2<(MF >= 3 && MF <= 7 ? MF : 3), NT, true, false>::TX
+                                    : MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::TX
+                                              : Geom3<0, NT>::TX;
+    static constexpr int TX_LATER = Geom3<M, NT>::TX;
+    static constexpr int TXK = PH == 2 ? TX_LATER : PH == 0 && TX_LATER < TX_FIRST ? TX_LATER : TX_FIRST;
+    static constexpr long long kMinRowsPerCta = MB4_MIN_ROWS_PER_CTA;
+
+    // CTAs of a launch: the co-resident grid, capped by grid_cap and, for small lattices, by
+    // the band-rows to march (no CTAs that only take part in the grid barriers)
+    static int launch_grid(const StepArgs& a, int device) {
         int grid = grid_size(device);
         if (a.grid_cap > 0 && a.grid_cap < grid) {
             grid = a.grid_cap;
@@ -1313,6 +1329,19 @@ struct Launcher3 {
             const int keep = sms + a.grid_cap > 0 ? sms + a.grid_cap : 1;
             grid = sms > 0 ? grid / sms * keep : grid;
         }
+        long long total = 0;  // band-rows, as for_segments counts them
+        const int nr = a.nrect > 0 ? a.nrect : 1;
+        for (int r = 0; r < nr; ++r) {
+            const long long w = a.nrect > 0 ? a.rect[r][2] : a.nx, h = a.nrect > 0 ? a.rect[r][3] : a.ny;
+            total += (w + TXK - 1) / TXK * h;
+        }
+        const long long want = (total + kMinRowsPerCta - 1) / kMinRowsPerCta;
+        if (want < grid) grid = want > 0 ? static_cast<int>(want) : 1;
+        return grid;
+    }
+
+    static cudaError_t launch(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
+        const int grid = launch_grid(a, device);
         if (grid <= 0) return cudaErrorLaunchOutOfResources;
         void* params[] = {&a, const_cast<SweepConsts*>(&c)};
         return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mb4_step3_kernel<MF, M, NT, ISO, GHOST, DEF, PH>),
@@ -1323,8 +1352,7 @@ struct Launcher3 {
 // the split pair: first sweep (PH 1), then the later sweeps (PH 2) on the same stream
 template <int MF, int M, int NT, bool ISO, bool DEF>
 cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
-    a.obs_blocks = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::grid_size(device);
-    if (a.grid_cap > 0 && a.grid_cap < a.obs_blocks) a.obs_blocks = a.grid_cap;
+    a.obs_blocks = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::launch_grid(a, device);
     const cudaError_t e = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::launch(a, c, device, s);
     if (e != cudaSuccess) return e;
     return Launcher3<MF, M, MB4_NT_LATER, ISO, false, DEF, 2>::launch(a, c, device, s);
