@@ -497,7 +497,7 @@ def run_dist(args, d: Dist):
     be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
                        overlap=not args.no_overlap, reserve_sms=2 if d.world > 1 else 0)
     be.set_state(pb)
-    sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon)
+    sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon, adaptive_m=args.neumann < 0)
     obs_w, _ = sess.run(cfg.dt, args.warmup) if args.warmup > 0 else (None, None)
     H0 = obs_w[0, 3] if obs_w is not None else sess.observables()[3]
     be.profile(True)
@@ -530,7 +530,8 @@ def run_dist(args, d: Dist):
         "data": "synthetic (seeded defects + Gaussian packets, configs.py)",
         "config": {"workload": f"{args.config} {'weak' if weak else 'strong'} scaling: {gnx}x{gny} lattice, "
                                f"{dec.lnx}x{dec.lny} sites per GPU, dt={cfg.dt}, g={cfg.g}, eps={cfg.epsilon}",
-                   "lattice": [gnx, gny], "sites_per_gpu": n_local, "neumann_terms": m,
+                   "lattice": [gnx, gny], "sites_per_gpu": n_local,
+                   "neumann_terms": m if args.neumann >= 0 else "adaptive 1..2",
                    "process_grid": [px, py], "parallelism": f"2-D domain decomposition {px}x{py}",
                    "halo_exchange": ("between sweeps" if args.no_overlap else
                                      "overlapped: boundary frame swept first, its NCCL exchange on a side "

@@ -177,6 +177,10 @@ int mb4cu_set_stream(mb4cu_ctx* ctx, void* cuda_stream);
  * mb4cu_spectral_bound and pass the result to mb4cu_set_spectral_bound (0 restores
  * the context's own bound). */
 int mb4cu_spectral_bound(mb4cu_ctx* ctx, double* rho);
+/* Neumann depth m of the later sweeps from now on (production kernel; m + 1 <= ghost for a
+ * sub-domain context).  A decomposed lattice applies the single-domain adaptive policy
+ * (m = 2 once a step needs >= 4 sweeps at m = 1, back to 1 after 64 steps) through it. */
+int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m);
 int mb4cu_set_spectral_bound(mb4cu_ctx* ctx, double rho);
 
 /* ---- Sub-domain (multi-GPU) stepping, ghost > 0 ---------------------------------

@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
         "mb4cu_set_stream": (I, [P, P]),
         "mb4cu_spectral_bound": (I, [P, DP]),
         "mb4cu_set_spectral_bound": (I, [P, D]),
+        "mb4cu_set_neumann_terms": (I, [P, I]),
         "mb4cu_apply_kv": (I, [P, DP, DP]),
         "mb4cu_rhs": (I, [P, DP, DP]),
         "mb4cu_eval_phi": (I, [P, DP, DP, DP, DP, D, DP, DP, DP]),
@@ -183,7 +184,7 @@ EXPORTED = [
     "mb4cu_create_error", "mb4cu_set_state", "mb4cu_get_state", "mb4cu_set_state_device",
     "mb4cu_get_state_device", "mb4cu_step", "mb4cu_run", "mb4cu_method_step", "mb4cu_method_run",
     "mb4cu_observables",
-    "mb4cu_set_stream", "mb4cu_spectral_bound", "mb4cu_set_spectral_bound", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
+    "mb4cu_set_stream", "mb4cu_spectral_bound", "mb4cu_set_spectral_bound", "mb4cu_set_neumann_terms", "mb4cu_apply_kv", "mb4cu_rhs", "mb4cu_eval_phi",
     "mb4cu_make_inputs", "mb4cu_scale_state", "mb4cu_version", "mb4cu_profile_enable",
     "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",
     "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_sweep_region", "mb4cu_commit_step", "mb4cu_observables_sums",

@@ -1329,6 +1329,17 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
 
 const char* mb4cu_last_error(const mb4cu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m) {
+    if (!ctx) return MB4CU_INVALID;
+    if (ctx->kernel != 0 || m < 0 || m > 2 || !mb4cu::march2_supported(ctx->mf, m) ||
+        (ctx->ghost > 0 && m + 1 > ctx->ghost))
+        return fail(ctx, MB4CU_INVALID, "set_neumann_terms: production kernel, m in 0..2 with a compiled "
+                                        "(neumann_first, m) pair and m + 1 <= ghost");
+    ctx->m = m;
+    ctx->m_auto = false;  // the caller drives the depth from now on
+    return MB4CU_OK;
+}
+
 int mb4cu_spectral_bound(mb4cu_ctx* ctx, double* rho) {
     if (!ctx || !rho) return fail(ctx, MB4CU_INVALID, "spectral_bound: null argument");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));

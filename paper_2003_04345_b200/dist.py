@@ -223,8 +223,13 @@ class DistributedSession:
     """MB4 stepping on one rank's block, collectives over torch.distributed."""
 
     def __init__(self, dec: Decomposition, backend, comm: Comm, gamma: float, cx: float, cy: float,
-                 epsilon: float, max_iters: int = 50, max_step_halvings: int = 4):
+                 epsilon: float, max_iters: int = 50, max_step_halvings: int = 4, adaptive_m: bool = False):
+        """adaptive_m: the later-sweep depth follows the single-domain policy (the library's
+        adapt_neumann): m = 2 once a sub-step needs >= 4 sweeps at m = 1, back to m = 1
+        after 64 sub-steps -- decided from sweep counts only, so every rank agrees."""
         self.dec, self.b, self.comm = dec, backend, comm
+        self.adaptive_m = adaptive_m
+        self._m_steps = 0
         self.gamma, self.cx, self.cy = gamma, cx, cy
         self.eps, self.max_iters, self.max_halvings = epsilon, max_iters, max_step_halvings
         self.halo = HaloExchange(dec, backend, comm)
@@ -363,6 +368,22 @@ class DistributedSession:
                 launched = s + 1
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
 
+    def _adapt_m(self, sweeps: int) -> None:
+        if not self.adaptive_m:
+            return
+        m = self.b.neumann_terms()
+        if m == 1 and sweeps >= 4:
+            self.b.set_neumann_terms(2)
+        elif m == 2:
+            self._m_steps += 1
+            if self._m_steps < 64:
+                return
+            self.b.set_neumann_terms(1)
+        else:
+            return
+        self._m_steps = 0
+        self._guess = 0  # as the library: no speculative final sweep right after a switch
+
     def sync_spectral_bound(self) -> None:
         """After a state was set: all ranks place the first sweep's Chebyshev polynomial
         on one interval, the max of the ranks' bounds (mb4cu_spectral_bound), which
@@ -390,6 +411,7 @@ class DistributedSession:
                 for _ in range(sub):
                     n, _ = self._substep(h / sub)
                     total += n
+                    self._adapt_m(n)
                 self.last_sweeps = total
                 return total, hv
             except NonConvergence as e:
@@ -430,6 +452,7 @@ class CudaBackend:
         p.V = _lib.dptr(self._v)
         p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, 0
         p.neumann_terms = neumann_terms
+        self.m = neumann_terms
         p.neumann_first = neumann_first
         p.first_poly = 0
         p.device = device
@@ -568,6 +591,13 @@ class CudaBackend:
         u = np.ascontiguousarray(u_block, dtype=np.complex128)
         self._chk(self.L.mb4cu_set_state(self.ctx, _lib.dptr(u)))
         self.bound_dirty = True
+
+    def neumann_terms(self) -> int:
+        return self.m
+
+    def set_neumann_terms(self, m: int) -> None:
+        self._chk(self.L.mb4cu_set_neumann_terms(self.ctx, m))
+        self.m = m
 
     def spectral_bound(self) -> float:
         rho = C.c_double(0.0)

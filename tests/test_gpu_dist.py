@@ -76,7 +76,7 @@ class LoopbackComm:
         self.h.bar.wait()
 
 
-def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None, reserve_sms=0):
+def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None, reserve_sms=0, adaptive_m=False):
     cfg = configs.CONFIGS[name]
     V, psi = configs.make_inputs(cfg)
     world = px * py
@@ -91,7 +91,8 @@ def _run_decomposed(name, px, py, m, nsteps, overlap=False, hs=None, reserve_sms
             be = D.CudaBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon,
                                cfg.max_iters, m, 0, overlap=overlap, reserve_sms=reserve_sms)
             be.set_state(dec.block(psi))
-            sess = D.DistributedSession(dec, be, LoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon)
+            sess = D.DistributedSession(dec, be, LoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon,
+                                        adaptive_m=adaptive_m)
             if hs is None:
                 obs, sweeps = sess.run(cfg.dt, nsteps)
             else:
@@ -213,3 +214,21 @@ def test_stage_split_matches_single_context_newton_krylov(world):
     for u, got_its in out:
         assert got_its == its
         assert np.array_equal(u, ref)
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_adaptive_depth_matches_single_domain(overlap):
+    """DistributedSession(adaptive_m=True) applies the library's adaptive later-sweep depth
+    (m = 2 once a step needs >= 4 sweeps at m = 1): the decomposed cfg1 run switches where the
+    single-domain default does and reproduces it bit for bit."""
+    name, nsteps = "cfg1", 4
+    cfg = configs.CONFIGS[name]
+    u_dec, _, sweeps_dec = _run_decomposed(name, 2, 2, 1, nsteps, overlap=overlap, adaptive_m=True)
+    V, psi = configs.make_inputs(cfg)
+    with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg)) as s:
+        s.set_state(psi)
+        _, sweeps = s.run(cfg.dt, nsteps)
+        u = s.get_state()
+    assert sweeps[0] >= 4  # the switch happens
+    assert list(sweeps_dec) == list(sweeps)
+    assert np.array_equal(u_dec, u), np.abs(u_dec - u).max()
