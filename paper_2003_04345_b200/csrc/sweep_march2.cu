@@ -1142,20 +1142,31 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
 // 2 = the later sweeps, continuing from a PH = 1 launch (its residual in rmax[0]);
 // 3 = the first sweep as a one-sweep launch with its status (sub-domain sweeps).
 // (PH 1 is kept free of the status path: a runtime switch costs it registers.)
+// the first sweep's kernel geometry (instantiated only where a first sweep runs)
+template <int MF, int NT>
+constexpr size_t first_sweep_bytes() {
+    if constexpr (MF >= 3 && MF <= 7 && MB4_FIRST_V2) return MarchFirst2<MF, NT, true, false>::bytes;
+    else if constexpr (MF >= 1) return MarchFirst<MF, NT, true, false>::bytes;
+    else return Geom3<0, NT>::bytes;
+}
+template <int MF, int NT>
+constexpr int first_sweep_tx() {
+    if constexpr (MF >= 3 && MF <= 7 && MB4_FIRST_V2) return MarchFirst2<MF, NT, true, false>::TX;
+    else if constexpr (MF >= 1) return MarchFirst<MF, NT, true, false>::TX;
+    else return Geom3<0, NT>::TX;
+}
+
 template <int MF, int M, int NT, int PH = 0>
 struct KGeom {
     // the first sweep runs MarchFirst (MF >= 1) or March3<0>; later sweeps March3<M>
-    static constexpr size_t first_bytes =
-        MF >= 3 && MF <= 7 && MB4_FIRST_V2 ? MarchFirst2<(MF >= 3 && MF <= 7 ? MF : 3), NT, true, false>::bytes
-        : MF >= 1                         ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::bytes
-                                          : Geom3<0, NT>::bytes;
+    static constexpr size_t first_bytes = PH == 2 ? 0 : first_sweep_bytes<MF, (PH == 2 ? 128 : NT)>();
     static constexpr size_t later_bytes = Geom3<M, NT>::bytes;
     static constexpr size_t bytes = PH == 1 || PH == 3 ? first_bytes
                                     : PH == 2 ? later_bytes
                                               : (first_bytes > later_bytes ? first_bytes : later_bytes);
     static constexpr int MINB = NT >= 256 ? 1
                                 : PH == 1 || PH == 3 ? 2
-                                : PH == 2 ? (M <= 1 ? MB4_MINB_LATER : 2) * (128 / NT)
+                                : PH == 2 ? (NT > 128 ? (M <= 1 ? 2 : 1) : (M <= 1 ? MB4_MINB_LATER : 2) * (128 / NT))
                                           : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
@@ -1218,7 +1229,8 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         unsigned rmax = 0u;
         if (PH == 1 || PH == 3 || (PH == 0 && sg == 0)) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
-            sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
+            if constexpr (PH != 2)  // (not instantiated for the later-sweep kernel)
+                sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
                 __shared__ double red[kObsFields][NT / 32];
 #pragma unroll
@@ -1309,10 +1321,7 @@ struct Launcher3 {
     }
 
     // output columns per band of this launch's sweeps (the smaller one if it runs both kinds)
-    static constexpr int TX_FIRST = MF >= 3 && MF <= 7 && MB4_FIRST_V2
-                                        ? MarchFirst2<(MF >= 3 && MF <= 7 ? MF : 3), NT, true, false>::TX
-                                    : MF >= 1 ? MarchFirst<(MF >= 1 ? MF : 1), NT, true, false>::TX
-                                              : Geom3<0, NT>::TX;
+    static constexpr int TX_FIRST = first_sweep_tx<MF, (PH == 2 ? 128 : NT)>();
     static constexpr int TX_LATER = Geom3<M, NT>::TX;
     static constexpr int TXK = PH == 2 ? TX_LATER : PH == 0 && TX_LATER < TX_FIRST ? TX_LATER : TX_FIRST;
     static constexpr long long kMinRowsPerCta = MB4_MIN_ROWS_PER_CTA;
