@@ -14,7 +14,7 @@ V, psi = configs.make_inputs(cfg)
 model = configs.model_for(cfg, V)
 newton = configs.newton_for(cfg)
 for kw in ({}, {"neumann_terms": 1, "neumann_first": 2}, {"neumann_terms": 2, "neumann_first": 6},
-           {"kernel": 1}, {"kernel": 3}):
+           {"neumann_terms": 1, "neumann_first": 5, "first_poly": 1}, {"kernel": 1}, {"kernel": 3}):
     with nls2d.Session(model, nls2d.Mb4Scheme(), newton, **kw) as s:
         s.set_state(psi)
         for h in (cfg.dt, 2 * cfg.dt, cfg.dt):
