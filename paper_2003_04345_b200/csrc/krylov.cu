@@ -223,6 +223,8 @@ int blocks(size_t n) {
     return static_cast<int>(b < 148 * 4 ? (b ? b : 1) : 148 * 4);
 }
 
+constexpr int kMaxDots = 32;  // >= the GMRES restart length + 1 (mb4cu_api.cu kKrylovRestart = 30)
+
 // One Arnoldi step after w = A v_j, in ONE cooperative launch (grid barriers
 // instead of host round trips): classical Gram-Schmidt twice against v_0..v_j,
 // hcol[i] = h_ij (both passes), hcol[j+1] = ||w||, v_{j+1} = w / ||w||.  Dot
@@ -239,15 +241,48 @@ __global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, do
     // captured graph serves every step of a cycle (kr_gmres_stages)
     const int j = jdev ? *jdev : j_arg;
     for (int pass = 0; pass < 2; ++pass) {
-        for (int i = 0; i <= j; ++i) {
-            const double2* vi = v[i];
-            double acc = 0.0;
+        if (j < kMaxDots) {
+            // all j + 1 dot products in one sweep over the sites and ONE block reduction (the
+            // per-dot block reductions dominate on small lattices); per-thread, warp and
+            // block sums in the same order as the one-dot-at-a-time loop below: bit-identical
+            __shared__ double red[kT / 32][kMaxDots];
+            double acc[kMaxDots];
+#pragma unroll
+            for (int i = 0; i < kMaxDots; ++i) acc[i] = 0.0;
             GRID_LOOP(k, n) {
-                const double2 a = w[k], b = vi[k];
-                acc = fma(a.x, b.x, fma(a.y, b.y, acc));
+                const double2 a = w[k];
+#pragma unroll
+                for (int i = 0; i < kMaxDots; ++i)
+                    if (i <= j) {
+                        const double2 b = v[i][k];
+                        acc[i] = fma(a.x, b.x, fma(a.y, b.y, acc[i]));
+                    }
             }
-            const double sblk = block_sum(acc);
-            if (threadIdx.x == 0) partial[static_cast<size_t>(i) * G + blockIdx.x] = sblk;
+#pragma unroll
+            for (int i = 0; i < kMaxDots; ++i)
+                if (i <= j) {
+                    double t = acc[i];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = t;
+                }
+            __syncthreads();
+            for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+                double t = 0.0;
+                for (int q = 0; q < kT / 32; ++q) t += red[q][i];
+                partial[static_cast<size_t>(i) * G + blockIdx.x] = t;
+            }
+        } else {
+            for (int i = 0; i <= j; ++i) {
+                const double2* vi = v[i];
+                double acc = 0.0;
+                GRID_LOOP(k, n) {
+                    const double2 a = w[k], b = vi[k];
+                    acc = fma(a.x, b.x, fma(a.y, b.y, acc));
+                }
+                const double sblk = block_sum(acc);
+                if (threadIdx.x == 0) partial[static_cast<size_t>(i) * G + blockIdx.x] = sblk;
+            }
         }
         grid.sync();
         if (blockIdx.x == 0) {
