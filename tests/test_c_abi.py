@@ -138,3 +138,6 @@ def test_abi_null_and_range_checks_without_a_gpu():
     assert L.mb4cu_spectral_bound(None, None) == _lib.MB4CU_INVALID
     assert L.mb4cu_set_spectral_bound(None, 1.0) == _lib.MB4CU_INVALID
     assert L.mb4cu_step(None, 0.01, None) == _lib.MB4CU_INVALID
+    assert L.mb4cu_set_neumann_terms(None, 1) == _lib.MB4CU_INVALID
+    assert L.mb4cu_ns_begin(None, 0.01) == _lib.MB4CU_INVALID
+    assert L.mb4cu_ns_commit(None) == _lib.MB4CU_INVALID

@@ -232,3 +232,24 @@ def test_adaptive_depth_matches_single_domain(overlap):
     assert sweeps[0] >= 4  # the switch happens
     assert list(sweeps_dec) == list(sweeps)
     assert np.array_equal(u_dec, u), np.abs(u_dec - u).max()
+
+
+def test_set_neumann_terms_validation():
+    """mb4cu_set_neumann_terms accepts the compiled (neumann_first, m) pairs within the ghost
+    width and rejects the rest; the stage-split entry points refuse to run without ns_begin."""
+    import ctypes as C
+
+    from paper_2003_04345_b200 import _lib
+
+    cfg = configs.CONFIGS["cfg1"]
+    V, psi = configs.make_inputs(cfg)
+    L = _lib.lib()
+    with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg)) as s:
+        assert L.mb4cu_set_neumann_terms(s._ctx, 2) == 0
+        assert L.mb4cu_set_neumann_terms(s._ctx, 3) == _lib.MB4CU_INVALID
+        assert L.mb4cu_set_neumann_terms(s._ctx, -1) == _lib.MB4CU_INVALID
+        r = C.c_double(0.0)
+        assert L.mb4cu_ns_update(s._ctx, C.byref(r)) == _lib.MB4CU_INVALID
+        assert L.mb4cu_ns_solve(s._ctx, 0) == _lib.MB4CU_INVALID
+        s.set_state(psi)
+        s.step(cfg.dt)  # still steps normally at the fixed depth
