@@ -67,6 +67,16 @@ typedef struct {
  * ComplexEigenvalueError (small_dense.cpp:100-101,127-128,151-152,171-172). */
 int mb4cu_scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* out);
 
+/* Scheme helpers of the reference API (host arithmetic, no device):
+ *   mb4cu_eval_a             eval_A(alpha1, tau, zeta)          mb4_scheme.hpp:14, mb4_scheme.cpp:66-68
+ *   mb4cu_lagrange_basis     lagrange_basis(nodes, i, zeta)     mb4_scheme.hpp:17, mb4_scheme.cpp:70-80
+ *                            (MB4CU_INVALID: index out of range / coincident nodes)
+ *   mb4cu_scheme_integrate_e Mb4Scheme::integrate_e(alpha1, nodes, points)
+ *                            mb4_scheme.hpp:55-58, mb4_scheme.cpp:141-157; out[i*4+j] = E_{i+1,j} */
+double mb4cu_eval_a(double alpha1, double tau, double zeta);
+int mb4cu_lagrange_basis(const double nodes[4], int i, double zeta, double* out);
+int mb4cu_scheme_integrate_e(double alpha1, const double nodes[4], int points, double out[12]);
+
 /* Problem description (replaces GridModel + NewtonConfig, lattice.hpp:49-73,
  * mb4_integrator.hpp:25-35). */
 typedef struct {
@@ -242,6 +252,11 @@ int mb4cu_ns_get_correction(mb4cu_ctx* ctx, int k, double* dev_out);
 int mb4cu_ns_set_correction(mb4cu_ctx* ctx, int k, const double* dev_in);
 int mb4cu_ns_update(mb4cu_ctx* ctx, double* rmax);
 int mb4cu_ns_commit(mb4cu_ctx* ctx);
+/* The three stage values U_1..U_3 of the open step (host buffers, 2N doubles each):
+ * NewtonResult::stages of newton_solve (mb4_integrator.hpp:85-95). */
+int mb4cu_ns_get_stages(mb4cu_ctx* ctx, double* u1_host, double* u2_host, double* u3_host);
+/* Close an open step without committing (the resident state is unchanged). */
+int mb4cu_ns_abort(mb4cu_ctx* ctx);
 /* Local energy sums of the resident state (ghosts of u0 must be current). */
 int mb4cu_observables_sums(mb4cu_ctx* ctx, double* local_sums5);
 

@@ -3,7 +3,10 @@
 //
 // Declarations follow the reference so existing callers compile unchanged:
 //   GridSpec / GridModel / rhs / observables      lattice.hpp:21-88
-//   Mb4Scheme                                     mb4_scheme.hpp:26-64
+//   split_state / join_state                      lattice.hpp:17-18
+//   SmallMat / Eig3                               small_dense.hpp:11-41
+//   eval_A / lagrange_basis / Mb4Scheme           mb4_scheme.hpp:14-64
+//   StageSystem / NewtonResult / newton_solve     mb4_integrator.hpp:76-95
 //   NewtonConfig / StepStats / NonConvergenceError / eval_phi / mb4_step
 //                                                 mb4_integrator.hpp:17-110
 //   MethodId / StepDriver                         integrators.hpp:11-66
@@ -20,10 +23,15 @@
 #include <array>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
 #include <cctype>
+#include <chrono>
+#include <limits>
+#include <functional>
 #include <memory>
 #include <optional>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -61,6 +69,114 @@ inline void throw_status(int rc, const std::string& text, double residual = 0.0)
     }
 }
 }  // namespace detail
+
+/// Split view [p; q] of a state (lattice.hpp:17-18): real parts, then imaginary parts.
+inline std::vector<double> split_state(const State& u) {
+    const std::size_t n = u.size();
+    std::vector<double> v(2 * n);
+    for (std::size_t k = 0; k < n; ++k) {
+        v[k] = u[k].real();
+        v[n + k] = u[k].imag();
+    }
+    return v;
+}
+inline State join_state(std::span<const double> v) {
+    if (v.size() % 2 != 0) throw std::invalid_argument("join_state: odd length");
+    const std::size_t n = v.size() / 2;
+    State u(n);
+    for (std::size_t k = 0; k < n; ++k) u[k] = Complex(v[k], v[n + k]);
+    return u;
+}
+
+/// Small row-major dense matrix (small_dense.hpp:11-34): the scheme-side 3x3 work.
+class SmallMat {
+public:
+    static constexpr int kMax = 8;
+    SmallMat() = default;
+    SmallMat(int rows, int cols) : rows_(rows), cols_(cols) {
+        if (rows < 0 || cols < 0 || rows > kMax || cols > kMax)
+            throw std::invalid_argument("SmallMat: dimension out of range");
+    }
+    static SmallMat identity(int n) {
+        SmallMat m(n, n);
+        for (int i = 0; i < n; ++i) m(i, i) = 1.0;
+        return m;
+    }
+    int rows() const { return rows_; }
+    int cols() const { return cols_; }
+    double& operator()(int r, int c) { return a_[static_cast<std::size_t>(r) * kMax + c]; }
+    double operator()(int r, int c) const { return a_[static_cast<std::size_t>(r) * kMax + c]; }
+    SmallMat operator*(const SmallMat& b) const {
+        if (cols_ != b.rows_) throw std::invalid_argument("SmallMat: dimension mismatch");
+        SmallMat p(rows_, b.cols_);
+        for (int i = 0; i < rows_; ++i)
+            for (int j = 0; j < b.cols_; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < cols_; ++k) acc += (*this)(i, k) * b(k, j);
+                p(i, j) = acc;
+            }
+        return p;
+    }
+    /// Gauss-Jordan elimination with partial pivoting on an augmented copy.
+    SmallMat inverse() const {
+        if (rows_ != cols_) throw std::invalid_argument("SmallMat: inverse of a non-square matrix");
+        const int n = rows_;
+        SmallMat w = *this, inv = identity(n);
+        for (int c = 0; c < n; ++c) {
+            int piv = c;
+            for (int r = c + 1; r < n; ++r)
+                if (std::abs(w(r, c)) > std::abs(w(piv, c))) piv = r;
+            if (w(piv, c) == 0.0) throw std::runtime_error("SmallMat: singular matrix");
+            for (int k = 0; k < n; ++k) {
+                std::swap(w(c, k), w(piv, k));
+                std::swap(inv(c, k), inv(piv, k));
+            }
+            const double d = w(c, c);
+            for (int k = 0; k < n; ++k) {
+                w(c, k) /= d;
+                inv(c, k) /= d;
+            }
+            for (int r = 0; r < n; ++r) {
+                if (r == c || w(r, c) == 0.0) continue;
+                const double f = w(r, c);
+                for (int k = 0; k < n; ++k) {
+                    w(r, k) -= f * w(c, k);
+                    inv(r, k) -= f * inv(c, k);
+                }
+            }
+        }
+        return inv;
+    }
+    double inf_norm() const {
+        double m = 0.0;
+        for (int i = 0; i < rows_; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < cols_; ++j) s += std::abs((*this)(i, j));
+            m = std::max(m, s);
+        }
+        return m;
+    }
+
+private:
+    int rows_ = 0, cols_ = 0;
+    std::array<double, kMax * kMax> a_{};
+};
+
+struct Eig3 {
+    std::array<double, 3> values{};  // ascending
+    SmallMat t;                      // columns are eigenvectors
+    SmallMat t_inv;
+};
+
+/// A(tau, zeta) of the scheme (mb4_scheme.hpp:14), computed by the library.
+inline double eval_A(double alpha1, double tau, double zeta) { return mb4cu_eval_a(alpha1, tau, zeta); }
+
+/// Cubic Lagrange basis over {0, c1, c2, c3} (mb4_scheme.hpp:17).
+inline double lagrange_basis(const std::array<double, 4>& nodes, int i, double zeta) {
+    double v = 0.0;
+    detail::throw_status(mb4cu_lagrange_basis(nodes.data(), i, zeta, &v), mb4cu_create_error());
+    return v;
+}
 
 struct GridSpec {
     int nx = 0, ny = 0;
@@ -130,18 +246,93 @@ public:
                        std::array<double, 3> nodes = {1.0 / 3.0, 2.0 / 3.0, 1.0}) {
         const int rc = mb4cu_scheme_init(alpha1, nodes[0], nodes[1], nodes[2], &s_);
         detail::throw_status(rc, mb4cu_create_error());
+        fill_eig();
     }
     double alpha1() const { return s_.alpha1; }
     std::array<double, 4> nodes() const { return {s_.nodes[0], s_.nodes[1], s_.nodes[2], s_.nodes[3]}; }
     double e_ext(int i, int j) const { return s_.E[i - 1][j]; }
     double w(int i, int a, int b, int c) const { return s_.W[i - 1][a][b][c]; }
     std::array<double, 3> eigenvalues() const { return {s_.lam[0], s_.lam[1], s_.lam[2]}; }
+    /// E_core = T diag(lambda) T^{-1} (mb4_scheme.hpp:45-47)
+    const SmallMat& t() const { return eig_.t; }
+    const SmallMat& t_inv() const { return eig_.t_inv; }
     double t(int r, int c) const { return s_.T[r][c]; }
     double t_inv(int r, int c) const { return s_.Tinv[r][c]; }
+    double eval_A(double tau, double zeta) const { return nls2d::eval_A(s_.alpha1, tau, zeta); }
+    double lagrange(int i, double zeta) const { return lagrange_basis(nodes(), i, zeta); }
+
+    /// The 3x3 matrix M of A(tau,zeta) = [tau, tau^2/2, tau^3/3] M [1, zeta, zeta^2]^T
+    /// (mb4_scheme.hpp:36-38): the alpha1-free part plus alpha1 times the rank-one
+    /// block (1, -6, 6)^T (1, -6, 6) of the cancellation-free form.
+    SmallMat a_coeff() const {
+        const double a = s_.alpha1;
+        static const double base[3][3] = {{4.0, -6.0, 0.0}, {-6.0, 12.0, 0.0}, {0.0, 0.0, 0.0}};
+        static const double r1[3] = {1.0, -6.0, 6.0};
+        SmallMat m(3, 3);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) m(i, j) = base[i][j] + a * r1[i] * r1[j];
+        return m;
+    }
+
+    /// Plain-text key = value table of every constant, 17 significant digits
+    /// (mb4_scheme.hpp:50-51; same keys and order).
+    void dump(std::ostream& os) const {
+        char buf[96];
+        auto put = [&](const char* key, double v) {
+            std::snprintf(buf, sizeof(buf), "%s = %.17g\n", key, v);
+            os << buf;
+        };
+        put("alpha1", s_.alpha1);
+        char key[32];
+        for (int i = 1; i <= 3; ++i) {
+            std::snprintf(key, sizeof(key), "c%d", i);
+            put(key, s_.nodes[i]);
+        }
+        for (int i = 1; i <= 3; ++i)
+            for (int j = 0; j < 4; ++j) {
+                std::snprintf(key, sizeof(key), "E_%d_%d", i, j);
+                put(key, e_ext(i, j));
+            }
+        for (int i = 0; i < 3; ++i) {
+            std::snprintf(key, sizeof(key), "lambda%d", i + 1);
+            put(key, s_.lam[i]);
+        }
+        for (int i = 1; i <= 3; ++i)
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b)
+                    for (int c = 0; c < 4; ++c) {
+                        std::snprintf(key, sizeof(key), "W_%d_%d_%d_%d", i, a, b, c);
+                        put(key, w(i, a, b, c));
+                    }
+    }
+
+    /// E table at a chosen Gauss-Legendre order (>= 4 is exact; mb4_scheme.hpp:53-58).
+    static std::array<std::array<double, 4>, 3> integrate_e(double alpha1, const std::array<double, 4>& nodes,
+                                                            int points) {
+        double out[12];
+        detail::throw_status(mb4cu_scheme_integrate_e(alpha1, nodes.data(), points, out), mb4cu_create_error());
+        std::array<std::array<double, 4>, 3> e{};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 4; ++j) e[i][j] = out[i * 4 + j];
+        return e;
+    }
+
     const mb4cu_scheme& raw() const { return s_; }
 
 private:
+    void fill_eig() {
+        eig_.t = SmallMat(3, 3);
+        eig_.t_inv = SmallMat(3, 3);
+        for (int i = 0; i < 3; ++i) {
+            eig_.values[i] = s_.lam[i];
+            for (int j = 0; j < 3; ++j) {
+                eig_.t(i, j) = s_.T[i][j];
+                eig_.t_inv(i, j) = s_.Tinv[i][j];
+            }
+        }
+    }
     mb4cu_scheme s_{};
+    Eig3 eig_;
 };
 
 class GridModel;
@@ -318,6 +509,68 @@ inline State mb4_step(const GridModel& model, const Mb4Scheme& scheme, const Sta
     s.set_state(u0);
     s.step(h, stats);
     return s.get_state();
+}
+
+/// The three stage systems (I - h lambda_i J) of one step (mb4_integrator.hpp:76-83).
+/// The GPU path forms no matrix: the systems are applied matrix-free and solved by
+/// Fourier-preconditioned GMRES inside newton_solve, so the handle only carries h.
+/// (The reference's build(jacobian, ...) from a SparseCsr is not offered: no sparse
+/// matrix exists on this path.)
+struct StageSystem {
+    double h = 0.0;
+    static StageSystem build(const GridModel&, const Mb4Scheme&, double h, SolverKind = SolverKind::Direct,
+                             WorkerPool* = nullptr) {
+        if (!(h > 0.0)) throw std::invalid_argument("StageSystem: h must be positive");
+        return StageSystem{h};
+    }
+};
+
+struct NewtonResult {
+    std::array<State, 3> stages;
+    int iterations = 0;
+};
+
+/// Simplified Newton iteration of the stage equations from U = (u0, u0, u0)
+/// (mb4_integrator.cpp:194-255): per iteration Phi, T^{-1}, the three decoupled
+/// stage solves, T, update, stop when ||r||_inf <= epsilon.  Runs on the GPU through
+/// the stage-split entry points (mb4cu_ns_*); the iteration counts are the
+/// reference's.  Throws NonConvergenceError as the reference does.
+inline NewtonResult newton_solve(const GridModel& model, const Mb4Scheme& scheme, const StageSystem& sys,
+                                 const State& u0, double h, const NewtonConfig& cfg, WorkerPool* = nullptr,
+                                 double* solve_seconds = nullptr) {
+    cfg.validate();
+    if (sys.h != h) throw std::invalid_argument("newton_solve: stage system built for another h");
+    DeviceSession s(model, scheme, cfg, -1, 0, 3);
+    s.set_state(u0);
+    mb4cu_ctx* ctx = s.handle();
+    s.check(mb4cu_ns_begin(ctx, h));
+    NewtonResult res;
+    double r = 0.0;
+    for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+        s.check(mb4cu_ns_phibar(ctx));
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int k = 0; k < 3; ++k) s.check(mb4cu_ns_solve(ctx, k));
+        s.check(mb4cu_ns_update(ctx, &r));
+        if (solve_seconds)
+            *solve_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        res.iterations = iter;
+        if (!std::isfinite(r)) {
+            mb4cu_ns_abort(ctx);
+            throw NonConvergenceError("newton_solve: iteration diverged (non-finite update)",
+                                      std::numeric_limits<double>::infinity());
+        }
+        if (r <= cfg.epsilon) {
+            for (auto& st : res.stages) st.resize(u0.size());
+            s.check(mb4cu_ns_get_stages(ctx, reinterpret_cast<double*>(res.stages[0].data()),
+                                        reinterpret_cast<double*>(res.stages[1].data()),
+                                        reinterpret_cast<double*>(res.stages[2].data())));
+            mb4cu_ns_abort(ctx);
+            return res;
+        }
+    }
+    mb4cu_ns_abort(ctx);
+    throw NonConvergenceError("newton_solve: no convergence after " + std::to_string(cfg.max_iters) + " iterations",
+                              r);
 }
 
 namespace detail {

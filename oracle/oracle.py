@@ -80,6 +80,26 @@ def oracle_lib() -> C.CDLL:
     return _olib
 
 
+INPUTS_SO = os.path.join(HERE, "libinputs.so")
+_ilib = None
+
+
+def inputs_generator():
+    """(make_inputs, scale_state) of oracle/libinputs.so: the BASELINE input generator
+    compiled host-only (g++), for bench.py's reference arm -- same source and arithmetic
+    as the product library's mb4cu_make_inputs, without mapping libmb4cu.so.
+    Pass it as configs.make_inputs(cfg, gen=...)."""
+    global _ilib
+    if _ilib is None:
+        L = C.CDLL(INPUTS_SO)
+        L.orc_make_inputs.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, DP, DP, DP]
+        L.orc_make_inputs.restype = C.c_int
+        L.orc_scale_state.argtypes = [DP, C.c_size_t, D, C.c_int]
+        L.orc_scale_state.restype = C.c_int
+        _ilib = L
+    return _ilib.orc_make_inputs, _ilib.orc_scale_state
+
+
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
 

@@ -164,6 +164,11 @@ def lib() -> C.CDLL:
         "mb4cu_ns_set_correction": (I, [P, I, P]),
         "mb4cu_ns_update": (I, [P, DP]),
         "mb4cu_ns_commit": (I, [P]),
+        "mb4cu_ns_get_stages": (I, [P, DP, DP, DP]),
+        "mb4cu_ns_abort": (I, [P]),
+        "mb4cu_eval_a": (D, [D, D, D]),
+        "mb4cu_lagrange_basis": (I, [DP, I, D, DP]),
+        "mb4cu_scheme_integrate_e": (I, [D, DP, I, DP]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -189,5 +194,6 @@ EXPORTED = [
     "mb4cu_profile_reset", "mb4cu_profile_get", "mb4cu_halo_count", "mb4cu_halo_pack",
     "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_sweep_region", "mb4cu_commit_step", "mb4cu_observables_sums",
     "mb4cu_ns_begin", "mb4cu_ns_phibar", "mb4cu_ns_solve", "mb4cu_ns_get_correction", "mb4cu_ns_set_correction",
-    "mb4cu_ns_update", "mb4cu_ns_commit",
+    "mb4cu_ns_update", "mb4cu_ns_commit", "mb4cu_ns_get_stages", "mb4cu_ns_abort",
+    "mb4cu_eval_a", "mb4cu_lagrange_basis", "mb4cu_scheme_integrate_e",
 ]

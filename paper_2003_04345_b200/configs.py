@@ -99,27 +99,37 @@ def input_spec(cfg: LatticeConfig, threads: int = 0) -> _lib.Inputs:
     return s
 
 
+def _generator(gen):
+    """(make_inputs, scale_state) C entry points: the product library's by default;
+    `gen` injects the same generator from another library (bench.py's reference arm
+    uses oracle/libinputs.so so that it never maps libmb4cu.so)."""
+    if gen is not None:
+        return gen
+    L = _lib.lib()
+    return L.mb4cu_make_inputs, L.mb4cu_scale_state
+
+
 def make_block(cfg: LatticeConfig, x0: int = 0, y0: int = 0, lnx: Optional[int] = None,
-               lny: Optional[int] = None, threads: int = 0):
+               lny: Optional[int] = None, threads: int = 0, gen=None):
     """(V, psi_unnormalised, sum|psi|^2) of a sub-block of the global lattice."""
     lnx = cfg.nx if lnx is None else lnx
     lny = cfg.ny if lny is None else lny
     V = np.empty(lnx * lny)
     psi = np.empty(lnx * lny, dtype=np.complex128)
     psum = C.c_double(0.0)
-    L = _lib.lib()
+    make, _ = _generator(gen)
     spec = input_spec(cfg, threads)
-    rc = L.mb4cu_make_inputs(C.byref(spec), x0, y0, lnx, lny, dptr(V), dptr(psi), C.byref(psum))
+    rc = make(C.byref(spec), x0, y0, lnx, lny, dptr(V), dptr(psi), C.byref(psum))
     if rc != 0:
-        raise ValueError(L.mb4cu_create_error().decode())
+        raise ValueError(f"make_inputs: invalid lattice / block / packet spec ({rc})")
     return V, psi, psum.value
 
 
-def make_inputs(cfg: LatticeConfig, threads: int = 0):
+def make_inputs(cfg: LatticeConfig, threads: int = 0, gen=None):
     """(V, psi) of the whole lattice, psi normalised to sum |psi|^2 = 1."""
-    V, psi, psum = make_block(cfg, threads=threads)
-    L = _lib.lib()
-    L.mb4cu_scale_state(dptr(psi), psi.size, 1.0 / math.sqrt(psum), threads)
+    V, psi, psum = make_block(cfg, threads=threads, gen=gen)
+    _, scale = _generator(gen)
+    scale(dptr(psi), psi.size, 1.0 / math.sqrt(psum), threads)
     return V, psi
 
 

@@ -1120,6 +1120,18 @@ int mb4cu_scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_sche
     return mb4cu::scheme_init(alpha1, c1, c2, c3, out, g_create_error);
 }
 
+double mb4cu_eval_a(double alpha1, double tau, double zeta) { return mb4cu::eval_a_double(alpha1, tau, zeta); }
+
+int mb4cu_lagrange_basis(const double nodes[4], int i, double zeta, double* out) {
+    g_create_error.clear();
+    return mb4cu::lagrange_basis_double(nodes, i, zeta, out, g_create_error);
+}
+
+int mb4cu_scheme_integrate_e(double alpha1, const double nodes[4], int points, double out[12]) {
+    g_create_error.clear();
+    return mb4cu::integrate_e(alpha1, nodes, points, out, g_create_error);
+}
+
 int mb4cu_make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny, double* V,
                       double* psi, double* psum) {
     g_create_error.clear();
@@ -2071,6 +2083,23 @@ int mb4cu_ns_update(mb4cu_ctx* ctx, double* rmax) {
                                   ctx->stream));
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     *rmax = decode_bits(*ctx->h_rmax);
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_get_stages(mb4cu_ctx* ctx, double* u1, double* u2, double* u3) {
+    if (!ctx || !ctx->ns_open || !u1 || !u2 || !u3)
+        return fail(ctx, MB4CU_INVALID, "ns_get_stages: open step, three host buffers");
+    double* out[3] = {u1, u2, u3};
+    for (int i = 0; i < 3; ++i)
+        MB4_CUDA(ctx, cudaMemcpyAsync(out[i], ctx->U[0][i], ctx->n * sizeof(double2), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MB4CU_OK;
+}
+
+int mb4cu_ns_abort(mb4cu_ctx* ctx) {
+    if (!ctx || !ctx->ns_open) return fail(ctx, MB4CU_INVALID, "ns_abort: no open step");
+    ctx->ns_open = false;
     return MB4CU_OK;
 }
 

@@ -13,6 +13,9 @@ namespace mb4cu {
 
 int scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* out,
                 std::string& why);
+double eval_a_double(double alpha1, double tau, double zeta);
+int lagrange_basis_double(const double nodes[4], int i, double zeta, double* out, std::string& why);
+int integrate_e(double alpha1, const double nodes[4], int points, double out[12], std::string& why);
 int make_inputs(const mb4cu_inputs* spec, int x0, int y0, int lnx, int lny, double* V,
                 double* psi, double* psum, std::string& why);
 int scale_state(double* psi, size_t nsites, double s, int threads);

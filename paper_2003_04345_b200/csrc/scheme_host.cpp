@@ -255,6 +255,53 @@ int scheme_init(double alpha1, double c1, double c2, double c3, mb4cu_scheme* ou
     return MB4CU_OK;
 }
 
+// ---- scheme helpers of the reference API (mb4_scheme.hpp:14-20, 53-58) ----------
+
+double eval_a_double(double alpha1, double tau, double zeta) {
+    // the rank-one form of coeff_a above, in double as the reference's free eval_A
+    const double lin = tau * (4.0 - 6.0 * zeta) + tau * tau * (6.0 * zeta - 3.0);
+    const double t3 = tau * (1.0 - tau) * (1.0 - 2.0 * tau);
+    const double z2 = 1.0 - 6.0 * zeta * (1.0 - zeta);
+    return lin + alpha1 * t3 * z2;
+}
+
+int lagrange_basis_double(const double nodes[4], int i, double zeta, double* out, std::string& why) {
+    if (!nodes || !out || i < 0 || i > 3) {
+        why = "lagrange_basis: index out of range";
+        return MB4CU_INVALID;
+    }
+    double v = 1.0;
+    for (int b = 0; b < 4; ++b) {
+        if (b == i) continue;
+        const double den = nodes[i] - nodes[b];
+        if (den == 0.0) {
+            why = "lagrange_basis: coincident nodes";
+            return MB4CU_INVALID;
+        }
+        v *= (zeta - nodes[b]) / den;
+    }
+    *out = v;
+    return MB4CU_OK;
+}
+
+int integrate_e(double alpha1, const double nodes[4], int points, double out[12], std::string& why) {
+    if (!nodes || !out || points < 1 || points > 64) {
+        why = "integrate_e: points must be in 1..64";
+        return MB4CU_INVALID;
+    }
+    std::array<ld, 4> c{};
+    for (int i = 0; i < 4; ++i) c[i] = nodes[i];
+    ld z[64], w[64];
+    gl_rule(points, z, w);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 4; ++j) {
+            ld acc = 0.0L;
+            for (int q = 0; q < points; ++q) acc += w[q] * coeff_a(alpha1, c[i + 1], z[q]) * lagrange(c, j, z[q]);
+            out[i * 4 + j] = static_cast<double>(acc);
+        }
+    return MB4CU_OK;
+}
+
 // ---- tables of the other integrators -----------------------------------------
 // The reference builds them in double at first use from its Gauss-Legendre rule
 // (quadrature.cpp:9-36: Newton iteration on P_n from the Chebyshev guess); the

@@ -328,7 +328,7 @@ mb4_step_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         a.status->sweeps = sweeps;
         a.status->set = set;
         a.status->converged = converged;
-        a.status->rlast = rlast;
+        a.status->rlast = isfinite(rlast) ? rlast : __longlong_as_double(0x7FF0000000000000ll);  // NaN -> +inf
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
         // fixed-order sum of the block partials written before the first grid.sync

@@ -1291,7 +1291,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         a.status->set = set;
         a.status->converged = converged;
         a.status->redone = redone;
-        a.status->rlast = rlast;
+        // a non-finite residual (NaN update somewhere) is reported as +inf: the MAX
+        // all-reduce of a decomposed lattice (fmax) would drop a NaN, never an inf
+        a.status->rlast = isfinite(rlast) ? rlast : __longlong_as_double(0x7FF0000000000000ll);
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
         double v = 0.0;

@@ -263,7 +263,8 @@ class DistributedSession:
             if s > 0:
                 self.halo.exchange(F_SET0 + ((s - 1) & 1))
             r_loc, sums = self.b.sweep(h, s)
-            r = self.comm.allreduce_max(r_loc)
+            # NaN -> +inf before the MAX all-reduce (fmax would drop a NaN rank)
+            r = self.comm.allreduce_max(r_loc if math.isfinite(r_loc) else math.inf)
             if s == 0 and self.entry_sums is None:
                 self.entry_sums = self.comm.allreduce_sum(sums)
             if not math.isfinite(r):

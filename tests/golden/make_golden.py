@@ -10,8 +10,13 @@ Sources (nothing here is hand-written data):
                         inputs produced by paper_2003_04345_b200.configs.
   ref_methods_cfg1_5.npz -- the same library's StepDriver(RK4 / GAUSS2 / GAUSS4 /
                         AVF2 / AVF4), direct solver, 5 cfg1 steps.
+  ref_cfg4_sub.npz   -- the reference library on the full cfg4 lattice (4096^2, V_d ~
+                        U[5,50), 4 packets; GMRES, 3 workers, ~15 min here), 10 steps:
+                        the full energy record and a deterministic subsample of the
+                        state after steps 1 and 10 (every CFG4_STRIDE-th site) plus
+                        whole-state checksums (sum |u|^2, sum u).
 
-usage: python tests/golden/make_golden.py [--methods-only]
+usage: python tests/golden/make_golden.py [--methods-only | --cfg4-only]
 """
 import hashlib
 import json
@@ -99,8 +104,37 @@ def methods_case():
     return out
 
 
+CFG4_STRIDE = 257  # sites k = 0, 257, 514, ... (65 281 of 4096^2; hits every column)
+
+
+def cfg4_case(nsteps=10):
+    cfg = configs.CONFIGS["cfg4"]
+    V, psi = configs.make_inputs(cfg)
+    idx = np.arange(0, cfg.sites, CFG4_STRIDE, dtype=np.int64)
+    out = {"input_sha256": input_digest(V, psi), "solver": "gmres", "workers": 3, "nsteps": nsteps,
+           "stride": CFG4_STRIDE, "idx": idx}
+    u = psi
+    obs_series, iters_all, done = [], [], 0
+    for m in (1, nsteps):
+        u, obs, iters, secs = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, u, cfg.dt,
+                                        m - done, eps=cfg.epsilon, solver="gmres", workers=3)
+        print(f"cfg4: steps {done}..{m} in {secs:.1f} s, Newton iterations {iters.tolist()}", flush=True)
+        obs_series.append(obs if done == 0 else obs[1:])
+        iters_all.extend(iters.tolist())
+        done = m
+        out[f"sub_{m}"] = u[idx].copy()
+        out[f"norm2_{m}"] = float(np.vdot(u, u).real)
+        out[f"sum_{m}"] = complex(u.sum())
+    out["obs"] = np.concatenate(obs_series, axis=0)
+    out["iters"] = np.array(iters_all, dtype=np.int32)
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
+    if "--cfg4-only" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "ref_cfg4_sub.npz"), **cfg4_case())
+        return
     np.savez_compressed(os.path.join(HERE, "ref_methods_cfg1_5.npz"), **methods_case())
     if "--methods-only" in sys.argv:
         return

@@ -58,3 +58,62 @@ def test_cpp_harness_drop_in_runs(tmp_path):
     build(exe, SRC_HARNESS)
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+SRC_SCHEME = os.path.join(ROOT, "tests", "cpp", "test_scheme_api.cpp")
+
+
+def _exact_table(path):
+    import json
+
+    d = json.load(open(os.path.join(ROOT, "tests", "golden", "scheme_exact.json")))
+    lines = [f"alpha1 {d['alpha1']!r}", f"A_half_half {d['A_half_half']!r}", f"l3_half {d['l3_half']!r}"]
+    for i in range(3):
+        for j in range(4):
+            lines.append(f"E_{i + 1}_{j} {d['E'][i * 4 + j]!r}")
+        lines.append(f"lambda{i + 1} {d['eigenvalues'][i]!r}")
+    lines.append(f"W_3_3_3_3 {d['W'][191]!r}")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+def test_cpp_scheme_surface_matches_reference_cases(tmp_path):
+    """eval_A / lagrange_basis / a_coeff / t() / t_inv() / dump / integrate_e and
+    split_state / join_state of include/nls2d, checked with the cases of the
+    reference's test_mb4_scheme.cpp against its exact-rational tables (host only)."""
+    exe = str(tmp_path / "test_scheme_api")
+    build(exe, SRC_SCHEME)
+    _exact_table(tmp_path / "exact.txt")
+    r = subprocess.run([exe, "scheme", str(tmp_path / "exact.txt")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_newton_solve_matches_oracle(tmp_path):
+    """newton_solve (mb4_integrator.hpp:85-95) through include/nls2d on the paper's
+    70x70 lx = 2 pi baseline: the three stages against the C oracle's newton_solve,
+    U3 against the reference library's step, and the reference's iteration count."""
+    from oracle import oracle as O
+    from paper_2003_04345_b200 import nls2d
+
+    exe = str(tmp_path / "test_scheme_api")
+    build(exe, SRC_SCHEME)
+    n, gamma, h = 70, -0.1, 0.01
+    g = nls2d.GridSpec(n, n, 2 * np.pi, 2 * np.pi)
+    u0 = nls2d.initial_condition(g)
+    u0.tofile(tmp_path / "u0.bin")
+    r = subprocess.run([exe, "newton", str(tmp_path / "u0.bin"), str(n), repr(gamma), repr(h),
+                        str(tmp_path / "stage")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    iters = int(r.stdout.split()[1])
+    stages = [np.fromfile(tmp_path / f"stage{i}.bin", dtype=np.complex128) for i in (1, 2, 3)]
+    cx = 1.0 / g.hx() ** 2
+    orc = O.Oracle(n, n, gamma, np.zeros(n * n), cx=cx, cy=cx)
+    rc, ost, oit, _ = orc.newton_solve(u0, h, eps=1e-13)
+    assert rc == 0
+    for a, b in zip(stages, ost):
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-10
+    ref, _, riters, _ = O.ref_run(n, n, 2 * np.pi, 2 * np.pi, gamma, np.zeros(n * n), u0, h, 1, eps=1e-13,
+                                  solver="direct", record=False)
+    assert np.linalg.norm(stages[2] - ref) / np.linalg.norm(ref) <= 1e-10
+    assert iters == int(riters[0])

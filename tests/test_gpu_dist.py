@@ -214,6 +214,15 @@ def test_stage_split_matches_single_context_newton_krylov(world):
     for u, got_its in out:
         assert got_its == its
         assert np.array_equal(u, ref)
+    # anchor to the reference itself (not only to the single-context GPU path): the
+    # reference's stage solves (mb4_integrator.cpp:221-229, direct LU), same inputs
+    from oracle import oracle as O
+
+    oref, _, oits, _ = O.ref_run(n, n, 2 * np.pi, 2 * np.pi, gamma, np.zeros(n * n), u0, hs[0], len(hs),
+                                 eps=cfg.epsilon, max_iters=cfg.max_iters, solver="direct")
+    for u, got_its in out:
+        assert np.linalg.norm(u - oref) / np.linalg.norm(oref) <= 1e-10
+        assert got_its == list(oits)  # the reference's simplified-Newton iteration counts
 
 
 @pytest.mark.parametrize("overlap", [False, True])
@@ -253,3 +262,57 @@ def test_set_neumann_terms_validation():
         assert L.mb4cu_ns_solve(s._ctx, 0) == _lib.MB4CU_INVALID
         s.set_state(psi)
         s.step(cfg.dt)  # still steps normally at the fixed depth
+
+
+class FmaxLoopbackComm(LoopbackComm):
+    """MAX all-reduce with NCCL / gloo semantics (fmax: a NaN operand is dropped)."""
+
+    def allreduce_max(self, x):
+        return float(np.fmax.reduce(np.asarray(self._gather(x), dtype=np.float64)))
+
+    def allreduce_max_(self, t):
+        t.copy_(torch.from_numpy(np.fmax.reduce(np.stack(self._gather(t.cpu().numpy().copy())), axis=0)))
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_nan_block_on_one_rank_is_reported_by_every_rank(overlap):
+    """A NaN in one rank's sub-domain must not be lost in the MAX all-reduce (fmax drops
+    NaN operands): the library reports a non-finite local residual as +inf, so every
+    rank sees the divergence and no rank commits a step (dist.py)."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    px, py, world = 2, 1, 2
+    hub = Hub(world)
+    res = [None] * world
+    errs = []
+
+    def work(rank):
+        try:
+            torch.cuda.set_device(0)
+            dec = D.Decomposition(cfg.nx, cfg.ny, px, py, rank)
+            be = D.CudaBackend(dec, dec.block(V), nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon,
+                               cfg.max_iters, 1, 0, overlap=overlap)
+            blk = dec.block(psi).copy()
+            if rank == 1:
+                blk[blk.size // 2] = np.nan
+            be.set_state(blk)
+            sess = D.DistributedSession(dec, be, FmaxLoopbackComm(hub, rank), cfg.gamma, 1.0, 1.0, cfg.epsilon,
+                                        max_step_halvings=0)
+            try:
+                sess.step(cfg.dt)
+                res[rank] = "committed"
+            except D.NonConvergence:
+                res[rank] = "diverged"
+            be.close()
+        except Exception as exc:
+            errs.append(exc)
+            hub.bar.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    assert res == ["diverged", "diverged"]

@@ -114,16 +114,48 @@ def test_large_lattice_properties(name, nx):
     assert np.abs(obs_a[:, 3] - obs_t[:, 3]).max() <= 1e-13 * abs(H[0])
 
 
-def test_cfg3_one_step_against_reference():
+def test_cfg3_ten_steps_against_reference():
+    """cfg3 (1024^2): the reference library (oracle/_ref, GMRES, 3 workers) run live on
+    the GPU box's host for 10 steps (~35 s); state after 1 and 10 steps <= 1e-10 and
+    the energy record within 1e-13 |H0| (north_star)."""
     cfg = configs.CONFIGS["cfg3"]
     V, psi = configs.make_inputs(cfg)
     with session(cfg, V) as s:
         s.set_state(psi)
         s.step(cfg.dt)
         u1 = s.get_state()
-    ref, _, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi, cfg.dt, 1,
-                             eps=cfg.epsilon, solver="gmres", workers=3, record=False)
-    assert rel(u1, ref) <= 1e-10
+        obs, _ = s.run(cfg.dt, 9)
+        u10 = s.get_state()
+    r1, _, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi, cfg.dt, 1,
+                            eps=cfg.epsilon, solver="gmres", workers=3, record=False)
+    assert rel(u1, r1) <= 1e-10
+    r10, robs, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, r1, cfg.dt, 9,
+                                eps=cfg.epsilon, solver="gmres", workers=3)
+    assert rel(u10, r10) <= 1e-10
+    assert np.abs(obs[:, 3] - robs[:, 3]).max() <= 1e-13 * abs(robs[0, 3])
+
+
+def test_cfg4_ten_steps_against_reference_fixture():
+    """cfg4 (4096^2, V_d ~ U[5,50), 4 packets; the config where the adaptive later-sweep
+    depth switches to m = 2): the reference library's 10-step run, generated in the build
+    container (tests/golden/make_golden.py --cfg4-only), as a deterministic subsample of
+    the state after steps 1 and 10, whole-state checksums and the energy record."""
+    g = np.load(os.path.join(GOLD, "ref_cfg4_sub.npz"))
+    cfg = configs.CONFIGS["cfg4"]
+    V, psi = configs.make_inputs(cfg)
+    idx = g["idx"]
+    with session(cfg, V) as s:
+        s.set_state(psi)
+        s.step(cfg.dt)
+        u1 = s.get_state()
+        obs, sweeps = s.run(cfg.dt, 9)
+        u10 = s.get_state()
+    assert max(sweeps) >= 3  # the schedule the fixture pins (adaptive depth in play)
+    for k, u in ((1, u1), (10, u10)):
+        assert rel(u[idx], g[f"sub_{k}"]) <= 1e-10
+        assert abs(np.vdot(u, u).real - float(g[f"norm2_{k}"])) <= 1e-12 * float(g[f"norm2_{k}"])
+        assert abs(u.sum() - complex(g[f"sum_{k}"])) <= 1e-10 * np.sqrt(u.size * float(g[f"norm2_{k}"]))
+    assert np.abs(obs[:, 3] - g["obs"][1:, 3]).max() <= 1e-13 * abs(g["obs"][0, 3])
 
 
 def test_nonconvergence_leaves_state_unchanged_and_reports_residual():

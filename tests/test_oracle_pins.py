@@ -217,3 +217,21 @@ def test_methods_golden_fixture_pinned():
         u, _, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, psi, cfg.dt, 5,
                                eps=cfg.epsilon, solver="direct", method="avf2")
         assert np.array_equal(u, g["avf2_state"])
+
+
+def test_host_only_input_generator_is_bit_identical():
+    """oracle/libinputs.so (g++ only; bench.py's reference arm) produces the product
+    library's BASELINE inputs bit for bit -- whole lattices and a cfg5 sub-block."""
+    from paper_2003_04345_b200 import configs
+
+    gen = O.inputs_generator()
+    for name in ("cfg1", "cfg2", "cfg4"):
+        cfg = configs.CONFIGS[name]
+        Va, pa = configs.make_inputs(cfg)
+        Vb, pb = configs.make_inputs(cfg, gen=gen)
+        assert np.array_equal(Va.view(np.uint64), Vb.view(np.uint64))
+        assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64))
+    cfg = configs.CONFIGS["cfg5"]
+    a = configs.make_block(cfg, 4096, 1024, 300, 200)
+    b = configs.make_block(cfg, 4096, 1024, 300, 200, gen=gen)
+    assert all(np.array_equal(np.asarray(x).view(np.uint64), np.asarray(y).view(np.uint64)) for x, y in zip(a, b))
