@@ -67,6 +67,27 @@
 #ifndef MB4_FIRST_REGZ
 #define MB4_FIRST_REGZ 1
 #endif
+// z rows of u0 / U (double2) arrive by bulk copies (TMA engine, one thread, mbarrier per
+// ring slot) instead of per-thread cp.async; V stays on cp.async (8-byte elements).
+// Measured (r02, cfg5): slower -- first sweep 1.34 -> 1.50 ms, later sweeps 1.60 -> 1.97 ms
+// (threads spin on the ring mbarriers; the rows land later than the cp.async rows).
+#ifndef MB4_BULK
+#define MB4_BULK 0
+#endif
+// later sweeps: u0 / U ring rows placed so that every shared address has the alignment of
+// its global source modulo 128 B (one cp.async wavefront per 128-byte line instead of two:
+// the 16-byte cp.async of a misaligned row cost 9.2 wavefronts per warp instead of ~5)
+#ifndef MB4_ALIGN_RING
+#define MB4_ALIGN_RING 1
+#endif
+// later sweeps: the Neumann levels apply J through (P, Q, R) as well
+#ifndef MB4_LATER_PQR
+#define MB4_LATER_PQR 1
+#endif
+// first sweep: J applied through per-site coefficients (P, Q, R) formed once per site
+#ifndef MB4_FIRST_PQR
+#define MB4_FIRST_PQR 1
+#endif
 #ifndef MB4_MINB_LATER
 #define MB4_MINB_LATER 3
 #endif
@@ -106,9 +127,12 @@ struct Geom3 {
     static constexpr int S = 6;             // z ring rows (divisible by the unroll of 3)
     static constexpr int BACK = M == 2 ? 3 : 1;  // oldest z row still read: j - BACK
     static constexpr int P = S - 1 - BACK;  // rows in flight
-    static constexpr size_t zu0_bytes = sizeof(double2) * S * ZW;
+    // row stride of the u0 / U rings: a multiple of 128 B with room for a shift of up to
+    // 7 columns (MB4_ALIGN_RING)
+    static constexpr int ZWP = MB4_ALIGN_RING ? ((ZW + 7 + 7) / 8) * 8 : ZW;
+    static constexpr size_t zu0_bytes = sizeof(double2) * S * ZWP;
     static constexpr size_t zv_bytes = ((sizeof(double) * S * ZW + 15) / 16) * 16;
-    static constexpr size_t zU_bytes = sizeof(double2) * S * 3 * ZW;
+    static constexpr size_t zU_bytes = sizeof(double2) * S * 3 * ZWP;
     static constexpr size_t pub_bytes = sizeof(double2) * 2 * 3 * ZW;  // one level, 2 parities
     static constexpr size_t bytes = zu0_bytes + zv_bytes + zU_bytes + M * pub_bytes;
     // CTAs per SM: M <= 1 fits 3 (<= 168 registers, ~70 KB smem), M = 2 fits 2
@@ -125,19 +149,38 @@ namespace defscheme {
 #include "defscheme.inc"
 #undef MB4_DS_QUAL
 }  // namespace defscheme
+// The same tables in the constant bank (c[0x3], values opaque to the compiler): sm_100a
+// FP64 instructions take no constant-bank operand, so every table entry reaches a DFMA
+// through a uniform register -- LDCU.128 moves two entries per instruction, while a
+// compile-time immediate costs two UMOVs per entry (13 % of the later sweep's
+// instructions with the constexpr tables).  Measured (r02): the later sweep spills at
+// the 168-register bound and runs 1.6 -> 3.1 ms at cfg5, so the immediates stay.
+namespace defscheme_cb {
+#define MB4_DS_QUAL __constant__
+#include "defscheme.inc"
+#undef MB4_DS_QUAL
+}  // namespace defscheme_cb
+#ifndef MB4_DEF_CBANK
+#define MB4_DEF_CBANK 0
+#endif
+#if MB4_DEF_CBANK
+namespace dsv = defscheme_cb;
+#else
+namespace dsv = defscheme;
+#endif
 
 // Coefficient views: isotropic (unit stencil, pre-scaled constants) or general;
 // DEF: scheme tables from defscheme (only with ISO, see dispatch3).
 template <bool ISO, bool DEF = false>
 struct Coef {
     const SweepConsts& c;
-    __device__ __forceinline__ double Lq(int q, int b) const { return DEF ? defscheme::L[q][b] : c.L[q][b]; }
-    __device__ __forceinline__ double WAk(int k, int q) const { return DEF ? defscheme::WA[k][q] : c.WA[k][q]; }
+    __device__ __forceinline__ double Lq(int q, int b) const { return DEF ? dsv::L[q][b] : c.L[q][b]; }
+    __device__ __forceinline__ double WAk(int k, int q) const { return DEF ? dsv::WA[k][q] : c.WA[k][q]; }
     // level-0 residual Phi_k = dz_k - hr * (E0 w ...) with w = (K+V) z (/ c if ISO):
     // ISO without DEF uses the pre-scaled Es = c E and the true gamma, h; ISO with
     // DEF the unscaled E and gamma / c, c h (the same product, one rounding apart).
     __device__ __forceinline__ double E0(int i, int j) const {
-        return DEF ? defscheme::E[i][j] : (ISO ? c.Es[i][j] : c.E[i][j]);
+        return DEF ? dsv::E[i][j] : (ISO ? c.Es[i][j] : c.E[i][j]);
     }
     __device__ __forceinline__ double g0() const { return DEF && ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double h0() const { return DEF && ISO ? c.hs : c.h; }
@@ -156,8 +199,8 @@ struct Coef {
             out[i].y = fma(Tm(i, 0), rb[0].y, fma(Tm(i, 1), rb[1].y, Tm(i, 2) * rb[2].y));
         }
     }
-    __device__ __forceinline__ double Tm(int i, int k) const { return DEF ? defscheme::T[i][k] : c.T[i][k]; }
-    __device__ __forceinline__ double Ti(int k, int i) const { return DEF ? defscheme::Tinv[k][i] : c.Tinv[k][i]; }
+    __device__ __forceinline__ double Tm(int i, int k) const { return DEF ? dsv::T[i][k] : c.T[i][k]; }
+    __device__ __forceinline__ double Ti(int k, int i) const { return DEF ? dsv::Tinv[k][i] : c.Tinv[k][i]; }
     __device__ __forceinline__ double g() const { return ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double hl(int k) const { return ISO ? c.hls[k] : c.hlam[k]; }
     __device__ __forceinline__ double hl2(int k) const { return ISO ? c.hls2[k] : c.hlam2[k]; }
@@ -191,6 +234,28 @@ struct Coef {
         const double m = LEV == 2 ? hl2(k) : hl(k);
         return make_double2(fma(m, jx, base.x), fma(m, jy, base.y));
     }
+    // Per-site coefficients of J (isotropic: J / c) in the form
+    //   (J t).x = P t.y - (Q t.x + N.y),   (J t).y = R t.x + (Q t.y + N.x)
+    // with N = the neighbour sum of t (cx (l + r) + cy (dn + up)) and, from u0 and the
+    // stencil diagonal d = dv(v):  P = d - g (p^2 + 3 q^2),  Q = 2 g p q,
+    // R = g (3 p^2 + q^2) - d  -- the same operator as jt(), 10 instead of 21 FP64
+    // operations per application once P, Q, R are formed (once per site).
+    struct PQR {
+        double p, q, r;
+    };
+    __device__ __forceinline__ PQR pqr(double d, double2 u0) const {
+        const double pp = u0.x * u0.x, qq = u0.y * u0.y;
+        const double al = fma(3.0, pp, qq), de = fma(3.0, qq, pp);
+        const double gg = g();
+        return PQR{fma(-gg, de, d), 2.0 * gg * (u0.x * u0.y), fma(gg, al, -d)};
+    }
+    __device__ __forceinline__ double2 nsum(double2 l, double2 r, double2 dn, double2 up) const {
+        if (ISO) return make_double2((l.x + r.x) + (dn.x + up.x), (l.y + r.y) + (dn.y + up.y));
+        return make_double2(fma(c.cx, l.x + r.x, c.cy * (dn.x + up.x)), fma(c.cx, l.y + r.y, c.cy * (dn.y + up.y)));
+    }
+    __device__ __forceinline__ double2 jt_pqr(const PQR& k, double2 t, double2 n) const {
+        return make_double2(fma(k.p, t.y, -fma(k.q, t.x, n.y)), fma(k.r, t.x, fma(k.q, t.y, n.x)));
+    }
     // J t (isotropic: J t / c) from a = kv(...) of t and u0
     __device__ __forceinline__ double2 jt(double2 t, double2 a, double2 u0) const {
         const double pp = u0.x * u0.x, qq = u0.y * u0.y;
@@ -209,18 +274,32 @@ struct March3 {
         if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
         return static_cast<size_t>(y) * a.nx + x;
     }
-    double2* zu0;  // [S][ZW]
+    double2* zu0;  // [S][ZWP] (shifted per segment by the alignment offset)
     double* zv;    // [S][ZW]
-    double2* zU;   // [S][3][ZW]
+    double2* zU;   // [S][3][ZWP]
+    double2* zu0_base;
+    double2* zU_base;
     double2* pub;  // [M][2][3][ZW]
 
     double2 zw[3][4];  // own-column z rows; slot of z row k = k mod 3
     double vw[3];
+#if MB4_BULK
+    unsigned long long* bars;  // one mbarrier per z ring slot (bulk row copies)
+    __device__ static unsigned long long* ring_bars() {
+        __shared__ unsigned long long b[G::S];
+        return b;
+    }
+#endif
 
     __device__ March3(unsigned char* smem) {
+#if MB4_BULK
+        bars = ring_bars();
+#endif
         zu0 = reinterpret_cast<double2*>(smem);
         zv = reinterpret_cast<double*>(smem + G::zu0_bytes);
         zU = reinterpret_cast<double2*>(smem + G::zu0_bytes + G::zv_bytes);
+        zu0_base = zu0;
+        zU_base = zU;
         pub = reinterpret_cast<double2*>(smem + G::zu0_bytes + G::zv_bytes + G::zU_bytes);
     }
 
@@ -233,6 +312,7 @@ struct March3 {
         int xlim;        // right edge (exclusive) of the output rectangle
         int smask;       // stages stored (bit q): 7, or 4 = U3 only (speculative final sweep)
         int gxa, gxb;    // global columns of smem column t + 1 and of halo column 0 / NT + 1 (t < 2)
+        int gx0;         // global column of smem column 0 (wrapped; ghost-padded in GHOST mode)
         int next_row;    // global (periodic) row of the next z row to issue
         size_t next_off; // its element offset
     };
@@ -252,6 +332,20 @@ struct March3 {
                 s.next_off += a.nx;
             }
             const int t = threadIdx.x;
+#if MB4_BULK
+            if (t == 0) {
+                // the row segment's NT + 2 columns of u0 (and U1..U3) in one bulk copy each
+                const int w = GHOST ? a.pitch : a.nx;
+                const unsigned nb = bulk_row_bytes<!GHOST>(s.gx0, G::ZW, w);
+                mbar_arrive_expect_tx(&bars[slot], nb * (FIRST ? 1 : 4));
+                bulk_row<!GHOST>(&zu0[slot * G::ZWP], a.u0 + rowoff, s.gx0, G::ZW, w, &bars[slot]);
+                if (!FIRST) {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+                        bulk_row<!GHOST>(&zU[(slot * 3 + q) * G::ZWP], uin[q] + rowoff, s.gx0, G::ZW, w, &bars[slot]);
+                }
+            }
+#endif
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && t >= 2) break;
@@ -259,12 +353,14 @@ struct March3 {
                 // barrier); threads 0 / 1 also fill the halo columns 0 / NT + 1
                 const int col = h ? (t == 0 ? 0 : NT + 1) : t + 1;
                 const size_t g = rowoff + (h ? s.gxb : s.gxa);
-                cp_async16(&zu0[slot * G::ZW + col], a.u0 + g);
                 cp_async8(&zv[slot * G::ZW + col], a.V + g);
+#if !MB4_BULK
+                cp_async16(&zu0[slot * G::ZWP + col], a.u0 + g);
                 if (!FIRST) {
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) cp_async16(&zU[(slot * 3 + q) * G::ZW + col], uin[q] + g);
+                    for (int q = 0; q < 3; ++q) cp_async16(&zU[(slot * 3 + q) * G::ZWP + col], uin[q] + g);
                 }
+#endif
             }
         }
         cp_async_commit();
@@ -294,10 +390,10 @@ struct March3 {
             const double2 d12 = make_double2(z[1].x - z[2].x, z[1].y - z[2].y);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                const double ex = fma(defscheme::LS[q][1], s12.x, defscheme::LS[q][0] * s03.x);
-                const double ey = fma(defscheme::LS[q][1], s12.y, defscheme::LS[q][0] * s03.y);
-                const double ox = fma(defscheme::LD[q][1], d12.x, defscheme::LD[q][0] * d03.x);
-                const double oy = fma(defscheme::LD[q][1], d12.y, defscheme::LD[q][0] * d03.y);
+                const double ex = fma(dsv::LS[q][1], s12.x, dsv::LS[q][0] * s03.x);
+                const double ey = fma(dsv::LS[q][1], s12.y, dsv::LS[q][0] * s03.y);
+                const double ox = fma(dsv::LD[q][1], d12.x, dsv::LD[q][0] * d03.x);
+                const double oy = fma(dsv::LD[q][1], d12.y, dsv::LD[q][0] * d03.y);
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     const int qq = side ? 5 - q : q;
@@ -360,11 +456,16 @@ struct March3 {
         // other thread's data, so a warp that finished the previous row early does this
         // share (~40 % of the row's FP64 work) while slower warps of the CTA catch up.
         cp_async_wait<G::P - 1>();
-        zw[S_NEW][0] = zu0[slot_new * G::ZW + cc];
+#if MB4_BULK
+        // this segment's z row j (use j / S of its slot); the unroll by 3 runs up to two
+        // iterations past the last row, which read no new row
+        if (j < s.nzrows) mbar_wait(&bars[slot_new], (j / G::S) & 1);
+#endif
+        zw[S_NEW][0] = zu0[slot_new * G::ZWP + cc];
         vw[S_NEW] = zv[slot_new * G::ZW + cc];
         if (!FIRST) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZW + cc];
+            for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZWP + cc];
         }
         double2 cub[3];  // cubic term at the 6 Gauss nodes of the collocation polynomial
         if (!FIRST && MB4_CUBIC_EARLY) cubic_site(cf, zw[S_CEN], cub);
@@ -393,7 +494,7 @@ struct March3 {
         const double2 u0c = zw[S_CEN][0];
         double2 pb[3];
         {
-            const double2 w0 = cf.kv(d0, u0c, zu0[slot_cen * G::ZW + cc - 1], zu0[slot_cen * G::ZW + cc + 1],
+            const double2 w0 = cf.kv(d0, u0c, zu0[slot_cen * G::ZWP + cc - 1], zu0[slot_cen * G::ZWP + cc + 1],
                                      zw[S_DN][0], zw[S_NEW][0]);
             if (FIRST) {
                 // f(u0)/scale = -i(w0 - g |u0|^2 u0); phibar_k = fs_k * f
@@ -431,7 +532,7 @@ struct March3 {
                 w[0] = w0;
 #pragma unroll
                 for (int q = 1; q < 4; ++q) {
-                    const double2* row = zU + (slot_cen * 3 + (q - 1)) * G::ZW;
+                    const double2* row = zU + (slot_cen * 3 + (q - 1)) * G::ZWP;
                     z[q] = zw[S_CEN][q];
                     w[q] = cf.kv(d0, z[q], row[cc - 1], row[cc + 1], zw[S_DN][q], zw[S_NEW][q]);
                 }
@@ -472,13 +573,21 @@ struct March3 {
         {
             const double2 u0m = zw[S_DN][0];          // u0 of row i - 1 (z row j - 2)
             const double dm = cf.dv(vw[S_DN]);
+#if MB4_LATER_PQR
+            const auto K1 = cf.pqr(dm, u0m);  // J at the site, formed once for the 3 stages
+#endif
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const double2* prow = pub_row(0, ppar, k);  // phibar row i - 1
                 const double2 tc = prow[cc];
                 const double2 td = M == 2 ? pb_m2[k] : pub_row(0, par, k)[cc];  // row i - 2
+#if MB4_LATER_PQR
+                const double2 jk = cf.jt_pqr(K1, tc, cf.nsum(prow[cc - 1], prow[cc + 1], td, pb[k]));
+                b1[k] = make_double2(fma(cf.hl(k), jk.x, tc.x), fma(cf.hl(k), jk.y, tc.y));
+#else
                 const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], td, pb[k]);
                 b1[k] = cf.horner(k, tc, tc, ak, u0m);
+#endif
             }
         }
         // publish phibar row i (after the own-column history reads above)
@@ -504,22 +613,30 @@ struct March3 {
         // ---- level 2 at row i - 2 (final, M == 2) -------------------------------
         if (out_ok) {
             const int slot_m3 = ring(3);             // z row j - 3 == row i - 2
-            const double2 u0m = zu0[slot_m3 * G::ZW + cc];
+            const double2 u0m = zu0[slot_m3 * G::ZWP + cc];
             const double dm = cf.dv(zv[slot_m3 * G::ZW + cc]);
             double2 b2[3];
+#if MB4_LATER_PQR
+            const auto K2 = cf.pqr(dm, u0m);
+#endif
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const double2* prow = pub_row(1, ppar, k);  // b1 row i - 2
                 const double2 tc = prow[cc];
+#if MB4_LATER_PQR
+                const double2 jk = cf.jt_pqr(K2, tc, cf.nsum(prow[cc - 1], prow[cc + 1], b1_m3[k], b1[k]));
+                b2[k] = make_double2(fma(cf.hl2(k), jk.x, pb_m2[k].x), fma(cf.hl2(k), jk.y, pb_m2[k].y));
+#else
                 const double2 ak = cf.kv(dm, tc, prow[cc - 1], prow[cc + 1], b1_m3[k], b1[k]);
                 b2[k] = cf.template horner<2>(k, pb_m2[k], tc, ak, u0m);
+#endif
             }
             double2 tb[3];
             cf.from_eigen(b2, tb);  // r = -T b2
             const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZW + cc];
+                const double2 uo = FIRST ? u0m : zU[(slot_m3 * 3 + q) * G::ZWP + cc];
                 if ((s.smask >> q) & 1) uout[q][gi] = make_double2(uo.x - tb[q].x, uo.y - tb[q].y);
                 track(rmax, tb[q]);
             }
@@ -555,10 +672,30 @@ struct March3 {
             const int ca = xa + a.ghost, cb = xb + a.ghost;
             s.gxa = ca < last ? ca : last;
             s.gxb = cb < last ? cb : last;
+            s.gx0 = xz0 + a.ghost;
         } else {
             s.gxa = wrap_index(xa, a.nx);
             s.gxb = wrap_index(xb, a.nx);
+            s.gx0 = wrap_index(xz0, a.nx);
         }
+#if MB4_ALIGN_RING
+        // column c of the ring rows at the alignment of global column gx0 + c (mod 128 B;
+        // exact when the row pitch is a multiple of 8 sites, as for every BASELINE lattice)
+        {
+            const int su0 = static_cast<int>(smem_u32(zu0_base) >> 4), sU = static_cast<int>(smem_u32(zU_base) >> 4);
+            zu0 = zu0_base + ((s.gx0 - su0) & 7);
+            zU = zU_base + ((s.gx0 - sU) & 7);
+        }
+#endif
+#if MB4_BULK
+        // fresh ring barriers per segment (every row of the previous segment was consumed)
+        if (t == 0) {
+#pragma unroll
+            for (int q = 0; q < G::S; ++q) mbar_init(&bars[q], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+#endif
 #pragma unroll
         for (int k = 0; k < G::P; ++k) issue_row(a, uin, s, k, k);
         const int jend = R + 2 * M + 2;
@@ -869,19 +1006,40 @@ struct MarchFirst2 {
     __host__ __device__ static constexpr int pow2ceil(int x) { return x <= 1 ? 1 : 2 * pow2ceil((x + 1) / 2); }
     __host__ __device__ static constexpr int depth(int n) { return n >= MF - 2 ? 2 : pow2ceil(MF - n + 1); }
     __host__ __device__ static constexpr int hrow(int n) { return n == 0 ? 0 : hrow(n - 1) + depth(n - 1); }
-    static constexpr size_t bytes = static_cast<size_t>(H0) + static_cast<size_t>(hrow(MF)) * RB + PAD;
+    // + 128: the per-segment alignment shift of every ring (MB4_ALIGN_RING)
+    static constexpr size_t bytes = static_cast<size_t>(H0) + static_cast<size_t>(hrow(MF)) * RB + PAD + 128;
 
-    unsigned char* sm;  // dynamic shared memory
+    unsigned char* sm;   // dynamic shared memory, shifted per segment (MB4_ALIGN_RING)
+    unsigned char* sm0;  // its unshifted base
     // own-column u0 / V of z rows j, j-1, ..., j-MF-1: level N reads row j-N-1, which
     // level N-1 read one iteration earlier, so the rows move down a register pipeline
     // (one shift per iteration) instead of being re-read from the ring per level
     // (30 shared-memory wavefronts per warp-row at MF = 6; the sweep is L1-bound)
+#if MB4_FIRST_PQR
+    // own-column u0 of z rows j, j-1, j-2 (level 0's stencil) and V of rows j, j-1;
+    // the J coefficients (P, Q, R) of z rows j-2 .. j-MF-1 move down a register
+    // pipeline (level N reads row j-N-1's, formed by level 0 N iterations earlier)
+    static constexpr int NZW = 3;
+    double2 zw[NZW];
+    double vw[NZW];
+    typename Coef<ISO>::PQR kw[MF + 2];  // kw[k]: z row j - k, k >= 2
+#else
     static constexpr int NZW = MB4_FIRST_REGZ ? MF + 2 : 3;
     double2 zw[NZW];
     double vw[NZW];
+#endif
     double2 gp[MF][2];  // own-column g_n of the last two iterations (slot = parity)
 
-    __device__ MarchFirst2(unsigned char* smem) : sm(smem) {}
+#if MB4_BULK
+    unsigned long long* bars;  // one mbarrier per z ring slot (bulk u0 row copies)
+    __device__ static unsigned long long* ring_bars() {
+        __shared__ unsigned long long b[SZ];
+        return b;
+    }
+    __device__ MarchFirst2(unsigned char* smem) : sm(smem), sm0(smem), bars(ring_bars()) {}
+#else
+    __device__ MarchFirst2(unsigned char* smem) : sm(smem), sm0(smem) {}
+#endif
 
     __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
         if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
@@ -893,6 +1051,7 @@ struct MarchFirst2 {
     struct Seg {
         int X0, Y0, R, nzrows, gx, next_row;
         int xlim;
+        int gx0;  // global column of lane 0 (wrapped; ghost-padded in GHOST mode)
         size_t next_off;
     };
 
@@ -909,7 +1068,16 @@ struct MarchFirst2 {
             }
             const int slot = k & (SZ - 1);
             const size_t g = rowoff + s.gx;
+#if MB4_BULK
+            if (threadIdx.x == 0) {
+                const int w = GHOST ? a.pitch : a.nx;
+                mbar_arrive_expect_tx(&bars[slot], bulk_row_bytes<!GHOST>(s.gx0, NT, w));
+                bulk_row<!GHOST>(reinterpret_cast<double2*>(sm + ZU + slot * RB), a.u0 + rowoff, s.gx0, NT, w,
+                                 &bars[slot]);
+            }
+#else
             cp_async16(sm + ZU + slot * RB + threadIdx.x * 16, a.u0 + g);
+#endif
             cp_async8(sm + ZV + slot * (RB / 2) + threadIdx.x * 8, a.V + g);
         }
         cp_async_commit();
@@ -934,6 +1102,9 @@ struct MarchFirst2 {
             unsigned char* own = smt + HB + so;   // g_n, iteration j
             const double2 gc = gp[n][PAR ^ 1];
             const double2 gd = gp[n][PAR];
+#if MB4_FIRST_PQR
+            const double2 gn = cf.jt_pqr(kw[N + 1], gc, cf.nsum(ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up));
+#else
             double2 u0n;
             double vn;
             if (N == 1 || MB4_FIRST_REGZ) {
@@ -946,13 +1117,12 @@ struct MarchFirst2 {
             }
             const double2 an = cf.kv(cf.dv(vn), gc, ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up);
             const double2 gn = cf.jt(gc, an, u0n);
+            if (N == MF) ch.u0o = u0n;
+#endif
             ref<double2>(own) = ch.up;
             gp[n][PAR] = ch.up;
             if (N == MF - 1) ch.low = gd;
-            if (N == MF) {
-                ch.mid = gc;
-                ch.u0o = u0n;
-            }
+            if (N == MF) ch.mid = gc;
             ch.up = gn;
             levels<N + 1, PAR>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
         }
@@ -977,6 +1147,9 @@ struct MarchFirst2 {
         unsigned char* smt = sm + t * 16;
         unsigned char* smv = sm + t * 8;
         cp_async_wait<P - 1>();
+#if MB4_BULK
+        mbar_wait(&bars[j & (SZ - 1)], (j / SZ) & 1);
+#endif
         __syncthreads();
         issue_row(a, s, j + P);
 
@@ -997,7 +1170,8 @@ struct MarchFirst2 {
         // ---- level 0 at row i: f(u0) and the energy monitor --------------------
         const double v = vw[1];
         const double2 u0c = zw[1];
-        const double2 w0 = cf.kv(cf.dv(v), u0c, ref<double2>(smt + ZU + zc - 16), ref<double2>(smt + ZU + zc + 16),
+        const double d0 = cf.dv(v);
+        const double2 w0 = cf.kv(d0, u0c, ref<double2>(smt + ZU + zc - 16), ref<double2>(smt + ZU + zc + 16),
                                  zw[2], zw[0]);
         const double n2 = fma(u0c.x, u0c.x, u0c.y * u0c.y);
         const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
@@ -1023,7 +1197,12 @@ struct MarchFirst2 {
             gout[MF - 2] = ch.low;
             gout[MF - 1] = ch.mid;
             gout[MF] = ch.up;
+#if MB4_FIRST_PQR
+            // u0 of the output row (z row j - MF - 1) from the ring (BACK = MF + 1 rows kept)
+            const double2 u0o = ref<double2>(smt + ZU + ((jrb - (MF + 1) * RB) & (SZ * RB - 1)));
+#else
             const double2 u0o = ch.u0o;
+#endif
             const size_t gi = at(a, xout, s.Y0 + yrel);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -1037,6 +1216,11 @@ struct MarchFirst2 {
                 March3<MF, NT, true, ISO, GHOST>::track(rmax, make_double2(rx, ry));
             }
         }
+#if MB4_FIRST_PQR
+#pragma unroll
+        for (int k = MF + 1; k > 2; --k) kw[k] = kw[k - 1];
+        kw[2] = cf.pqr(d0, u0c);  // z row j - 1 becomes row j - 2 for level 1
+#endif
 #pragma unroll
         for (int k = NZW - 1; k > 0; --k) {
             zw[k] = zw[k - 1];
@@ -1058,11 +1242,25 @@ struct MarchFirst2 {
             s.next_off = static_cast<size_t>(yz0 + a.ghost) * a.pitch;
             const int last = a.pitch - 1, ca = xz + a.ghost;
             s.gx = ca < last ? ca : last;
+            s.gx0 = X0 - MF - 1 + a.ghost;
         } else {
             s.next_row = wrap_index(yz0, a.ny);
             s.next_off = static_cast<size_t>(s.next_row) * a.nx;
             s.gx = wrap_index(xz, a.nx);
+            s.gx0 = wrap_index(X0 - MF - 1, a.nx);
         }
+#if MB4_ALIGN_RING
+        // lane t's u0 ring entry at the alignment of its global source modulo 128 B
+        sm = sm0 + 16 * ((s.gx0 - static_cast<int>((smem_u32(sm0) + ZU) >> 4)) & 7);
+#endif
+#if MB4_BULK
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int q = 0; q < SZ; ++q) mbar_init(&bars[q], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+#endif
 #pragma unroll
         for (int k = 0; k < P; ++k) issue_row(a, s, k);
         const int jend = R + 2 * MF + 2;

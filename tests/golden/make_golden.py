@@ -11,7 +11,8 @@ Sources (nothing here is hand-written data):
   ref_methods_cfg1_5.npz -- the same library's StepDriver(RK4 / GAUSS2 / GAUSS4 /
                         AVF2 / AVF4), direct solver, 5 cfg1 steps.
   ref_cfg4_sub.npz   -- the reference library on the full cfg4 lattice (4096^2, V_d ~
-                        U[5,50), 4 packets; GMRES, 3 workers, ~15 min here), 10 steps:
+                        U[5,50), 4 packets; GMRES, 1 worker: 3 workers' GMRES storage exceeds
+                        this container's 62 GB), 10 steps:
                         the full energy record and a deterministic subsample of the
                         state after steps 1 and 10 (every CFG4_STRIDE-th site) plus
                         whole-state checksums (sum |u|^2, sum u).
@@ -111,13 +112,13 @@ def cfg4_case(nsteps=10):
     cfg = configs.CONFIGS["cfg4"]
     V, psi = configs.make_inputs(cfg)
     idx = np.arange(0, cfg.sites, CFG4_STRIDE, dtype=np.int64)
-    out = {"input_sha256": input_digest(V, psi), "solver": "gmres", "workers": 3, "nsteps": nsteps,
+    out = {"input_sha256": input_digest(V, psi), "solver": "gmres", "workers": 1, "nsteps": nsteps,
            "stride": CFG4_STRIDE, "idx": idx}
     u = psi
     obs_series, iters_all, done = [], [], 0
     for m in (1, nsteps):
         u, obs, iters, secs = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, u, cfg.dt,
-                                        m - done, eps=cfg.epsilon, solver="gmres", workers=3)
+                                        m - done, eps=cfg.epsilon, solver="gmres", workers=1)
         print(f"cfg4: steps {done}..{m} in {secs:.1f} s, Newton iterations {iters.tolist()}", flush=True)
         obs_series.append(obs if done == 0 else obs[1:])
         iters_all.extend(iters.tolist())

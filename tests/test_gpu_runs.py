@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from energy_ref import energy_ld
 from paper_2003_04345_b200 import configs, nls2d
 
 pytestmark = pytest.mark.gpu
@@ -132,7 +133,21 @@ def test_cfg3_ten_steps_against_reference():
     r10, robs, _, _ = O.ref_run(cfg.nx, cfg.ny, float(cfg.nx), float(cfg.ny), cfg.gamma, V, r1, cfg.dt, 9,
                                 eps=cfg.epsilon, solver="gmres", workers=3)
     assert rel(u10, r10) <= 1e-10
-    assert np.abs(obs[:, 3] - robs[:, 3]).max() <= 1e-13 * abs(robs[0, 3])
+    check_energy_records(cfg, V, obs, robs, u10)
+
+
+def check_energy_records(cfg, V, obs, robs, u_last):
+    """Energy records at >= 1e6 sites: the reference's sequential double sums carry
+    O(sqrt(N) eps |H|) rounding (~1e-13 |H| at 1024^2), a constant offset in its record.
+    So: the drift records H(t) - H(t0) agree within 1e-13 |H0| (north_star); the GPU's
+    H of the last state is within 1e-15 relative of an extended-precision evaluation;
+    the two absolute records agree within the reference's monitor rounding, bounded by
+    8 sqrt(N) eps |H0| (measured: 0.8 sqrt(N) eps at 1024^2, 0.6 sqrt(N) eps at 4096^2)."""
+    H0 = abs(robs[0, 3])
+    assert np.abs((obs[:, 3] - obs[0, 3]) - (robs[:, 3] - robs[0, 3])).max() <= 1e-13 * H0
+    assert np.abs(obs[:, 3] - robs[:, 3]).max() <= 8.0 * np.sqrt(cfg.sites) * 2.0 ** -52 * H0
+    H_ld = energy_ld(u_last, V, cfg.gamma, cfg.nx, cfg.ny)
+    assert abs(obs[-1, 3] - H_ld) <= 1e-15 * abs(H_ld), (obs[-1, 3], H_ld, robs[-1, 3])
 
 
 def test_cfg4_ten_steps_against_reference_fixture():
@@ -155,7 +170,7 @@ def test_cfg4_ten_steps_against_reference_fixture():
         assert rel(u[idx], g[f"sub_{k}"]) <= 1e-10
         assert abs(np.vdot(u, u).real - float(g[f"norm2_{k}"])) <= 1e-12 * float(g[f"norm2_{k}"])
         assert abs(u.sum() - complex(g[f"sum_{k}"])) <= 1e-10 * np.sqrt(u.size * float(g[f"norm2_{k}"]))
-    assert np.abs(obs[:, 3] - g["obs"][1:, 3]).max() <= 1e-13 * abs(g["obs"][0, 3])
+    check_energy_records(cfg, V, obs, g["obs"][1:], u10)
 
 
 def test_nonconvergence_leaves_state_unchanged_and_reports_residual():
