@@ -62,6 +62,15 @@ struct mb4cu_ctx {
     double* d_obs_march = nullptr;             // [grid][kObsFields]
     mb4cu::StepStatus* d_status = nullptr;
     mb4cu::StepStatus* h_status = nullptr;     // pinned
+    bool batched = true;                       // mb4cu_run enqueues steps device-resident
+    int obs_grid = 0;                          // CTAs d_obs_march holds partial sums for
+    // batched stepping (mb4cu_run): per-step status and residual slots, the abort flag and
+    // per-step events, allocated on first use
+    mb4cu::StepStatus* d_bstatus = nullptr;
+    mb4cu::StepStatus* h_bstatus = nullptr;   // pinned
+    unsigned long long* d_brmax = nullptr;     // [kBatch][max_iters]
+    int* d_babort = nullptr;
+    cudaEvent_t bev[65] = {};
     bool obs_cached = false;                   // energy sums of the current u0 known
     double obs_cache[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
     double entry_obs[mb4cu::kObsFields] = {0, 0, 0, 0, 0};
@@ -1187,6 +1196,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     ctx->max_halvings = p->max_step_halvings;
     ctx->m = m;
     ctx->kernel = p->kernel;
+    ctx->batched = std::getenv("MB4CU_NO_BATCH") == nullptr;  // A/B switch for the bench
     ctx->ghost = p->ghost;
     if (p->kernel < 0 || p->kernel > 3) {
         g_create_error = "mb4cu_create: kernel must be 0 (default), 1 (tiled), 2 (march v1) or 3 (Newton-Krylov)";
@@ -1275,6 +1285,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
             return bail(e, "cudaMalloc(rmax_arr)");
         if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * grid)) != cudaSuccess)
             return bail(e, "cudaMalloc(obs_march)");
+        ctx->obs_grid = grid;
         if ((e = cudaMalloc(&ctx->d_status, sizeof(mb4cu::StepStatus))) != cudaSuccess)
             return bail(e, "cudaMalloc(status)");
         if ((e = cudaMallocHost(&ctx->h_status, sizeof(mb4cu::StepStatus))) != cudaSuccess)
@@ -1322,6 +1333,12 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs_march);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
+    cudaFree(ctx->d_bstatus);
+    cudaFreeHost(ctx->h_bstatus);
+    cudaFree(ctx->d_brmax);
+    cudaFree(ctx->d_babort);
+    for (auto& ev : ctx->bev)
+        if (ev) cudaEventDestroy(ev);
     kr_free(ctx);
     krb_free(ctx);
     if (ctx->fft.have1) cufftDestroy(ctx->fft.plan1);
@@ -1347,6 +1364,18 @@ int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m) {
         (ctx->ghost > 0 && m + 1 > ctx->ghost))
         return fail(ctx, MB4CU_INVALID, "set_neumann_terms: production kernel, m in 0..2 with a compiled "
                                         "(neumann_first, m) pair and m + 1 <= ghost");
+    // the first sweeps write one energy partial per CTA: the grid of the new (mf, m)
+    // pair must fit the buffer sized at create time (reallocate if it does not)
+    const int grid = mb4cu::march2_grid_size(ctx->mf, m, ctx->device);
+    if (grid > ctx->obs_grid) {
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        double* fresh = nullptr;
+        MB4_CUDA(ctx, cudaMalloc(&fresh, sizeof(double) * mb4cu::kObsFields * grid));
+        cudaFree(ctx->d_obs_march);
+        ctx->d_obs_march = fresh;
+        ctx->obs_grid = grid;
+    }
+    if (m != ctx->m) ctx->last_sweeps = 0;  // as adapt_neumann: no speculative sweep right after a switch
     ctx->m = m;
     ctx->m_auto = false;  // the caller drives the depth from now on
     return MB4CU_OK;
@@ -1553,6 +1582,108 @@ static void put_obs(double* row, const mb4cu_obs& o) {
     row[6] = o.raw_quartic;
 }
 
+namespace {
+
+constexpr int kBatch = 64;  // steps enqueued per host round trip (mb4cu_run)
+
+// Steps mb4cu_run may enqueue without waiting: the production sweep path of a whole
+// lattice, non-stiff, with a known sweep count to predict from.
+bool batchable(const mb4cu_ctx* ctx, double h) {
+    return ctx->kernel == 0 && ctx->ghost == 0 && ctx->last_sweeps >= 1 && mb4cu::march2_supported(ctx->mf, ctx->m) &&
+           !stiff_step(ctx, h);
+}
+
+int batch_alloc(mb4cu_ctx* ctx) {
+    if (ctx->d_bstatus) return MB4CU_OK;
+    MB4_CUDA(ctx, cudaMalloc(&ctx->d_bstatus, sizeof(mb4cu::StepStatus) * kBatch));
+    MB4_CUDA(ctx, cudaMallocHost(&ctx->h_bstatus, sizeof(mb4cu::StepStatus) * kBatch));
+    MB4_CUDA(ctx, cudaMalloc(&ctx->d_brmax, sizeof(unsigned long long) * kBatch * ctx->max_iters));
+    MB4_CUDA(ctx, cudaMalloc(&ctx->d_babort, sizeof(int)));
+    for (auto& ev : ctx->bev) MB4_CUDA(ctx, cudaEventCreate(&ev));
+    return MB4CU_OK;
+}
+
+// Device-resident stepping: up to kBatch steps of size h enqueued back to back, with
+// one host round trip at the end.  Each step is launched on the buffers of the sweep
+// count of the step before it (the same prediction substep_march makes for its
+// speculative final sweep); the step's last launch ends the batch on the device (the
+// later launches return at once) when the step did not converge, took another sweep
+// count, or made the adaptive depth switch.  The host then commits the steps that ran,
+// in order, exactly as the one-step path does -- the results are bit-identical to
+// stepping one at a time -- and the caller steps the rest (a failed step goes through
+// mb4cu_step's fallbacks).  Returns the steps committed in *done.
+int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, mb4cu_stats* stats, int* done) {
+    *done = 0;
+    if (int rc = batch_alloc(ctx)) return rc;
+    int B = std::min(nmax, kBatch);
+    if (ctx->m_auto && ctx->m == 2) B = std::min(B, std::max(1, 64 - ctx->auto_steps));
+    const int expect = ctx->last_sweeps;
+    const int spec = expect >= 2 ? expect - 1 : -1;
+    const mb4cu::BatchCtl ctl{ctx->d_babort, expect, ctx->m_auto && ctx->m == 1 ? 4 : 0};
+    const SweepConsts c = make_consts(ctx, h);
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_babort, 0, sizeof(int), ctx->stream));
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_bstatus, 0, sizeof(mb4cu::StepStatus) * B, ctx->stream));
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_brmax, 0, sizeof(unsigned long long) * B * ctx->max_iters, ctx->stream));
+    const double2* u0p = ctx->u0;
+    double2* Up[2][3];
+    std::memcpy(Up, ctx->U, sizeof(Up));
+    const int set = (expect - 1) & 1;
+    MB4_CUDA(ctx, cudaEventRecord(ctx->bev[0], ctx->stream));
+    for (int k = 0; k < B; ++k) {
+        MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, u0p, ctx->V, Up,
+                                                ctx->d_brmax + static_cast<size_t>(k) * ctx->max_iters,
+                                                ctx->d_obs_march, ctx->d_bstatus + k, ctx->max_iters, ctx->eps, 1, c,
+                                                ctx->device, ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, &ctl));
+        MB4_CUDA(ctx, cudaEventRecord(ctx->bev[k + 1], ctx->stream));
+        // the predicted commit: u0 <-> U[set][2]
+        double2* nu0 = Up[set][2];
+        Up[set][2] = const_cast<double2*>(u0p);
+        u0p = nu0;
+    }
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_bstatus, ctx->d_bstatus, sizeof(mb4cu::StepStatus) * B,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const int launches = mb4cu::march2_launches(ctx->mf, 0, 0, ctx->max_iters);
+    if (ctx->profiling) ctx->prof.launches += launches * B;
+    for (int k = 0; k < B; ++k) {
+        const mb4cu::StepStatus& st = ctx->h_bstatus[k];
+        if (st.sweeps == 0 || !st.converged || !std::isfinite(st.rlast)) break;  // not run, or failed
+        float ms = 0.f;
+        MB4_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->bev[k], ctx->bev[k + 1]));
+        if (ctx->profiling) {
+            ctx->prof.kernel_ms += ms;
+            ctx->prof.sweeps += st.sweeps;
+            const bool spec_hit = st.sweeps - 1 == spec && spec >= 1;
+            ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (st.sweeps - 1) - (spec_hit ? 32.0 : 0.0));
+            ctx->prof.redone += st.redone;
+            for (int q = 0; q < st.sweeps && q < 8; ++q) {
+                ctx->prof.sweep_ms[q] += 1e-6 * static_cast<double>(st.t[q + 1] - st.t[q]);
+                ctx->prof.sweep_n[q] += 1;
+            }
+        }
+        std::swap(ctx->u0, ctx->U[st.set][2]);
+        ctx->obs_cached = false;
+        ctx->last_sweeps = st.sweeps;
+        adapt_neumann(ctx, st.sweeps);
+        std::memcpy(ctx->entry_obs, st.obs, sizeof(ctx->entry_obs));
+        if (obs_rows) {
+            mb4cu_obs o{};
+            if (int rc = finish_obs(ctx, st.obs, &o)) return rc;
+            put_obs(obs_rows + 7 * k, o);
+        }
+        if (iters) iters[k] = st.sweeps;
+        if (stats) {
+            stats->newton_iters += st.sweeps;
+            stats->solve_seconds += 1e-3 * ms;
+            stats->last_residual = st.rlast;
+        }
+        ++*done;
+    }
+    return MB4CU_OK;
+}
+
+}  // namespace
+
 int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* iters_series,
               mb4cu_stats* stats) {
     if (!ctx) return MB4CU_INVALID;
@@ -1565,7 +1696,19 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
     const bool fused = (ctx->kernel == 0 && !stiff_step(ctx, h)) || ctx->kernel == 2;
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     for (int s = 1; s <= nsteps; ++s) {
+        if (ctx->batched && batchable(ctx, h)) {
+            int done = 0;
+            if (int rc = run_batch(ctx, h, nsteps - s + 1, obs_series ? obs_series + 7 * (s - 1) : nullptr,
+                                   iters_series ? iters_series + (s - 1) : nullptr, stats, &done))
+                return rc;
+            if (done > 0) {
+                s += done - 1;  // (the loop advances past the last committed step)
+                continue;
+            }
+            // the batch's first step failed: it goes through the one-step path below
+        }
         if (obs_series && !fused) {
             const int rc0 = mb4cu_observables(ctx, &o);
             if (rc0) return rc0;

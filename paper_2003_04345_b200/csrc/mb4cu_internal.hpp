@@ -153,6 +153,21 @@ struct StepArgs {
     int grid_cap;               // host side: at most this many CTAs (0 = full occupancy), e.g.
                                 // to leave SMs to NCCL kernels running concurrently
     int obs_blocks;             // blocks that wrote obs_partial (0: this launch's grid)
+    // Batched (device-resident) stepping: the host enqueues several steps without
+    // waiting, each with the buffers of the sweep count it predicts.  A launch whose
+    // batch_abort flag is set does nothing; the status-writing launch of a step sets it
+    // when the step did not converge, took another sweep count than expect_sweeps, or
+    // reached switch_sweeps (the adaptive Neumann depth changes after it).
+    int* batch_abort;           // nullptr: not batched
+    int expect_sweeps;
+    int switch_sweeps;          // 0: none
+};
+
+// batch control of launch_step_march2 (see StepArgs::batch_abort)
+struct BatchCtl {
+    int* abort;
+    int expect_sweeps;
+    int switch_sweeps;
 };
 
 // ---- the other integrators (methods.cu) ------------------------------------
@@ -216,7 +231,8 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
-                               const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0);
+                               const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0,
+                               const BatchCtl* batch = nullptr);
 int march2_grid_size(int mf, int m, int device);
 
 // Halo transfer between a padded sub-domain array set and a contiguous buffer

@@ -1372,6 +1372,9 @@ template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH>
 __global__ void __launch_bounds__(NT, (KGeom<MF, M, NT, PH>::MINB))
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
+    // a batched step after one that ended the batch: nothing to do (the flag was set by
+    // an earlier launch on this stream, so every CTA of this grid reads the same value)
+    if (a.batch_abort && *reinterpret_cast<volatile const int*>(a.batch_abort)) return;
     cg::grid_group grid = cg::this_grid();
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #if MB4_CONSTS_IN_SMEM
@@ -1492,6 +1495,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         // a non-finite residual (NaN update somewhere) is reported as +inf: the MAX
         // all-reduce of a decomposed lattice (fmax) would drop a NaN, never an inf
         a.status->rlast = isfinite(rlast) ? rlast : __longlong_as_double(0x7FF0000000000000ll);
+        if (a.batch_abort &&
+            (!converged || sweeps != a.expect_sweeps || (a.switch_sweeps > 0 && sweeps >= a.switch_sweeps)))
+            *a.batch_abort = 1;
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
         double v = 0.0;
@@ -1651,8 +1657,13 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
-                               int obs_accumulate, int grid_cap) {
+                               int obs_accumulate, int grid_cap, const BatchCtl* batch) {
     StepArgs a{};
+    if (batch) {
+        a.batch_abort = batch->abort;
+        a.expect_sweeps = batch->expect_sweeps;
+        a.switch_sweeps = batch->switch_sweeps;
+    }
     a.nrect = nrect;
     for (int r = 0; r < nrect && r < 4; ++r)
         for (int k = 0; k < 4; ++k) a.rect[r][k] = rects[r][k];

@@ -314,3 +314,54 @@ def test_quarter_billion_site_lattice():
     H = obs[:, 3]
     assert np.abs(H - H[0]).max() / abs(H[0]) <= 1e-13
     assert abs(obs[-1, 4] - obs[0, 4]) <= 1e-13 * obs[0, 4]  # probability
+
+
+def _run_with(cfg, V, psi, nsteps, batched, monkeypatch, **kw):
+    if batched:
+        monkeypatch.delenv("MB4CU_NO_BATCH", raising=False)
+    else:
+        monkeypatch.setenv("MB4CU_NO_BATCH", "1")
+    with session(cfg, V, **kw) as s:
+        s.set_state(psi)
+        obs, iters = s.run(cfg.dt, nsteps)
+        return obs, iters, s.get_state()
+
+
+@pytest.mark.parametrize("name,nsteps", [("cfg1", 70), ("cfg2", 40), ("cfg3", 12)])
+def test_batched_run_is_bit_identical_to_step_by_step(name, nsteps, monkeypatch):
+    """mb4cu_run enqueues up to 64 steps per host round trip (device-resident batches,
+    ended on the device when a step's sweep count changes or the adaptive depth switches);
+    the committed trajectory, energy record and sweep counts equal the one-step-per-round-
+    trip path bit for bit -- cfg1 crosses the depth switch and its 64-step re-probe, cfg2
+    changes its sweep count from step to step."""
+    cfg = configs.CONFIGS[name]
+    V, psi = configs.make_inputs(cfg)
+    a = _run_with(cfg, V, psi, nsteps, True, monkeypatch)
+    b = _run_with(cfg, V, psi, nsteps, False, monkeypatch)
+    assert list(a[1]) == list(b[1])
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[2], b[2])
+
+
+def test_batched_run_falls_back_on_failing_steps(monkeypatch):
+    """A step that does not converge within max_iters sweeps ends the batch on the device;
+    the host retries it through the one-step path (Newton-Krylov fallback, then halving):
+    the same trajectory as stepping one at a time (cfg2 with max_iters = 4, where a part
+    of the steps needs a fifth sweep)."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    out = []
+    for batched in (True, False):
+        if batched:
+            monkeypatch.delenv("MB4CU_NO_BATCH", raising=False)
+        else:
+            monkeypatch.setenv("MB4CU_NO_BATCH", "1")
+        with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), nls2d.NewtonConfig(cfg.epsilon, 4, 4)) as s:
+            s.set_state(psi)
+            obs, iters = s.run(cfg.dt, 16)
+            out.append((obs, iters, s.get_state()))
+    (oa, ia, ua), (ob, ib, ub) = out
+    assert list(ia) == list(ib)
+    assert max(ia) > 4  # some steps took the fallback (their count includes the failed sweeps)
+    assert np.array_equal(oa, ob)
+    assert np.array_equal(ua, ub)
