@@ -192,6 +192,11 @@ int mb4cu_spectral_bound(mb4cu_ctx* ctx, double* rho);
  * (m = 2 once a step needs >= 4 sweeps at m = 1, back to 1 after 64 steps) through it. */
 int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m);
 int mb4cu_set_spectral_bound(mb4cu_ctx* ctx, double rho);
+/* max|u0|^2 the context's spectral bound and stiffness test use from now on.  A whole
+ * lattice tracks it itself (every step's first sweep measures its entry state, and the
+ * next step uses it); a decomposed lattice passes the all-reduced (max) value of the
+ * last step's dev_out7[6] to every rank, then agrees on the bound as above. */
+int mb4cu_set_amax2(mb4cu_ctx* ctx, double amax2);
 
 /* ---- Sub-domain (multi-GPU) stepping, ghost > 0 ---------------------------------
  * The caller owns the decomposition and the exchange (paper_2003_04345_b200/dist.py
@@ -215,22 +220,23 @@ int mb4cu_halo_unpack(mb4cu_ctx* ctx, int field, int side, const double* dev_buf
 int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* local_sums5);
 /* Accept the iterate after `sweeps` sweeps as the step result (u0 <- U3). */
 /* Asynchronous sweep for device-side collectives: enqueues sweep s on the context
- * stream and a copy of [local ||r||_inf, 5 local energy sums of u0 (s = 0 only)]
- * into dev_out6 (device memory), without a host synchronisation, so the caller
+ * stream and a copy of [local ||r||_inf, 5 local energy sums of u0, local max|u0|^2
+ * (the last six for s = 0 only)] into dev_out7 (device memory; 7 doubles; a non-finite
+ * residual is reported as +inf), without a host synchronisation, so the caller
  * can all-reduce the buffer on the same stream (NCCL) and read it once.
  * final_guess != 0 (s > 0): the sweep is predicted to be the last, only U3 (the
  * step result) is stored; if the reduced residual does not converge the caller
  * repeats the same sweep with final_guess = 0 before going on. */
-int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6);
+int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out7);
 /* Halo-exchange overlap: sweep s in two launches.  region 1 = the boundary frame
  * (the `ghost`-wide strips the neighbours' halos need; run it first, then start
  * exchanging them), region 2 = the interior (needs no halo; launched with at most
  * grid_cap CTAs -- 0 = all, < 0 = all but those of -grid_cap SMs -- to leave SMs to the
  * concurrent NCCL kernels) which then
- * leaves [||r||_inf over both, energy sums] in dev_out6 like mb4cu_sweep_async.
+ * leaves [||r||_inf over both, energy sums, max|u0|^2] in dev_out7 like mb4cu_sweep_async.
  * region 0 = the whole sub-domain (= mb4cu_sweep_async). */
 int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
-                       double* dev_out6);
+                       double* dev_out7);
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
 
 /* ---- Stage-split Newton-Krylov (the paper's 3-way stage partition) ---------------

@@ -169,6 +169,7 @@ def lib() -> C.CDLL:
         "mb4cu_eval_a": (D, [D, D, D]),
         "mb4cu_lagrange_basis": (I, [DP, I, D, DP]),
         "mb4cu_scheme_integrate_e": (I, [D, DP, I, DP]),
+        "mb4cu_set_amax2": (I, [P, D]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -195,5 +196,5 @@ EXPORTED = [
     "mb4cu_halo_unpack", "mb4cu_sweep", "mb4cu_sweep_async", "mb4cu_sweep_region", "mb4cu_commit_step", "mb4cu_observables_sums",
     "mb4cu_ns_begin", "mb4cu_ns_phibar", "mb4cu_ns_solve", "mb4cu_ns_get_correction", "mb4cu_ns_set_correction",
     "mb4cu_ns_update", "mb4cu_ns_commit", "mb4cu_ns_get_stages", "mb4cu_ns_abort",
-    "mb4cu_eval_a", "mb4cu_lagrange_basis", "mb4cu_scheme_integrate_e",
+    "mb4cu_eval_a", "mb4cu_lagrange_basis", "mb4cu_scheme_integrate_e", "mb4cu_set_amax2",
 ]

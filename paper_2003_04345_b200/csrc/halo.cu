@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "mb4cu_internal.hpp"
+#include "site_math.cuh"
 
 namespace mb4cu {
 namespace {
@@ -68,6 +69,7 @@ constexpr int kThreads = 256;
 __global__ void __launch_bounds__(kThreads)
 observables_ghost_kernel(const ObsArgs a, int ghost, int pitch) {
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double car[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};  // compensation (two_sum_add)
     // rows round-robin over the blocks, columns over the threads (no division)
     for (int j = blockIdx.x; j < a.ny; j += gridDim.x) {
         const size_t g0 = static_cast<size_t>(j + ghost) * pitch + ghost;
@@ -76,35 +78,22 @@ observables_ghost_kernel(const ObsArgs a, int ghost, int pitch) {
             const double2 u = a.u[g], l = a.u[g - 1], r = a.u[g + 1], d = a.u[g - pitch], up = a.u[g + pitch];
             const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (d.x + up.x)));
             const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (d.y + up.y)));
-            acc[0] += fma(u.x, kx, u.y * ky);
+            two_sum_add(acc[0], car[0], fma(u.x, kx, u.y * ky));
             acc[1] += fma(u.x, ky, -u.y * kx);
             const double n2 = fma(u.x, u.x, u.y * u.y);
-            acc[2] += n2;
-            acc[3] += n2 * n2;
-            acc[4] += a.V[g] * n2;
+            two_sum_add(acc[2], car[2], n2);
+            two_sum_add(acc[3], car[3], n2 * n2);
+            two_sum_add(acc[4], car[4], a.V[g] * n2);
         }
     }
-    __shared__ double red[kObsFields][kThreads / 32];
-#pragma unroll
-    for (int f = 0; f < kObsFields; ++f) {
-        double v = acc[f];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < kObsFields) {
-        double v = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
-        a.partial[blockIdx.x * kObsFields + threadIdx.x] = v;
-    }
+    block_csum_store<kThreads, kObsFields>(acc, car, a.partial + blockIdx.x * kObsFields);
 }
 
 __global__ void observables_ghost_finalize(const double* partial, int nblocks, double* out) {
     if (threadIdx.x < kObsFields) {
-        double v = 0.0;
-        for (int b = 0; b < nblocks; ++b) v += partial[b * kObsFields + threadIdx.x];
-        out[threadIdx.x] = v;
+        double v = 0.0, c = 0.0;
+        for (int b = 0; b < nblocks; ++b) two_sum_add(v, c, partial[b * kObsFields + threadIdx.x]);
+        out[threadIdx.x] = v + c;
     }
 }
 

@@ -58,7 +58,7 @@ struct mb4cu_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t pev0 = nullptr, pev1 = nullptr;
     // persistent-kernel path
-    unsigned long long* d_rmax_arr = nullptr;  // [max_iters]
+    unsigned long long* d_rmax_arr = nullptr;  // [max_iters + 1]: residual bits per sweep, max |u0|^2
     double* d_obs_march = nullptr;             // [grid][kObsFields]
     mb4cu::StepStatus* d_status = nullptr;
     mb4cu::StepStatus* h_status = nullptr;     // pinned
@@ -338,9 +338,18 @@ double decode_bits(unsigned long long b) {
 
 // Persistent path: the whole stage iteration of one sub-step in one cooperative
 // launch (sweep_march.cu); the host reads back a 80-byte status block.
+// Per-step spectral bound: the first sweep of every (sub)step measures max|u0|^2 of its
+// entry state in its energy monitor (no extra pass); the next (sub)step's Chebyshev
+// interval and stiffness test use it.  Only a newly set state pays a separate pass
+// (refresh_amax2), as does the step after a Newton-Krylov step (no sweep measured it).
+void track_amax2(mb4cu_ctx* ctx, double amax2) {
+    ctx->amax2 = amax2;
+    ctx->amax2_valid = true;
+}
+
 int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     const SweepConsts c = make_consts(ctx, h);
-    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * ctx->max_iters,
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long) * (ctx->max_iters + 1),
                                   ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
     // the step is predicted to converge at the previous step's sweep count: that
@@ -392,7 +401,9 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
     if (st.converged) {
         std::swap(ctx->u0, ctx->U[st.set][2]);
         ctx->obs_cached = false;
-        ctx->last_sweeps = mb4cu::march2_supported(ctx->mf, ctx->m) && ctx->kernel == 0 ? st.sweeps : 0;
+        const bool prod = mb4cu::march2_supported(ctx->mf, ctx->m) && ctx->kernel == 0;
+        ctx->last_sweeps = prod ? st.sweeps : 0;
+        if (prod) track_amax2(ctx, st.amax2);
         adapt_neumann(ctx, st.sweeps);
         return MB4CU_OK;
     }
@@ -1052,7 +1063,11 @@ int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         // default policy: matrix-free sweeps unless the step is stiff; a sweep
         // iteration that fails falls back to Newton-Krylov at the same step size
         // (the reference would not halve there), then the halving policy applies.
-        if (stiff_step(ctx, h)) return substep_krylov(ctx, h, sweeps, last_res);
+        if (stiff_step(ctx, h)) {
+            const int rck = substep_krylov(ctx, h, sweeps, last_res);
+            if (rck == MB4CU_OK) ctx->amax2_valid = false;  // no sweep measured the new state
+            return rck;
+        }
         int sw = 0;
         const int rc = substep_march(ctx, h, &sw, last_res);
         if (rc != MB4CU_NONCONVERGED) {
@@ -1061,6 +1076,7 @@ int substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         }
         int it = 0;
         const int rc2 = substep_krylov(ctx, h, &it, last_res);
+        if (rc2 == MB4CU_OK) ctx->amax2_valid = false;
         *sweeps = sw + it;
         return rc2;
     }
@@ -1281,7 +1297,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
                                 : 0);
         if (ctx->m_auto) grid = std::max(grid, mb4cu::march2_grid_size(ctx->mf, 2, ctx->device));
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
-        if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * ctx->max_iters)) != cudaSuccess)
+        if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * (ctx->max_iters + 1))) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
         if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * grid)) != cudaSuccess)
             return bail(e, "cudaMalloc(obs_march)");
@@ -1394,6 +1410,13 @@ int mb4cu_set_spectral_bound(mb4cu_ctx* ctx, double rho) {
     if (!ctx) return MB4CU_INVALID;
     if (!(rho >= 0.0) || !std::isfinite(rho)) return fail(ctx, MB4CU_INVALID, "set_spectral_bound: rho must be >= 0");
     ctx->rho_override = rho;
+    return MB4CU_OK;
+}
+
+int mb4cu_set_amax2(mb4cu_ctx* ctx, double amax2) {
+    if (!ctx) return MB4CU_INVALID;
+    if (!(amax2 >= 0.0) || !std::isfinite(amax2)) return fail(ctx, MB4CU_INVALID, "set_amax2: amax2 must be >= 0");
+    track_amax2(ctx, amax2);
     return MB4CU_OK;
 }
 
@@ -1593,11 +1616,34 @@ bool batchable(const mb4cu_ctx* ctx, double h) {
            !stiff_step(ctx, h);
 }
 
+// The max|u0|^2 values for which the step constants of h stay what they are for the
+// current ctx->amax2: the same power-of-2^(1/16) Chebyshev interval (first_poly = 2)
+// and a non-stiff step.  Shrunk by a relative 1e-9 so that the device's test never
+// disagrees with the host's rounding at a boundary (a step ending there just ends the
+// batch; the host then takes the next step on the one-step path).
+void amax2_interval(const mb4cu_ctx* ctx, double h, double* lo, double* hi) {
+    *lo = -1.0;
+    *hi = HUGE_VAL;
+    const double g3 = 3.0 * std::fabs(ctx->gamma);
+    if (g3 == 0.0) return;
+    const double base = 4.0 * ctx->cx + 4.0 * ctx->cy + ctx->vmax;
+    if (ctx->first_poly == 2 && ctx->rho_override <= 0.0) {
+        const double L = std::ceil(16.0 * std::log2(spectral_bound(ctx)));
+        *lo = (std::exp2((L - 1.0) / 16.0) - base) / g3;
+        *hi = (std::exp2(L / 16.0) - base) / g3;
+    }
+    const double lam = std::max({std::fabs(ctx->scheme.lam[0]), std::fabs(ctx->scheme.lam[1]),
+                                 std::fabs(ctx->scheme.lam[2])});
+    *hi = std::min(*hi, (kStiffKappa / (h * lam) - base) / g3);
+    *lo += 1e-9 * std::fabs(*lo);
+    *hi -= 1e-9 * std::fabs(*hi);
+}
+
 int batch_alloc(mb4cu_ctx* ctx) {
     if (ctx->d_bstatus) return MB4CU_OK;
     MB4_CUDA(ctx, cudaMalloc(&ctx->d_bstatus, sizeof(mb4cu::StepStatus) * kBatch));
     MB4_CUDA(ctx, cudaMallocHost(&ctx->h_bstatus, sizeof(mb4cu::StepStatus) * kBatch));
-    MB4_CUDA(ctx, cudaMalloc(&ctx->d_brmax, sizeof(unsigned long long) * kBatch * ctx->max_iters));
+    MB4_CUDA(ctx, cudaMalloc(&ctx->d_brmax, sizeof(unsigned long long) * kBatch * (ctx->max_iters + 1)));
     MB4_CUDA(ctx, cudaMalloc(&ctx->d_babort, sizeof(int)));
     for (auto& ev : ctx->bev) MB4_CUDA(ctx, cudaEventCreate(&ev));
     return MB4CU_OK;
@@ -1619,11 +1665,13 @@ int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, 
     if (ctx->m_auto && ctx->m == 2) B = std::min(B, std::max(1, 64 - ctx->auto_steps));
     const int expect = ctx->last_sweeps;
     const int spec = expect >= 2 ? expect - 1 : -1;
-    const mb4cu::BatchCtl ctl{ctx->d_babort, expect, ctx->m_auto && ctx->m == 1 ? 4 : 0};
+    mb4cu::BatchCtl ctl{ctx->d_babort, expect, ctx->m_auto && ctx->m == 1 ? 4 : 0, 0.0, 0.0};
+    amax2_interval(ctx, h, &ctl.amax2_lo, &ctl.amax2_hi);
     const SweepConsts c = make_consts(ctx, h);
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_babort, 0, sizeof(int), ctx->stream));
     MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_bstatus, 0, sizeof(mb4cu::StepStatus) * B, ctx->stream));
-    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_brmax, 0, sizeof(unsigned long long) * B * ctx->max_iters, ctx->stream));
+    const size_t rstride = static_cast<size_t>(ctx->max_iters) + 1;
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_brmax, 0, sizeof(unsigned long long) * B * rstride, ctx->stream));
     const double2* u0p = ctx->u0;
     double2* Up[2][3];
     std::memcpy(Up, ctx->U, sizeof(Up));
@@ -1631,7 +1679,7 @@ int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, 
     MB4_CUDA(ctx, cudaEventRecord(ctx->bev[0], ctx->stream));
     for (int k = 0; k < B; ++k) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, u0p, ctx->V, Up,
-                                                ctx->d_brmax + static_cast<size_t>(k) * ctx->max_iters,
+                                                ctx->d_brmax + static_cast<size_t>(k) * rstride,
                                                 ctx->d_obs_march, ctx->d_bstatus + k, ctx->max_iters, ctx->eps, 1, c,
                                                 ctx->device, ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, &ctl));
         MB4_CUDA(ctx, cudaEventRecord(ctx->bev[k + 1], ctx->stream));
@@ -1664,6 +1712,7 @@ int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, 
         std::swap(ctx->u0, ctx->U[st.set][2]);
         ctx->obs_cached = false;
         ctx->last_sweeps = st.sweeps;
+        track_amax2(ctx, st.amax2);
         adapt_neumann(ctx, st.sweeps);
         std::memcpy(ctx->entry_obs, st.obs, sizeof(ctx->entry_obs));
         if (obs_rows) {
@@ -1695,9 +1744,11 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
     }
     // With the persistent kernel the energy monitor of each step's entry state is
     // fused into that step's first sweep; only the final state needs its own pass.
-    const bool fused = (ctx->kernel == 0 && !stiff_step(ctx, h)) || ctx->kernel == 2;
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     for (int s = 1; s <= nsteps; ++s) {
+        if (ctx->kernel == 0) {
+            if (int rca = refresh_amax2(ctx)) return rca;  // (a no-op unless a Newton-Krylov step ran)
+        }
         if (ctx->batched && batchable(ctx, h)) {
             int done = 0;
             if (int rc = run_batch(ctx, h, nsteps - s + 1, obs_series ? obs_series + 7 * (s - 1) : nullptr,
@@ -1709,6 +1760,9 @@ int mb4cu_run(mb4cu_ctx* ctx, double h, int nsteps, double* obs_series, int* ite
             }
             // the batch's first step failed: it goes through the one-step path below
         }
+        // the step's energy sums come from its first sweep's fused monitor, unless the
+        // step goes straight to the Newton-Krylov solver (stiff) or the kernel has none
+        const bool fused = (ctx->kernel == 0 && !stiff_step(ctx, h)) || ctx->kernel == 2;
         if (obs_series && !fused) {
             const int rc0 = mb4cu_observables(ctx, &o);
             if (rc0) return rc0;
@@ -1996,7 +2050,7 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
     if (!(h > 0.0) || s < 0) return fail(ctx, MB4CU_INVALID, "sweep: h must be positive, s >= 0");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     const SweepConsts c = make_consts(ctx, h);
-    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, 2 * sizeof(unsigned long long), ctx->stream));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
     MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
                                             ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
@@ -2045,16 +2099,16 @@ int region_rects(const mb4cu_ctx* ctx, int region, int rects[4][4]) {
 }  // namespace
 
 int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
-                       double* dev_out6) {
+                       double* dev_out7) {
     if (!ctx || ctx->ghost <= 0) return fail(ctx, MB4CU_INVALID, "sweep: sub-domain contexts only");
-    if (!(h > 0.0) || s < 0 || region < 0 || region > 2 || (region != 1 && !dev_out6))
+    if (!(h > 0.0) || s < 0 || region < 0 || region > 2 || (region != 1 && !dev_out7))
         return fail(ctx, MB4CU_INVALID, "sweep: h > 0, s >= 0, region 0..2, output buffer");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     const SweepConsts c = make_consts(ctx, h);
     int rects[4][4];
     const int nrect = region_rects(ctx, region, rects);
     // the frame (or the whole domain) starts the residual max; the interior adds to it
-    if (region != 2) MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, sizeof(unsigned long long), ctx->stream));
+    if (region != 2) MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, 2 * sizeof(unsigned long long), ctx->stream));
     if (nrect > 0) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status, 1, -1.0,
@@ -2064,12 +2118,14 @@ int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int reg
         if (ctx->profiling) ctx->prof.launches += 1;
     }
     if (region != 1) {
-        // [local ||r||_inf, the 5 energy sums of u0 (s = 0)] -> the caller's device buffer
-        static_assert(offsetof(mb4cu::StepStatus, obs) == offsetof(mb4cu::StepStatus, rlast) + sizeof(double),
-                      "rlast and obs are contiguous");
-        MB4_CUDA(ctx, cudaMemcpyAsync(dev_out6, reinterpret_cast<const char*>(ctx->d_status) +
+        // [local ||r||_inf, the 5 energy sums of u0, max|u0|^2 (s = 0)] -> the caller's device buffer
+        static_assert(offsetof(mb4cu::StepStatus, obs) == offsetof(mb4cu::StepStatus, rlast) + sizeof(double) &&
+                          offsetof(mb4cu::StepStatus, amax2) ==
+                              offsetof(mb4cu::StepStatus, obs) + sizeof(double) * mb4cu::kObsFields,
+                      "rlast, obs and amax2 are contiguous");
+        MB4_CUDA(ctx, cudaMemcpyAsync(dev_out7, reinterpret_cast<const char*>(ctx->d_status) +
                                                     offsetof(mb4cu::StepStatus, rlast),
-                                      sizeof(double) * (1 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
+                                      sizeof(double) * (2 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
         if (ctx->profiling) {
             ctx->prof.sweeps += 1;
             ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : (final_guess ? 88.0 : 120.0));
@@ -2078,8 +2134,8 @@ int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int reg
     return MB4CU_OK;
 }
 
-int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out6) {
-    return mb4cu_sweep_region(ctx, h, s, final_guess, 0, 0, dev_out6);
+int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out7) {
+    return mb4cu_sweep_region(ctx, h, s, final_guess, 0, 0, dev_out7);
 }
 
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps) {

@@ -110,6 +110,7 @@ struct StepStatus {
     int redone;        // speculative final sweeps redone with all stages (production kernel)
     double rlast;      // ||r||_inf of the last sweep
     double obs[kObsFields];  // energy sums of u0 (first sweep)
+    double amax2;            // max |u0|^2 of the entry state (first sweep; 0 if not measured)
     // %globaltimer (ns) at kernel start and after each sweep's grid barrier
     // (block 0), for per-sweep timing; entries past `sweeps` are stale.
     static constexpr int kMaxTimed = 16;
@@ -130,7 +131,8 @@ struct StepArgs {
     const double2* u0;
     const double* V;
     double2* U[2][3];
-    unsigned long long* rmax;   // [max_iters], zeroed by the host before launch
+    unsigned long long* rmax;   // [max_iters + 1], zeroed by the host before launch; [max_iters]:
+                                // max |u0|^2 bits of the entry state (first sweep)
     double* obs_partial;        // [gridDim.x][kObsFields]
     StepStatus* status;
     int max_iters;
@@ -161,6 +163,7 @@ struct StepArgs {
     int* batch_abort;           // nullptr: not batched
     int expect_sweeps;
     int switch_sweeps;          // 0: none
+    double amax2_lo, amax2_hi;  // the batch's step constants hold while max|u0|^2 stays inside
 };
 
 // batch control of launch_step_march2 (see StepArgs::batch_abort)
@@ -168,6 +171,7 @@ struct BatchCtl {
     int* abort;
     int expect_sweeps;
     int switch_sweeps;
+    double amax2_lo, amax2_hi;
 };
 
 // ---- the other integrators (methods.cu) ------------------------------------

@@ -17,6 +17,85 @@
 
 namespace mb4cu {
 
+// Compensated summation (Knuth TwoSum, branch-free): s + c carries the running sum with
+// the rounding error of every addition kept in c, so the energy monitor's relative error
+// does not grow with the number of sites a thread, block or grid adds up.
+__device__ __forceinline__ void two_sum_add(double& s, double& c, double x) {
+    const double t = s + x;
+    const double z = t - s;
+    c += (s - (t - z)) + (x - z);
+    s = t;
+}
+// (s, c) += (s2, c2)
+__device__ __forceinline__ void two_sum_merge(double& s, double& c, double s2, double c2) {
+    two_sum_add(s, c, s2);
+    c += c2;
+}
+
+// Compensated block reduction of NF per-thread (sum, carry) pairs, fixed order; thread f < NF
+// of the block writes field f's block total (one rounding) to out[f].
+template <int NT, int NF>
+__device__ __forceinline__ void block_csum_store(const double* acc, const double* car, double* out) {
+    __shared__ double red[NF][NT / 32][2];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        double v = acc[f], c = car[f];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(0xffffffffu, v, o), c2 = __shfl_xor_sync(0xffffffffu, c, o);
+            two_sum_merge(v, c, v2, c2);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            red[f][threadIdx.x >> 5][0] = v;
+            red[f][threadIdx.x >> 5][1] = c;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < NF) {
+        double v = 0.0, c = 0.0;
+        for (int w = 0; w < NT / 32; ++w) two_sum_merge(v, c, red[threadIdx.x][w][0], red[threadIdx.x][w][1]);
+        out[threadIdx.x] = v + c;
+    }
+}
+
+// Energy monitor accumulators of a first-sweep thread: plain sums of the current block of
+// rows (fields 0..4), max|u0|^2, and the compensated totals (sum, carry) into which
+// monitor_flush folds the block sums every kMonitorRows rows -- the per-site cost of
+// plain accumulation with the accuracy of compensated summation (a block sum of <= 16
+// terms is the only uncompensated step).
+constexpr int kAccMax = kObsFields;            // max |u0|^2
+constexpr int kAccTot = kObsFields + 1;        // compensated totals of fields 0..4
+constexpr int kAccCarry = kAccTot + kObsFields;  // their carries
+constexpr int kAccSize = kAccCarry + kObsFields;
+constexpr int kMonitorRows = 16;
+#ifndef MB4_MONITOR_COMP
+#define MB4_MONITOR_COMP 1  // 0: plain block folding (experiment knob)
+#endif
+#ifndef MB4_MONITOR_AMAX
+#define MB4_MONITOR_AMAX 1  // 0: no max|u0|^2 in the monitor (experiment knob)
+#endif
+
+__device__ __forceinline__ void monitor_add(double* acc, double kin, double kin_im, double n2, double vn) {
+    acc[0] += kin;
+    acc[1] += kin_im;
+    acc[2] += n2;
+    acc[3] += n2 * n2;
+    acc[4] += vn;
+    if (MB4_MONITOR_AMAX) acc[kAccMax] = fmax(acc[kAccMax], n2);  // max |u0|^2 (spectral bound)
+}
+
+__device__ __forceinline__ void monitor_flush(double* acc) {
+#pragma unroll
+    for (int f = 0; f < kObsFields; ++f) {
+        if (f == 1 || !MB4_MONITOR_COMP) {
+            acc[kAccTot + f] += acc[f];  // imaginary kinetic part: a health check, plain
+        } else {
+            two_sum_add(acc[kAccTot + f], acc[kAccCarry + f], acc[f]);
+        }
+        acc[f] = 0.0;
+    }
+}
+
 __device__ __forceinline__ int wrap_index(int x, int n) {
     x %= n;
     return x < 0 ? x + n : x;

@@ -432,7 +432,7 @@ struct March3 {
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO, DEF>& cf,
                                          const double2* const uin[3], double2* const uout[3],
                                          Seg& s, int j, int h3, unsigned& rmax,
-                                         double acc[kObsFields]) {
+                                         double* acc) {
         constexpr int S_NEW = PH;            // z row j      (own column, newly loaded)
         constexpr int S_CEN = (PH + 2) % 3;  // z row j - 1  (level-0 centre row)
         constexpr int S_DN = (PH + 1) % 3;   // z row j - 2
@@ -520,11 +520,8 @@ struct March3 {
                 if (i >= M && i < M + s.R && t >= M && t < NT - M && xout < s.xlim) {
                     const double vn = v * n2;
                     const double sc = ISO ? c.cx : 1.0;
-                    acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
-                    acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
-                    acc[2] += n2;
-                    acc[3] += n2 * n2;
-                    acc[4] += vn;
+                    monitor_add(acc, fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn), sc * fma(u0c.x, w0.y, -u0c.y * w0.x), n2,
+                                vn);
                 }
             } else {
                 double2 z[4], w[4];
@@ -647,7 +644,7 @@ struct March3 {
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, const double2* const uin[3],
                         double2* const uout[3], int X0, int xlim, int Y0, int R, unsigned& rmax,
-                        double acc[kObsFields], int smask) {
+                        double* acc, int smask) {
         const Coef<ISO, DEF> cf{c};
         Seg s;
         s.smask = smask;
@@ -705,11 +702,13 @@ struct March3 {
             body<0>(a, cf, uin, uout, s, j, h3, rmax, acc);
             body<1>(a, cf, uin, uout, s, j + 1, h3, rmax, acc);
             body<2>(a, cf, uin, uout, s, j + 2, h3, rmax, acc);
+            if (FIRST) monitor_flush(acc);  // (shallow first sweeps: every 3 rows)
         }
 #else
         // one body per row; the register window rotates by explicit moves
         for (int j = 0; j < jend; ++j) {
             body<0>(a, cf, uin, uout, s, j, j % 6, rmax, acc);
+            if (FIRST) monitor_flush(acc);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 zw[1][q] = zw[2][q];
@@ -870,7 +869,7 @@ struct MarchFirst {
     // are masked (out_ok / the monitor window), as in March3.
     template <int PAR>  // = j & 1
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3],
-                                         Seg& s, int j, unsigned& rmax, double acc[kObsFields]) {
+                                         Seg& s, int j, unsigned& rmax, double* acc) {
         const SweepConsts& c = cf.c;
         const int t = threadIdx.x, cc = t + 1, i = j - 2;
         const int slot_new = zs, slot_cen = zslot(1);
@@ -897,11 +896,8 @@ struct MarchFirst {
         if (i >= MF && i < MF + s.R && t >= MF && t < NT - MF && xout < s.xlim) {
             const double vn = v * n2;
             const double sc = ISO ? c.cx : 1.0;
-            acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
-            acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
-            acc[2] += n2;
-            acc[3] += n2 * n2;
-            acc[4] += vn;
+            monitor_add(acc, fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn), sc * fma(u0c.x, w0.y, -u0c.y * w0.x), n2,
+                        vn);
         }
 
         // ---- levels 1..MF: g_n at row i - n from g_{n-1} rows i-n-1, i-n, i-n+1 ----
@@ -942,7 +938,7 @@ struct MarchFirst {
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int X0, int xlim,
-                        int Y0, int R, unsigned& rmax, double acc[kObsFields]) {
+                        int Y0, int R, unsigned& rmax, double* acc) {
         const Coef<ISO> cf{c};
         Seg s;
         s.X0 = X0;
@@ -973,6 +969,7 @@ struct MarchFirst {
         for (; j + 1 < jend; j += 2) {
             body<0>(a, cf, uout, s, j, rmax, acc);
             body<1>(a, cf, uout, s, j + 1, rmax, acc);
+            if ((j & (kMonitorRows - 1)) == kMonitorRows - 2) monitor_flush(acc);  // every kMonitorRows rows
         }
         if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
         cp_async_wait<0>();
@@ -1141,7 +1138,7 @@ struct MarchFirst2 {
 
     template <int PAR>  // = j & 1
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3], Seg& s,
-                                         int j, unsigned& rmax, double acc[kObsFields]) {
+                                         int j, unsigned& rmax, double* acc) {
         const SweepConsts& c = cf.c;
         const int t = threadIdx.x, i = j - 2;
         unsigned char* smt = sm + t * 16;
@@ -1180,11 +1177,8 @@ struct MarchFirst2 {
         if (lane_ok && i >= MF && i < MF + s.R) {
             const double vn = v * n2;
             const double sc = ISO ? c.cx : 1.0;
-            acc[0] += fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn);
-            acc[1] += sc * fma(u0c.x, w0.y, -u0c.y * w0.x);
-            acc[2] += n2;
-            acc[3] += n2 * n2;
-            acc[4] += vn;
+            monitor_add(acc, fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn), sc * fma(u0c.x, w0.y, -u0c.y * w0.x), n2,
+                        vn);
         }
 
         // ---- levels 1..MF --------------------------------------------------------
@@ -1229,7 +1223,7 @@ struct MarchFirst2 {
     }
 
     __device__ void run(const StepArgs& a, const SweepConsts& c, double2* const uout[3], int X0, int xlim,
-                        int Y0, int R, unsigned& rmax, double acc[kObsFields]) {
+                        int Y0, int R, unsigned& rmax, double* acc) {
         const Coef<ISO> cf{c};
         Seg s;
         s.X0 = X0;
@@ -1268,6 +1262,7 @@ struct MarchFirst2 {
         for (; j + 1 < jend; j += 2) {
             body<0>(a, cf, uout, s, j, rmax, acc);
             body<1>(a, cf, uout, s, j + 1, rmax, acc);
+            if ((j & (kMonitorRows - 1)) == kMonitorRows - 2) monitor_flush(acc);  // every kMonitorRows rows
         }
         if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
         cp_async_wait<0>();
@@ -1311,7 +1306,7 @@ __device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) 
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
-                           unsigned& rmax, double acc[kObsFields], int smask = 7) {
+                           unsigned& rmax, double* acc, int smask = 7) {
     if constexpr (FIRST && M >= 3 && M <= 7 && MB4_FIRST_V2) {
         using MFirst = MarchFirst2<M, NT, ISO, GHOST>;
         MFirst mf(smem);
@@ -1376,7 +1371,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     // an earlier launch on this stream, so every CTA of this grid reads the same value)
     if (a.batch_abort && *reinterpret_cast<volatile const int*>(a.batch_abort)) return;
     cg::grid_group grid = cg::this_grid();
-    double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double acc[kAccSize] = {};  // energy sums, max |u0|^2, carries (monitor_add)
 #if MB4_CONSTS_IN_SMEM
     // M = 2: scheme / step constants as a shared-memory broadcast table (LDS)
     // instead of the constant bank (LDCU + uniform-register shuffling), which
@@ -1433,20 +1428,15 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             if constexpr (PH != 2)  // (not instantiated for the later-sweep kernel)
                 sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
             if (a.want_obs) {
-                __shared__ double red[kObsFields][NT / 32];
+                // compensated warp and block trees; one rounding per block partial
+                monitor_flush(acc);
+                block_csum_store<NT, kObsFields>(acc + kAccTot, acc + kAccCarry, a.obs_partial + blockIdx.x * kObsFields);
+                // max |u0|^2 of the entry state (non-negative: its bits order as integers)
+                double mx = acc[kAccMax];
 #pragma unroll
-                for (int f = 0; f < kObsFields; ++f) {
-                    double v = acc[f];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
-                }
-                __syncthreads();
-                if (threadIdx.x < kObsFields) {
-                    double v = 0.0;
-                    for (int w = 0; w < NT / 32; ++w) v += red[threadIdx.x][w];
-                    a.obs_partial[blockIdx.x * kObsFields + threadIdx.x] = v;
-                }
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if ((threadIdx.x & 31) == 0 && mx > 0.0)
+                    atomicMax(&a.rmax[a.max_iters], static_cast<unsigned long long>(__double_as_longlong(mx)));
             }
         } else if constexpr (PH != 1 && PH != 3) {
             // Speculative final sweep (sg == spec_sweep, predicted by the host from the
@@ -1495,15 +1485,19 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         // a non-finite residual (NaN update somewhere) is reported as +inf: the MAX
         // all-reduce of a decomposed lattice (fmax) would drop a NaN, never an inf
         a.status->rlast = isfinite(rlast) ? rlast : __longlong_as_double(0x7FF0000000000000ll);
+        const double amax2 = a.want_obs ? __longlong_as_double(static_cast<long long>(__ldcg(&a.rmax[a.max_iters]))) : 0.0;
+        a.status->amax2 = amax2;
         if (a.batch_abort &&
-            (!converged || sweeps != a.expect_sweeps || (a.switch_sweeps > 0 && sweeps >= a.switch_sweeps)))
+            (!converged || sweeps != a.expect_sweeps || (a.switch_sweeps > 0 && sweeps >= a.switch_sweeps) ||
+             !(amax2 >= a.amax2_lo && amax2 <= a.amax2_hi)))
             *a.batch_abort = 1;
     }
     if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
-        double v = 0.0;
+        double v = 0.0, cv = 0.0;  // fixed block order, compensated
         const int nb = a.obs_blocks > 0 ? a.obs_blocks : static_cast<int>(gridDim.x);
-        for (int b = 0; b < nb; ++b) v += a.obs_partial[b * kObsFields + threadIdx.x];
-        a.status->obs[threadIdx.x] = (a.obs_accumulate ? a.status->obs[threadIdx.x] : 0.0) + v;
+        for (int b = 0; b < nb; ++b) two_sum_add(v, cv, a.obs_partial[b * kObsFields + threadIdx.x]);
+        if (a.obs_accumulate) two_sum_add(v, cv, a.status->obs[threadIdx.x]);
+        a.status->obs[threadIdx.x] = v + cv;
     }
 }
 
@@ -1663,6 +1657,8 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
         a.batch_abort = batch->abort;
         a.expect_sweeps = batch->expect_sweeps;
         a.switch_sweeps = batch->switch_sweeps;
+        a.amax2_lo = batch->amax2_lo;
+        a.amax2_hi = batch->amax2_hi;
     }
     a.nrect = nrect;
     for (int r = 0; r < nrect && r < 4; ++r)

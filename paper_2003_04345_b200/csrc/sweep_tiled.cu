@@ -178,6 +178,7 @@ constexpr int kObsThreads = 256;
 
 __global__ void __launch_bounds__(kObsThreads) observables_partial_kernel(const ObsArgs a) {
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double car[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};  // compensation (two_sum_add)
     // Tiles of kObsThreads columns x a band of rows; each thread marches down its
     // column with the vertical neighbours in registers (one HBM read of u per site;
     // left/right come from the same row, L1-resident), periodic wrap by
@@ -199,49 +200,42 @@ __global__ void __launch_bounds__(kObsThreads) observables_partial_kernel(const 
             const double2 l = row[il], r = row[ir];
             const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (dn.x + up.x)));
             const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (dn.y + up.y)));
-            acc[0] += fma(u.x, kx, u.y * ky);   // Re conj(u) Ku
-            acc[1] += fma(u.x, ky, -u.y * kx);  // Im conj(u) Ku
+            two_sum_add(acc[0], car[0], fma(u.x, kx, u.y * ky));  // Re conj(u) Ku
+            acc[1] += fma(u.x, ky, -u.y * kx);                    // Im conj(u) Ku (health check)
             const double n2 = fma(u.x, u.x, u.y * u.y);
-            acc[2] += n2;
-            acc[3] += n2 * n2;
-            acc[4] += a.V[static_cast<size_t>(j) * a.nx + i] * n2;
+            two_sum_add(acc[2], car[2], n2);
+            two_sum_add(acc[3], car[3], n2 * n2);
+            two_sum_add(acc[4], car[4], a.V[static_cast<size_t>(j) * a.nx + i] * n2);
             dn = u;
             u = up;
         }
     }
-    __shared__ double red[kObsFields][kObsThreads / 32];
-#pragma unroll
-    for (int f = 0; f < kObsFields; ++f) {
-        double v = acc[f];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < kObsFields) {
-        double v = 0.0;
-        for (int w = 0; w < kObsThreads / 32; ++w) v += red[threadIdx.x][w];
-        a.partial[blockIdx.x * kObsFields + threadIdx.x] = v;
-    }
+    block_csum_store<kObsThreads, kObsFields>(acc, car, a.partial + blockIdx.x * kObsFields);
 }
 
 // Fixed-order final sum of the block partials (bit-reproducible).
 __global__ void observables_finalize_kernel(const double* partial, int nblocks, double* out) {
-    __shared__ double red[kObsFields][256];
+    __shared__ double red[kObsFields][256][2];
     double acc[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double car[kObsFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
 #pragma unroll
-        for (int f = 0; f < kObsFields; ++f) acc[f] += partial[b * kObsFields + f];
+        for (int f = 0; f < kObsFields; ++f) two_sum_add(acc[f], car[f], partial[b * kObsFields + f]);
 #pragma unroll
-    for (int f = 0; f < kObsFields; ++f) red[f][threadIdx.x] = acc[f];
+    for (int f = 0; f < kObsFields; ++f) {
+        red[f][threadIdx.x][0] = acc[f];
+        red[f][threadIdx.x][1] = car[f];
+    }
     __syncthreads();
     for (int s = blockDim.x / 2; s > 0; s >>= 1) {
         if (threadIdx.x < s)
 #pragma unroll
-            for (int f = 0; f < kObsFields; ++f) red[f][threadIdx.x] += red[f][threadIdx.x + s];
+            for (int f = 0; f < kObsFields; ++f)
+                two_sum_merge(red[f][threadIdx.x][0], red[f][threadIdx.x][1], red[f][threadIdx.x + s][0],
+                              red[f][threadIdx.x + s][1]);
         __syncthreads();
     }
-    if (threadIdx.x < kObsFields) out[threadIdx.x] = red[threadIdx.x][0];
+    if (threadIdx.x < kObsFields) out[threadIdx.x] = red[threadIdx.x][0][0] + red[threadIdx.x][0][1];
 }
 
 __global__ void apply_kv_kernel(int nx, int ny, double cx, double cy, const double2* __restrict__ u,

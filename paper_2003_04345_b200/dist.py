@@ -236,10 +236,13 @@ class DistributedSession:
         self.halo.exchange(F_V)
         self.last_sweeps = 0
         self.entry_sums: Optional[np.ndarray] = None
+        # max|u0|^2 of the current sub-step's entry state (all-reduced), measured by its
+        # first sweep; the next sub-step's spectral bound uses it, as on one GPU
+        self._sub_amax2: Optional[float] = None
 
     # -- energy monitor: global sums -> Observables (lattice.cpp:113-137)
     def finish(self, sums) -> np.ndarray:
-        qr, qi, prob, quart, ext = sums
+        qr, qi, prob, quart, ext = sums[:5]
         imag_scale = max(abs(qr), (4 * self.cx + 4 * self.cy) * prob)
         if abs(qi) > 1e-12 * imag_scale and imag_scale > 0.0:
             raise RuntimeError("observables: non-real kinetic quadratic form")
@@ -252,7 +255,23 @@ class DistributedSession:
         self.halo.exchange(F_U0)
         return self.finish(self.comm.allreduce_sum(self.b.obs_sums()))
 
+    def _take_entry(self, sums) -> None:
+        """Reduced sums of a sub-step's first sweep: the step's energy record (first
+        sub-step) and, when the backend reports it, max|u0|^2 of the entry state."""
+        if self.entry_sums is None:
+            self.entry_sums = np.asarray(sums[:5])
+        self._sub_amax2 = float(sums[5]) if len(sums) > 5 else None
+
+    def _commit(self, sweeps: int) -> None:
+        """Accept the sub-step; the next one's spectral bound follows the measured
+        amplitude (the single-domain rule: mb4cu's per-step max|u0|^2 tracking)."""
+        self.b.commit(sweeps)
+        if self._sub_amax2 is not None and hasattr(self.b, "set_amax2"):
+            self.b.set_amax2(self._sub_amax2)
+            self.b.bound_dirty = True
+
     def _substep(self, h: float) -> Tuple[int, float]:
+        self.sync_spectral_bound()
         if getattr(self.b, "overlap", False):
             return self._substep_overlap(h)
         if hasattr(self.b, "sweep_launch"):
@@ -265,12 +284,15 @@ class DistributedSession:
             r_loc, sums = self.b.sweep(h, s)
             # NaN -> +inf before the MAX all-reduce (fmax would drop a NaN rank)
             r = self.comm.allreduce_max(r_loc if math.isfinite(r_loc) else math.inf)
-            if s == 0 and self.entry_sums is None:
-                self.entry_sums = self.comm.allreduce_sum(sums)
+            if s == 0:
+                red = list(self.comm.allreduce_sum(sums[:5]))
+                if len(sums) > 5:
+                    red.append(self.comm.allreduce_max(float(sums[5])))
+                self._take_entry(red)
             if not math.isfinite(r):
                 raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
             if stage_converged(r, r_prev, s, self.eps):
-                self.b.commit(s + 1)
+                self._commit(s + 1)
                 return s + 1, r
             r_prev = r
         raise NonConvergence(f"stage iteration: no convergence after {self.max_iters} sweeps", r)
@@ -281,7 +303,7 @@ class DistributedSession:
         is repeated with all stages if the reduced residual does not converge."""
         self.halo.exchange(F_U0)
         guess = getattr(self, "_guess", 0)
-        want0 = self.entry_sums is None
+        want0 = True  # every sub-step's first sweep: energy sums + max|u0|^2
         finals = {}
 
         def launch(s):
@@ -303,11 +325,11 @@ class DistributedSession:
                 launched = s + 1
             r, sums = self.b.sweep_read(slot=s & 1, want_sums=(s == 0 and want0))
             if sums is not None:
-                self.entry_sums = sums
+                self._take_entry(sums)
             if not math.isfinite(r):
                 raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
             if stage_converged(r, r_prev, s, self.eps):
-                self.b.commit(s + 1)
+                self._commit(s + 1)
                 self._guess = s + 1
                 return s + 1, r
             if finals[s]:
@@ -330,7 +352,7 @@ class DistributedSession:
             self.halo.exchange(F_U0)
         self.b.u0_halo_ok = False
         guess = getattr(self, "_guess", 0)
-        want0 = self.entry_sums is None
+        want0 = True  # every sub-step's first sweep: energy sums + max|u0|^2
         finals = {}
 
         def launch(s, final=None):
@@ -349,11 +371,11 @@ class DistributedSession:
                 launched = s + 1
             r, sums = self.b.sweep_read(slot=s & 1, want_sums=(s == 0 and want0))
             if sums is not None:
-                self.entry_sums = sums
+                self._take_entry(sums)
             if not math.isfinite(r):
                 raise NonConvergence("stage iteration diverged (non-finite update)", math.inf)
             if stage_converged(r, r_prev, s, self.eps):
-                self.b.commit(s + 1)
+                self._commit(s + 1)
                 self._guess = s + 1
                 # the exchange after sweep s moved U3 ghost-wide: the new u0's halos
                 # (a look-ahead sweep s + 1 writes the other stage set; wait_exchange
@@ -508,26 +530,32 @@ class CudaBackend:
         self._chk(self.L.mb4cu_halo_unpack(self.ctx, field, side, C.c_void_p(buf.data_ptr())))
 
     def sweep(self, h, s):
-        r = C.c_double(0.0)
-        sums = np.zeros(5)
-        self._chk(self.L.mb4cu_sweep(self.ctx, h, s, C.byref(r), _lib.dptr(sums)))
-        return r.value, sums
+        """Sweep s, waiting for it: (local ||r||_inf, [5 local energy sums, local max|u0|^2])."""
+        out = self._red_buf(0)
+        self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, 0, C.c_void_p(out.data_ptr())))
+        host = out.cpu().numpy()
+        return float(host[0]), host[1:7].copy()
+
+    def set_amax2(self, amax2: float) -> None:
+        self._chk(self.L.mb4cu_set_amax2(self.ctx, amax2))
+        self._amax2 = amax2
 
     def sweep_launch(self, h, s, final, comm, slot=0, want_sums=False):
         """Enqueue sweep s and the all-reduce of [residual max, energy sums] into the
         device buffer `slot`, on the stream shared with NCCL (no host wait)."""
         if self._red is None:
-            self._red = [self.torch.zeros(6, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
+            self._red = [self.torch.zeros(7, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
         red = self._red[slot]
         self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, int(final), C.c_void_p(red.data_ptr())))
         comm.allreduce_max_(red[0:1])
         if want_sums:
             comm.allreduce_sum_(red[1:6])
+            comm.allreduce_max_(red[6:7])
 
     def sweep_read(self, slot=0, want_sums=False):
-        """Host read of a launched sweep's reduced [r, sums] (waits for it)."""
+        """Host read of a launched sweep's reduced [r, 5 sums, max|u0|^2] (waits for it)."""
         host = self._red_buf(slot).cpu().numpy()
-        return float(host[0]), (host[1:6].copy() if want_sums else None)
+        return float(host[0]), (host[1:7].copy() if want_sums else None)
 
     def sweep_reduce(self, h, s, final, comm, want_sums=False):
         self.sweep_launch(h, s, final, comm, 0, want_sums)
@@ -536,7 +564,7 @@ class CudaBackend:
     # ---- halo-exchange overlap (DistributedSession._substep_overlap) -------------
     def _red_buf(self, slot):
         if self._red is None:
-            self._red = [self.torch.zeros(6, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
+            self._red = [self.torch.zeros(7, dtype=self.torch.float64, device=self.dev) for _ in range(2)]
         return self._red[slot]
 
     def sweep_frame(self, h, s, final):
@@ -570,11 +598,12 @@ class CudaBackend:
         comm.allreduce_max_(red[0:1])
         if want_sums:
             comm.allreduce_sum_(red[1:6])
+            comm.allreduce_max_(red[6:7])
 
     def sweep_repeat(self, h, s):
         """Repeat sweep s storing every stage (after a missed final guess)."""
         if self._scratch is None:
-            self._scratch = self.torch.zeros(6, dtype=self.torch.float64, device=self.dev)
+            self._scratch = self.torch.zeros(7, dtype=self.torch.float64, device=self.dev)
         self._chk(self.L.mb4cu_sweep_async(self.ctx, h, s, 0, C.c_void_p(self._scratch.data_ptr())))
 
     def commit(self, sweeps):
@@ -592,6 +621,7 @@ class CudaBackend:
         u = np.ascontiguousarray(u_block, dtype=np.complex128)
         self._chk(self.L.mb4cu_set_state(self.ctx, _lib.dptr(u)))
         self.bound_dirty = True
+        self._amax2 = None  # the library measures a newly set state itself
 
     def neumann_terms(self) -> int:
         return self.m
@@ -618,7 +648,10 @@ class CudaBackend:
 
     def restore(self):
         dirty = getattr(self, "bound_dirty", False)  # an internal restore keeps the step's bound
+        amax2 = getattr(self, "_amax2", None)
         self.set_state(self._saved)
+        if amax2 is not None:  # as on one GPU: a restore keeps the tracked amplitude
+            self.set_amax2(amax2)
         self.bound_dirty = dirty
 
     def profile(self, on=True):

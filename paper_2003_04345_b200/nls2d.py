@@ -391,6 +391,13 @@ class Session:
         self._check(rc, st.last_residual)
         return obs, iters
 
+    def spectral_bound(self) -> float:
+        """The bound rho >= rho(J(u0)) placing the next step's Chebyshev polynomial (the
+        context tracks max|u0|^2 per step through its first sweeps)."""
+        rho = C.c_double(0.0)
+        self._check(self._L.mb4cu_spectral_bound(self._ctx, C.byref(rho)))
+        return rho.value
+
     def profile_enable(self, on: bool = True):
         self._check(self._L.mb4cu_profile_enable(self._ctx, int(on)))
 

@@ -365,3 +365,49 @@ def test_batched_run_falls_back_on_failing_steps(monkeypatch):
     assert max(ia) > 4  # some steps took the fallback (their count includes the failed sweeps)
     assert np.array_equal(oa, ob)
     assert np.array_equal(ua, ub)
+
+
+def _colliding_packets(n=96, amp=3.0, sigma=3.0, k=1.0):
+    x = np.arange(n)
+    X, Y = np.meshgrid(x, x)
+    u = np.zeros((n, n), dtype=np.complex128)
+    for cx, kx in ((n / 2 - 12, k), (n / 2 + 12, -k)):
+        u += amp * np.exp(-((X - cx) ** 2 + (Y - n / 2) ** 2) / (2 * sigma ** 2)) * np.exp(1j * kx * (X - cx))
+    return u.reshape(-1)
+
+
+def test_spectral_bound_tracks_the_amplitude_per_step(monkeypatch):
+    """Two high-amplitude packets (defocusing, g = 1; max|u|^2 = 9 falls ~10 % in 40 steps as
+    they spread): the Chebyshev interval rho = 4cx + 4cy + max|V| + 3|gamma| max|u0|^2
+    (rounded up to a power of 2^(1/16)) follows the amplitude step by step -- after step k the
+    context's bound is the one of the max|u|^2 that step's first sweep measured,
+    max|u_(k-1)|^2 (no separate pass) -- through three bound levels.  The results stay the
+    reference's (oracle/_ref, 40 steps) and the batched run equals stepping one at a time
+    (a batch ends where the level changes)."""
+    n, gamma, dt, nsteps = 96, -1.0, 0.005, 40  # h max|lambda| rho <= 0.28: the sweep path
+    g = nls2d.GridSpec(n, n, float(n), float(n))
+    model = nls2d.GridModel(g, gamma)
+    u0 = _colliding_packets(n)
+    base = 8.0
+    level = lambda a: 2.0 ** (np.ceil(16.0 * np.log2(base + 3.0 * abs(gamma) * a)) / 16.0)  # noqa: E731
+    bounds, amps = [], []
+    with nls2d.Session(model, nls2d.Mb4Scheme(), nls2d.NewtonConfig(1e-14, 50, 4)) as s:
+        s.set_state(u0)
+        prev = u0
+        for _ in range(nsteps):
+            s.step(dt)
+            bounds.append(s.spectral_bound())
+            amps.append(float(np.max(np.abs(prev) ** 2)))
+            prev = s.get_state()
+        u_step = s.get_state()
+    assert bounds == [level(a) for a in amps]
+    assert len(set(bounds)) >= 3  # the bound moved with the collision
+    monkeypatch.delenv("MB4CU_NO_BATCH", raising=False)
+    with nls2d.Session(model, nls2d.Mb4Scheme(), nls2d.NewtonConfig(1e-14, 50, 4)) as s:
+        s.set_state(u0)
+        s.run(dt, nsteps)
+        u_run = s.get_state()
+    assert np.array_equal(u_run, u_step)
+    ref, _, _, _ = O.ref_run(n, n, float(n), float(n), gamma, np.zeros(n * n), u0, dt, nsteps, eps=1e-14,
+                             solver="gmres", record=False)
+    assert rel(u_step, ref) <= 1e-10
