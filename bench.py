@@ -470,53 +470,74 @@ def run_ours(args, d: Dist):
 # ----------------------------------------------------------------------------- multi-GPU arm
 
 
-def run_dist(args, d: Dist):
+def run_dist(args, d: Dist, make_backend=None, comm=None, lattice=None):
     """N GPUs: the cfg5 weak-scaling lattice (8192^2 per GPU) split over a px x py
-    torus (dist.choose_grid), halo exchange + scalar all-reduces over NCCL each sweep."""
+    torus (dist.choose_grid), halo exchange + scalar all-reduces over NCCL each sweep.
+
+    make_backend / comm / lattice: injection points for the CPU test of this control flow
+    (tests/test_dist_gloo.py: gloo ranks, the numpy sub-domain backend, a small lattice)."""
     import torch
 
     from paper_2003_04345_b200 import configs, dist as D, nls2d
 
     if args.config not in ("cfg3", "cfg4", "cfg5"):
         raise SystemExit("multi-GPU runs: cfg5 (weak scaling) or cfg3 / cfg4 (strong scaling)")
-    torch.cuda.set_device(d.local)
+    on_gpu = make_backend is None
+    if on_gpu:
+        torch.cuda.set_device(d.local)
     weak = args.config == "cfg5"
     if weak:  # BASELINE configs[4]: 8192^2 sites per GPU
-        gnx, gny = configs.cfg5_lattice(d.world)
+        gnx, gny = lattice or configs.cfg5_lattice(d.world)
         cfg = configs.CONFIGS["cfg5"].with_lattice(gnx, gny)
     else:  # BASELINE configs[2] / [3]: the fixed lattice split over the GPUs
         cfg = configs.CONFIGS[args.config]
+        if lattice:
+            cfg = cfg.with_lattice(*lattice)
         gnx, gny = cfg.nx, cfg.ny
     px, py = D.choose_grid(d.world, gnx, gny)
     dec = D.Decomposition(gnx, gny, px, py, d.rank)
+    # first-contact evidence for multi-GPU runs: the world, the process grid and NCCL's own
+    # communicator lines (NCCL_DEBUG=INFO, set in main) on stderr
+    print(f"[bench] rank {d.rank}/{d.world} local {d.local}: {args.config} {gnx}x{gny} on a {px}x{py} process grid, "
+          f"block {dec.lnx}x{dec.lny} at ({dec.x0},{dec.y0}), transport "
+          f"{'nccl' if d.world > 1 and on_gpu else 'local' if on_gpu else 'injected'}", file=sys.stderr, flush=True)
     Vb, pb, psum = configs.make_block(cfg, dec.x0, dec.y0, dec.lnx, dec.lny)
-    comm = D.Comm("cuda") if d.world > 1 else _LocalComm()
+    if comm is None:
+        comm = D.Comm("cuda") if d.world > 1 else _LocalComm()
     total_p = comm.allreduce_sum([psum])[0]
     pb *= 1.0 / math.sqrt(total_p)
     m = args.neumann if args.neumann >= 0 else 1
     # halo exchange overlapped with the interior sweep; the interior leaves 2 SMs to
     # NCCL's kernels when there are peers
-    be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
-                       overlap=not args.no_overlap, reserve_sms=2 if d.world > 1 else 0)
+    if on_gpu:
+        be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
+                           overlap=not args.no_overlap, reserve_sms=2 if d.world > 1 else 0)
+    else:
+        be = make_backend(dec, Vb, cfg)
     be.set_state(pb)
     sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon, adaptive_m=args.neumann < 0)
     obs_w, _ = sess.run(cfg.dt, args.warmup) if args.warmup > 0 else (None, None)
     H0 = obs_w[0, 3] if obs_w is not None else sess.observables()[3]
-    be.profile(True)
+    if hasattr(be, "profile"):
+        be.profile(True)
     clocks = ClockSampler(d.local)
     d.barrier()
-    torch.cuda.synchronize()
+    if on_gpu:
+        torch.cuda.synchronize()
     clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    if on_gpu:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    t0 = time.perf_counter()
     obs_t, sweeps = sess.run(cfg.dt, args.steps)
-    ev1.record()
-    torch.cuda.synchronize()
+    if on_gpu:
+        ev1.record()
+        torch.cuda.synchronize()
     clk = clocks.stop()
-    ms = d.max(ev0.elapsed_time(ev1))
+    ms = d.max(ev0.elapsed_time(ev1) if on_gpu else 1e3 * (time.perf_counter() - t0))
     d.barrier()
-    p = _lib_profile(be)
+    p = _lib_profile(be) if on_gpu else {"alg_bytes": 0.0, "launches": 0, "other_launches": 0}
     H = np.concatenate([obs_w[:, 3] if obs_w is not None else [], obs_t[:, 3]])
     drift = float(np.abs(H - H0).max() / abs(H0))
     n_local = dec.lnx * dec.lny
@@ -550,7 +571,7 @@ def run_dist(args, d: Dist):
         "gpu_launches": int(p["launches"] + p["other_launches"]),
         "clocks": clk,
     }
-    if not args.no_e2e:
+    if not args.no_e2e and on_gpu:
         # end to end per step through the public API: this rank's block host -> device,
         # one distributed step, device -> host (pinned host buffer)
         host = torch.empty(2 * n_local, dtype=torch.float64, pin_memory=True)
@@ -568,7 +589,8 @@ def run_dist(args, d: Dist):
         res["e2e"] = {"value": float(gnx) * gny * k_e2e / e2e_s, "unit": UNIT,
                       "h2d_bytes_per_step": 16 * n_local * d.world, "d2h_bytes_per_step": 16 * n_local * d.world,
                       "steps": k_e2e, "api": "per rank: mb4cu_set_state -> DistributedSession.step -> mb4cu_get_state"}
-    be.close()
+    if hasattr(be, "close"):
+        be.close()
     return res
 
 
@@ -668,6 +690,10 @@ def main():
         res["n_gpus"] = world  # the launch's N (the CPU path itself runs on rank 0's host cores)
         print(json.dumps(res))
         return 0
+    if world > 1:
+        # NCCL's communicator lines (ranks, rings, NVLS) on stderr: evidence of the N-rank run
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     d = Dist(world, rank, local)
     res = run_dist(args, d) if (world > 1 or args.force_dist) else run_ours(args, d)
     if rank == 0:
