@@ -54,6 +54,9 @@ def parse():
                     help="multi-GPU: exchange halos between sweeps instead of overlapping the interior")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the sub-domain (multi-GPU) path even on one GPU")
+    ap.add_argument("--python-dist", action="store_true",
+                    help="multi-GPU: the Python-driven sweep loop (dist.DistributedSession) instead of the "
+                         "library's native NCCL stepper")
     ap.add_argument("--profile-only", action="store_true",
                     help="warm-up + a few steps, no JSON extras (for ncu captures)")
     return ap.parse_args()
@@ -69,6 +72,21 @@ def dist_env():
     return world, rank, local
 
 
+class _StdoutToStderr:
+    """fd-level redirect of stdout to stderr while NCCL initialises: its version banner is a
+    plain printf to stdout, and stdout must carry only the JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 class Dist:
     def __init__(self, world: int, rank: int, local: int):
         self.world, self.rank, self.local = world, rank, local
@@ -78,7 +96,9 @@ class Dist:
             import torch.distributed as dist
 
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            with _StdoutToStderr():
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+                dist.barrier()  # (the communicator is created lazily: once here, banner included)
             self.dist = dist
             self.torch = torch
 
@@ -509,13 +529,27 @@ def run_dist(args, d: Dist, make_backend=None, comm=None, lattice=None):
     m = args.neumann if args.neumann >= 0 else 1
     # halo exchange overlapped with the interior sweep; the interior leaves 2 SMs to
     # NCCL's kernels when there are peers
-    if on_gpu:
+    if on_gpu and not getattr(args, "python_dist", False):
+        be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
+                           max_step_halvings=cfg.max_step_halvings)
+    elif on_gpu:
         be = D.CudaBackend(dec, Vb, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, m, d.local,
                            overlap=not args.no_overlap, reserve_sms=2 if d.world > 1 else 0)
     else:
         be = make_backend(dec, Vb, cfg)
     be.set_state(pb)
-    sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon, adaptive_m=args.neumann < 0)
+    native = on_gpu and not getattr(args, "python_dist", False)
+    if native:
+        # the step inside the library over NCCL (one host read per step); the communicator id
+        # from rank 0 to every rank through torch.distributed
+        nid = [D.nccl_unique_id() if d.rank == 0 else None]
+        if d.world > 1:
+            d.dist.broadcast_object_list(nid, src=0)
+        with _StdoutToStderr():
+            sess = D.NativeSession(dec, be, nid[0], cfg.gamma, 1.0, 1.0, adaptive_m=args.neumann < 0,
+                                   grid_cap=-2 if d.world > 1 else 0)
+    else:
+        sess = D.DistributedSession(dec, be, comm, cfg.gamma, 1.0, 1.0, cfg.epsilon, adaptive_m=args.neumann < 0)
     obs_w, _ = sess.run(cfg.dt, args.warmup) if args.warmup > 0 else (None, None)
     H0 = obs_w[0, 3] if obs_w is not None else sess.observables()[3]
     if hasattr(be, "profile"):
@@ -556,7 +590,10 @@ def run_dist(args, d: Dist, make_backend=None, comm=None, lattice=None):
                    "lattice": [gnx, gny], "sites_per_gpu": n_local,
                    "neumann_terms": m if args.neumann >= 0 else "adaptive 1..2",
                    "process_grid": [px, py], "parallelism": f"2-D domain decomposition {px}x{py}",
-                   "halo_exchange": ("between sweeps" if args.no_overlap else
+                   "halo_exchange": ("in the library (mb4cu_dist_step): boundary frame first, its NCCL "
+                                     "send/recv on a communication stream while the interior is swept; residual "
+                                     "all-reduce and stopping test on the device, one host read per step"
+                                     if native else "between sweeps" if args.no_overlap else
                                      "overlapped: boundary frame swept first, its NCCL exchange on a side "
                                      "stream while the interior is swept"),
                    "l2": (f"working set {dec.lnx * dec.lny * 120 / 2**20:.0f} MiB per GPU "
@@ -589,6 +626,8 @@ def run_dist(args, d: Dist, make_backend=None, comm=None, lattice=None):
         res["e2e"] = {"value": float(gnx) * gny * k_e2e / e2e_s, "unit": UNIT,
                       "h2d_bytes_per_step": 16 * n_local * d.world, "d2h_bytes_per_step": 16 * n_local * d.world,
                       "steps": k_e2e, "api": "per rank: mb4cu_set_state -> DistributedSession.step -> mb4cu_get_state"}
+    if hasattr(sess, "close"):
+        sess.close()
     if hasattr(be, "close"):
         be.close()
     return res
@@ -681,6 +720,8 @@ def repo_libs_mapped():
 
 
 def main():
+    # NCCL's banner / INFO lines go to stderr: stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":

@@ -239,6 +239,29 @@ int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int reg
                        double* dev_out7);
 int mb4cu_commit_step(mb4cu_ctx* ctx, int sweeps);
 
+/* ---- Native multi-GPU stepping over NCCL (optional; libnccl is dlopen'ed) ---------
+ * The decomposed step without the host in the sweep loop: per sweep the boundary frame,
+ * its halo exchange (NCCL send / recv on the context's communication stream) concurrently
+ * with the interior, the all-reduce of [||r||_inf, energy sums, max|u0|^2] and the stopping
+ * test (mb4_integrator.cpp:250 with the margin) on the device; the sweeps the previous
+ * step's count predicts are enqueued at once and the host reads once per step.  Halving as
+ * mb4cu_step.  The whole lattice's max|V| / min V are all-reduced at attach, so every rank
+ * places the single domain's Chebyshev polynomial (bit-identical to one GPU).
+ *   mb4cu_nccl_unique_id   rank 0: a communicator id (128 bytes) to broadcast to the ranks
+ *   mb4cu_dist_attach      every rank, after mb4cu_set_state: neighbours = ranks west,
+ *                          east, south, north on the px x py torus; grid_cap as
+ *                          mb4cu_sweep_region; force_p2p: exchange through NCCL even with
+ *                          oneself (1-GPU tests); adaptive_m: the single-domain depth policy
+ *   mb4cu_dist_step        one MB4 step; entry_sums5 = the entry state's global energy sums
+ *   mb4cu_dist_observables global energy sums of the resident state
+ * libnccl: path of the process's libnccl.so.2 (NULL: the loader's). */
+int mb4cu_nccl_unique_id(const char* libnccl, unsigned char id[128]);
+int mb4cu_dist_attach(mb4cu_ctx* ctx, const char* libnccl, const unsigned char id[128], int nranks, int rank,
+                      const int neighbours[4], int px, int py, int grid_cap, int force_p2p, int adaptive_m);
+int mb4cu_dist_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats, double* entry_sums5);
+int mb4cu_dist_observables(mb4cu_ctx* ctx, double* sums5);
+int mb4cu_dist_detach(mb4cu_ctx* ctx);
+
 /* ---- Stage-split Newton-Krylov (the paper's 3-way stage partition) ---------------
  * The simplified Newton iteration of the stiff-regime solver (mb4_integrator.cpp:194-255
  * with matrix-free, Fourier-preconditioned GMRES stage solves), opened up so that the

@@ -74,7 +74,7 @@ def build_lib(force: bool = False, verbose: bool = False, defines=(), name: str 
         if verbose and out:
             print(out)
     tmp = target + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcufft", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcufft", "-lpthread", "-ldl"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, target)
     return target

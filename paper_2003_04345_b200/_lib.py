@@ -170,6 +170,11 @@ def lib() -> C.CDLL:
         "mb4cu_lagrange_basis": (I, [DP, I, D, DP]),
         "mb4cu_scheme_integrate_e": (I, [D, DP, I, DP]),
         "mb4cu_set_amax2": (I, [P, D]),
+        "mb4cu_nccl_unique_id": (I, [C.c_char_p, C.c_char_p]),
+        "mb4cu_dist_attach": (I, [P, C.c_char_p, C.c_char_p, I, I, IP, I, I, I, I, I]),
+        "mb4cu_dist_step": (I, [P, D, C.POINTER(Stats), DP]),
+        "mb4cu_dist_observables": (I, [P, DP]),
+        "mb4cu_dist_detach": (I, [P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -197,4 +202,5 @@ EXPORTED = [
     "mb4cu_ns_begin", "mb4cu_ns_phibar", "mb4cu_ns_solve", "mb4cu_ns_get_correction", "mb4cu_ns_set_correction",
     "mb4cu_ns_update", "mb4cu_ns_commit", "mb4cu_ns_get_stages", "mb4cu_ns_abort",
     "mb4cu_eval_a", "mb4cu_lagrange_basis", "mb4cu_scheme_integrate_e", "mb4cu_set_amax2",
+    "mb4cu_nccl_unique_id", "mb4cu_dist_attach", "mb4cu_dist_step", "mb4cu_dist_observables", "mb4cu_dist_detach",
 ]

@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "mb4cu_internal.hpp"
@@ -230,7 +231,12 @@ constexpr int kMaxDots = 32;  // >= the GMRES restart length + 1 (mb4cu_api.cu k
 // hcol[i] = h_ij (both passes), hcol[j+1] = ||w||, v_{j+1} = w / ||w||.  Dot
 // products are block partials summed by block 0 in a fixed order (bit-
 // reproducible; the same grid as the other Krylov kernels).
-__global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, double2* const* __restrict__ v, int j_arg,
+#ifndef MB4_DOT_CHUNK
+#define MB4_DOT_CHUNK 8  // 32: all dots in one sweep (118 registers, 2 CTAs per SM; round 1)
+#endif
+constexpr int kDotChunk = MB4_DOT_CHUNK;
+
+__global__ void __launch_bounds__(kT, MB4_DOT_CHUNK >= 32 ? 1 : 4) arnoldi_kernel(double2* __restrict__ w, double2* const* __restrict__ v, int j_arg,
                                                      size_t n, double* __restrict__ partial,
                                                      double* __restrict__ hbuf, double* __restrict__ hcol,
                                                      int* __restrict__ jdev) {
@@ -245,27 +251,32 @@ __global__ void __launch_bounds__(kT) arnoldi_kernel(double2* __restrict__ w, do
             // all j + 1 dot products in one sweep over the sites and ONE block reduction (the
             // per-dot block reductions dominate on small lattices); per-thread, warp and
             // block sums in the same order as the one-dot-at-a-time loop below: bit-identical
+            // in chunks of kDotChunk dots (kDotChunk accumulators live: 4 CTAs per SM, so the
+            // three stage solves' cooperative launches fit the device together on large
+            // lattices); w is re-read once per chunk
             __shared__ double red[kT / 32][kMaxDots];
-            double acc[kMaxDots];
+            for (int c0 = 0; c0 <= j; c0 += kDotChunk) {
+                double acc[kDotChunk];
 #pragma unroll
-            for (int i = 0; i < kMaxDots; ++i) acc[i] = 0.0;
-            GRID_LOOP(k, n) {
-                const double2 a = w[k];
+                for (int i = 0; i < kDotChunk; ++i) acc[i] = 0.0;
+                GRID_LOOP(k, n) {
+                    const double2 a = w[k];
 #pragma unroll
-                for (int i = 0; i < kMaxDots; ++i)
-                    if (i <= j) {
-                        const double2 b = v[i][k];
-                        acc[i] = fma(a.x, b.x, fma(a.y, b.y, acc[i]));
+                    for (int i = 0; i < kDotChunk; ++i)
+                        if (c0 + i <= j) {
+                            const double2 b = v[c0 + i][k];
+                            acc[i] = fma(a.x, b.x, fma(a.y, b.y, acc[i]));
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < kDotChunk; ++i)
+                    if (c0 + i <= j) {
+                        double t = acc[i];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c0 + i] = t;
                     }
             }
-#pragma unroll
-            for (int i = 0; i < kMaxDots; ++i)
-                if (i <= j) {
-                    double t = acc[i];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = t;
-                }
             __syncthreads();
             for (int i = threadIdx.x; i <= j; i += blockDim.x) {
                 double t = 0.0;
@@ -339,7 +350,9 @@ __global__ void gather_basis_kernel(double2* __restrict__ y, double2* const* __r
 
 }  // namespace
 
-int arnoldi_grid(size_t n) {
+// co-resident Arnoldi blocks on the current device (the three batched stage solves'
+// concurrent cooperative launches must fit together)
+int arnoldi_capacity() {
     static std::atomic<int> cap[64];  // co-resident blocks per device (0 = unknown)
     int dev = 0;
     cudaGetDevice(&dev);
@@ -351,6 +364,17 @@ int arnoldi_grid(size_t n) {
         c = per_sm * sms;
         if (dev >= 0 && dev < 64) cap[dev].store(c, std::memory_order_release);
     }
+    return c;
+}
+
+// Grid of one Arnoldi launch: at most 2 blocks per SM even where 4 fit -- block 0 sums
+// the per-block partials of every dot in sequence, which a wider grid only lengthens
+// (measured: 400^2 Newton-Krylov step 16.4 ms at 296 blocks, 19.2 ms at 592)
+int arnoldi_grid(size_t n) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int c = std::min(arnoldi_capacity(), 2 * sms);
     const int b = blocks(n);
     return b < c ? b : c;
 }

@@ -4,12 +4,17 @@
 // interfaces each entry point replaces.
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstddef>
 #include <cstdlib>
+#include <dlfcn.h>
+
+#include <type_traits>
+
 #include <cstring>
 #include <string>
 #include <utility>
@@ -63,6 +68,8 @@ struct mb4cu_ctx {
     mb4cu::StepStatus* d_status = nullptr;
     mb4cu::StepStatus* h_status = nullptr;     // pinned
     bool batched = true;                       // mb4cu_run enqueues steps device-resident
+    struct DistNative* dn = nullptr;           // native NCCL stepping of a sub-domain (mb4cu_dist_*)
+    bool first_poly_auto = false;
     int obs_grid = 0;                          // CTAs d_obs_march holds partial sums for
     // batched stepping (mb4cu_run): per-step status and residual slots, the abort flag and
     // per-step events, allocated on first use
@@ -729,7 +736,7 @@ int krb_alloc(mb4cu_ctx* ctx, size_t len) {
     const int m = kKrylovRestart;
     const size_t per = static_cast<size_t>(m + 4);
     // concurrent cooperative Arnoldi launches must fit the device together
-    int cap = mb4cu::arnoldi_grid(size_t(1) << 40);
+    const int cap = mb4cu::arnoldi_capacity();
     if (3 * per * len * sizeof(double2) > kKrBatchBytes || 3 * mb4cu::krylov_blocks(len) > cap) return 0;
     if (B.mem) {
         if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return 0;
@@ -1244,7 +1251,9 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         delete ctx;
         return MB4CU_INVALID;
     }
-    ctx->pitch = p->nx + 2 * p->ghost;
+    // sub-domain rows padded to a multiple of 8 sites (128 B): every row of a band then
+    // has one alignment, which the sweeps' cp.async ring placement relies on
+    ctx->pitch = p->ghost > 0 ? (p->nx + 2 * p->ghost + 7) / 8 * 8 : p->nx;
     ctx->alloc_n = static_cast<size_t>(ctx->pitch) * (p->ny + 2 * p->ghost);
     ctx->scheme = *scheme;
     for (size_t k = 0; k < ctx->n; ++k) ctx->vmax = std::max(ctx->vmax, std::fabs(p->V[k]));
@@ -1260,6 +1269,7 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     // cross-check knob: MB4CU_KR_BATCH=0 solves the stage systems one after the other
     if (const char* kb = std::getenv("MB4CU_KR_BATCH")) ctx->kr_batch = std::atoi(kb) != 0;
     ctx->first_poly = p->first_poly != 0 ? p->first_poly : (ctx->vmin >= 0.0 && ctx->gamma <= 0.0 ? 2 : 1);
+    ctx->first_poly_auto = p->first_poly == 0;
     // the cross-check kernels (and the v1 march the production kernel falls back to for
     // pairs it does not compile) run the per-stage Neumann recursion
     if (p->kernel != 0 || !mb4cu::march2_supported(ctx->mf, m)) ctx->first_poly = 1;
@@ -1331,6 +1341,11 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
     return MB4CU_OK;
 }
 
+namespace {
+void dn_free(mb4cu_ctx* ctx);
+void dn_state_set(mb4cu_ctx* ctx);  // a new resident state: its halos are not exchanged yet
+}  // namespace
+
 int mb4cu_destroy(mb4cu_ctx* ctx) {
     if (!ctx) return MB4CU_OK;
     cudaSetDevice(ctx->device);
@@ -1349,6 +1364,7 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs_march);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
+    dn_free(ctx);
     cudaFree(ctx->d_bstatus);
     cudaFreeHost(ctx->h_bstatus);
     cudaFree(ctx->d_brmax);
@@ -1443,6 +1459,7 @@ int mb4cu_set_state(mb4cu_ctx* ctx, const double* u) {
     MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->obs_cached = false;
     ctx->amax2_valid = false;
+    dn_state_set(ctx);
     return MB4CU_OK;
 }
 
@@ -1459,6 +1476,7 @@ int mb4cu_set_state_device(mb4cu_ctx* ctx, const double* u) {
     MB4_CUDA(ctx, copy_state(ctx, ctx->u0, u, true, cudaMemcpyDeviceToDevice));
     ctx->obs_cached = false;
     ctx->amax2_valid = false;
+    dn_state_set(ctx);
     return MB4CU_OK;
 }
 
@@ -2054,7 +2072,8 @@ int mb4cu_sweep(mb4cu_ctx* ctx, double h, int s, double* local_rmax, double* loc
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev0, ctx->stream));
     MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U, ctx->d_rmax_arr,
                                             ctx->d_obs_march, ctx->d_status, 1, -1.0, s == 0 ? 1 : 0, c,
-                                            ctx->device, ctx->stream, ctx->ghost, s));
+                                            ctx->device, ctx->stream, ctx->ghost, s, -1, 0, nullptr, 0, 0, nullptr,
+                                            ctx->pitch));
     if (ctx->profiling) MB4_CUDA(ctx, cudaEventRecord(ctx->pev1, ctx->stream));
     MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(mb4cu::StepStatus), cudaMemcpyDeviceToHost,
                                   ctx->stream));
@@ -2077,9 +2096,14 @@ namespace {
 
 // Output rectangles of a region of the sub-domain: 0 all, 1 the boundary frame of
 // width ghost (the sites the neighbours' halos need), 2 the interior (needs no halo).
-int region_rects(const mb4cu_ctx* ctx, int region, int rects[4][4]) {
+int region_rects(const mb4cu_ctx* ctx, int region, int rects[4][4], int s) {
     const int w = ctx->ghost, nx = ctx->nx, ny = ctx->ny;
     const bool thin = nx <= 2 * w || ny <= 2 * w;  // no interior: the frame is everything
+    // west / east frame strips one sweep band wide (not `ghost` columns): a band computes
+    // its full width anyway, so a ghost-wide strip would redo ~(band - ghost) columns per
+    // row; large sub-domains only (small ones keep the ghost-wide frame and an interior)
+    const int tx = mb4cu::march2_band_width(ctx->mf, ctx->m, s == 0);
+    const int wx = tx > w && nx >= 4 * tx ? tx : w;
     if (region == 0 || (region == 1 && thin)) {
         const int r[4] = {0, 0, nx, ny};
         std::memcpy(rects[0], r, sizeof(r));
@@ -2087,26 +2111,39 @@ int region_rects(const mb4cu_ctx* ctx, int region, int rects[4][4]) {
     }
     if (region == 2) {
         if (thin) return 0;
-        const int r[4] = {w, w, nx - 2 * w, ny - 2 * w};
+        const int r[4] = {wx, w, nx - 2 * wx, ny - 2 * w};
         std::memcpy(rects[0], r, sizeof(r));
         return 1;
     }
-    const int f[4][4] = {{0, 0, nx, w}, {0, ny - w, nx, w}, {0, w, w, ny - 2 * w}, {nx - w, w, w, ny - 2 * w}};
+    const int f[4][4] = {{0, 0, nx, w}, {0, ny - w, nx, w}, {0, w, wx, ny - 2 * w}, {nx - wx, w, wx, ny - 2 * w}};
     std::memcpy(rects, f, sizeof(f));
     return 4;
 }
 
 }  // namespace
 
+namespace {
+int sweep_region_impl(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap, double* dev_out7,
+                      const int* skip, bool count);
+}  // namespace
+
 int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap,
                        double* dev_out7) {
+    return sweep_region_impl(ctx, h, s, final_guess, region, grid_cap, dev_out7, nullptr, true);
+}
+
+namespace {
+int sweep_region_impl(mb4cu_ctx* ctx, double h, int s, int final_guess, int region, int grid_cap, double* dev_out7,
+                      const int* skip, bool count) {
     if (!ctx || ctx->ghost <= 0) return fail(ctx, MB4CU_INVALID, "sweep: sub-domain contexts only");
     if (!(h > 0.0) || s < 0 || region < 0 || region > 2 || (region != 1 && !dev_out7))
         return fail(ctx, MB4CU_INVALID, "sweep: h > 0, s >= 0, region 0..2, output buffer");
     MB4_CUDA(ctx, cudaSetDevice(ctx->device));
     const SweepConsts c = make_consts(ctx, h);
     int rects[4][4];
-    const int nrect = region_rects(ctx, region, rects);
+    const int nrect = region_rects(ctx, region, rects, s);
+    mb4cu::BatchCtl skipctl{};
+    skipctl.skip = skip;
     // the frame (or the whole domain) starts the residual max; the interior adds to it
     if (region != 2) MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax_arr, 0, 2 * sizeof(unsigned long long), ctx->stream));
     if (nrect > 0) {
@@ -2114,7 +2151,7 @@ int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int reg
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status, 1, -1.0,
                                                 s == 0 ? 1 : 0, c, ctx->device, ctx->stream, ctx->ghost, s,
                                                 final_guess && s > 0 ? s : -1, nrect, rects, region == 2 ? 1 : 0,
-                                                region == 2 ? grid_cap : 0));
+                                                region == 2 ? grid_cap : 0, skip ? &skipctl : nullptr, ctx->pitch));
         if (ctx->profiling) ctx->prof.launches += 1;
     }
     if (region != 1) {
@@ -2126,13 +2163,14 @@ int mb4cu_sweep_region(mb4cu_ctx* ctx, double h, int s, int final_guess, int reg
         MB4_CUDA(ctx, cudaMemcpyAsync(dev_out7, reinterpret_cast<const char*>(ctx->d_status) +
                                                     offsetof(mb4cu::StepStatus, rlast),
                                       sizeof(double) * (2 + mb4cu::kObsFields), cudaMemcpyDeviceToDevice, ctx->stream));
-        if (ctx->profiling) {
+        if (ctx->profiling && count) {
             ctx->prof.sweeps += 1;
             ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (s == 0 ? 72.0 : (final_guess ? 88.0 : 120.0));
         }
     }
     return MB4CU_OK;
 }
+}  // namespace
 
 int mb4cu_sweep_async(mb4cu_ctx* ctx, double h, int s, int final_guess, double* dev_out7) {
     return mb4cu_sweep_region(ctx, h, s, final_guess, 0, 0, dev_out7);
@@ -2310,4 +2348,505 @@ int mb4cu_ns_commit(mb4cu_ctx* ctx) {
     return MB4CU_OK;
 }
 
+// ---- Native multi-GPU stepping over NCCL (mb4cu_dist_*) -----------------------------
+// The decomposed step without the host in the sweep loop: per sweep the boundary frame,
+// its ghost-wide halo exchange (NCCL send / recv on a communication stream) concurrently
+// with the interior, the all-reduce of [||r||_inf, energy sums, max|u0|^2] and the
+// convergence test on the device (dist_converge_kernel), whose flag turns the sweeps
+// enqueued ahead into no-ops.  The host enqueues the sweeps the previous step's count
+// predicts and reads once per step when the prediction holds (dist.py's Python loop reads
+// once per sweep).  Every NCCL call of a communicator goes through its one stream, in
+// the same order on every rank.  libnccl is opened at run time (the process's own, e.g.
+// torch's), so single-GPU users do not depend on it.
+
+struct NcclApi {
+    void* so = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+namespace {
+
+bool nccl_open(NcclApi& api, const char* path, std::string& why) {
+    const char* name = path && *path ? path : "libnccl.so.2";
+    api.so = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (!api.so) {
+        why = std::string("dlopen(") + name + "): " + dlerror();
+        return false;
+    }
+    bool ok = true;
+    auto sym = [&](auto& fn, const char* s) {
+        fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(api.so, s));
+        if (!fn) {
+            ok = false;
+            why = std::string("libnccl lacks ") + s;
+        }
+    };
+    sym(api.getUniqueId, "ncclGetUniqueId");
+    sym(api.commInitRank, "ncclCommInitRank");
+    sym(api.commDestroy, "ncclCommDestroy");
+    sym(api.groupStart, "ncclGroupStart");
+    sym(api.groupEnd, "ncclGroupEnd");
+    sym(api.send, "ncclSend");
+    sym(api.recv, "ncclRecv");
+    sym(api.allReduce, "ncclAllReduce");
+    sym(api.errorString, "ncclGetErrorString");
+    return ok;
+}
+
+constexpr int kOutStride = 8;  // doubles per sweep row of the reduction buffer (7 used)
+
+}  // namespace
+
+struct DistNative {
+    NcclApi api;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0, px = 1, py = 1;
+    int nbr[4] = {0, 0, 0, 0};    // west, east, south, north neighbour ranks
+    bool force_p2p = false;       // exchange through NCCL even with oneself (tests on one GPU)
+    int grid_cap = 0;             // interior launches leave SMs to NCCL's kernels
+    cudaStream_t comms = nullptr;
+    cudaEvent_t ev_frame = nullptr, ev_int = nullptr, ev_x = nullptr;
+    double* d_out = nullptr;      // [max_iters][kOutStride]
+    double* h_out = nullptr;      // pinned
+    int* d_state = nullptr;       // [4]: done, sweeps, diverged
+    int* h_state = nullptr;       // pinned
+    double* sbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* rbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t cap = 0;               // doubles per halo buffer
+    double2* u0bak = nullptr;     // halving backup (padded array)
+    bool u0_halo_ok = false;
+};
+
+namespace {
+
+#define MB4_NCCL(ctx, call)                                                                       \
+    do {                                                                                          \
+        const ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                                    \
+            return fail(ctx, MB4CU_COMM_ERROR,                                                    \
+                        std::string("NCCL: ") + (ctx)->dn->api.errorString(r_) + " at " #call);  \
+    } while (0)
+
+int dn_exchange(mb4cu_ctx* ctx, int field) {
+    DistNative& D = *ctx->dn;
+    const struct {
+        int lo, hi, extent;
+    } phases[2] = {{0, 1, D.px}, {2, 3, D.py}};
+    for (const auto& ph : phases) {
+        if (ph.extent == 1 && !D.force_p2p) {
+            // this rank is its own neighbour: owned strips straight into the opposite ghosts
+            double2* arr[3] = {ctx->u0, nullptr, nullptr};
+            int narr = 1;
+            if (field >= 2) {
+                narr = 3;
+                for (int q = 0; q < 3; ++q) arr[q] = ctx->U[(field - 2) & 1][q];
+            }
+            MB4_CUDA(ctx, mb4cu::launch_halo_wrap(field == 1 ? nullptr : arr, field == 1 ? ctx->V : nullptr, narr,
+                                                  ctx->pitch, ctx->ghost, ctx->nx, ctx->ny, halo_width(ctx, field),
+                                                  &ph == &phases[0] ? 0 : 1, D.comms));
+            ctx->prof.other_launches += 1;
+            continue;
+        }
+        const size_t n = mb4cu_halo_count(ctx, field, ph.lo);
+        const int sides[2] = {ph.lo, ph.hi};
+        for (int side : sides) {
+            int x0, y0, w, h;
+            halo_rect(ctx, field, side, true, &x0, &y0, &w, &h);
+            if (field == 1) {
+                MB4_CUDA(ctx, mb4cu::launch_halo_copy1(ctx->V, ctx->pitch, ctx->ghost, x0, y0, w, h, D.sbuf[side],
+                                                       true, D.comms));
+            } else {
+                double2* arr[3] = {ctx->u0, nullptr, nullptr};
+                int narr = 1;
+                if (field != 0) {
+                    narr = 3;
+                    for (int q = 0; q < 3; ++q) arr[q] = ctx->U[(field - 2) & 1][q];
+                }
+                MB4_CUDA(ctx, mb4cu::launch_halo_copy2(arr, narr, ctx->pitch, ctx->ghost, x0, y0, w, h,
+                                                       reinterpret_cast<double2*>(D.sbuf[side]), true, D.comms));
+            }
+        }
+        double* src_for_hi = D.sbuf[ph.lo];  // periodic wrap onto this rank: my low strip is my high ghost
+        double* src_for_lo = D.sbuf[ph.hi];
+        if (ph.extent > 1 || D.force_p2p) {
+            // sends [low strip -> low neighbour, high strip -> high neighbour], receives
+            // [high ghost <- high neighbour, low ghost <- low neighbour] (dist.HaloExchange's
+            // order: correct when both neighbours are the same rank, or this rank)
+            MB4_NCCL(ctx, D.api.groupStart());
+            MB4_NCCL(ctx, D.api.send(D.sbuf[ph.lo], n, ncclDouble, D.nbr[ph.lo], D.comm, D.comms));
+            MB4_NCCL(ctx, D.api.send(D.sbuf[ph.hi], n, ncclDouble, D.nbr[ph.hi], D.comm, D.comms));
+            MB4_NCCL(ctx, D.api.recv(D.rbuf[ph.hi], n, ncclDouble, D.nbr[ph.hi], D.comm, D.comms));
+            MB4_NCCL(ctx, D.api.recv(D.rbuf[ph.lo], n, ncclDouble, D.nbr[ph.lo], D.comm, D.comms));
+            MB4_NCCL(ctx, D.api.groupEnd());
+            src_for_hi = D.rbuf[ph.hi];
+            src_for_lo = D.rbuf[ph.lo];
+        }
+        const int dst[2] = {ph.hi, ph.lo};
+        double* src[2] = {src_for_hi, src_for_lo};
+        for (int k = 0; k < 2; ++k) {
+            int x0, y0, w, h;
+            halo_rect(ctx, field, dst[k], false, &x0, &y0, &w, &h);
+            if (field == 1) {
+                MB4_CUDA(ctx, mb4cu::launch_halo_copy1(ctx->V, ctx->pitch, ctx->ghost, x0, y0, w, h, src[k], false,
+                                                       D.comms));
+            } else {
+                double2* arr[3] = {ctx->u0, nullptr, nullptr};
+                int narr = 1;
+                if (field != 0) {
+                    narr = 3;
+                    for (int q = 0; q < 3; ++q) arr[q] = ctx->U[(field - 2) & 1][q];
+                }
+                MB4_CUDA(ctx, mb4cu::launch_halo_copy2(arr, narr, ctx->pitch, ctx->ghost, x0, y0, w, h,
+                                                       reinterpret_cast<double2*>(src[k]), false, D.comms));
+            }
+        }
+        ctx->prof.other_launches += 4;
+    }
+    return MB4CU_OK;
+}
+
+// comms stream after everything enqueued so far on the compute stream, and vice versa
+int dn_comms_after_compute(mb4cu_ctx* ctx) {
+    MB4_CUDA(ctx, cudaEventRecord(ctx->dn->ev_int, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamWaitEvent(ctx->dn->comms, ctx->dn->ev_int, 0));
+    return MB4CU_OK;
+}
+int dn_compute_after_comms(mb4cu_ctx* ctx) {
+    MB4_CUDA(ctx, cudaEventRecord(ctx->dn->ev_x, ctx->dn->comms));
+    MB4_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->dn->ev_x, 0));
+    return MB4CU_OK;
+}
+
+// Sweep s of a decomposed sub-step, fully enqueued (no host wait): frame -> its exchange
+// (comms) || interior -> all-reduce -> device convergence test (comms).
+int dn_launch_sweep(mb4cu_ctx* ctx, double h, int s, bool final_guess) {
+    DistNative& D = *ctx->dn;
+    double* out = D.d_out + static_cast<size_t>(s) * kOutStride;
+    MB4_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, D.ev_x, 0));  // input halos and the convergence flag
+    if (int rc = sweep_region_impl(ctx, h, s, final_guess, 1, 0, nullptr, D.d_state, false)) return rc;
+    MB4_CUDA(ctx, cudaEventRecord(D.ev_frame, ctx->stream));
+    MB4_CUDA(ctx, cudaStreamWaitEvent(D.comms, D.ev_frame, 0));
+    if (int rc = dn_exchange(ctx, 4 + (s & 1))) return rc;  // the frame's stage set, ghost wide
+    if (int rc = sweep_region_impl(ctx, h, s, final_guess, 2, D.grid_cap, out, D.d_state, false)) return rc;
+    if (int rc = dn_comms_after_compute(ctx)) return rc;
+    MB4_NCCL(ctx, D.api.allReduce(out, out, 1, ncclDouble, ncclMax, D.comm, D.comms));
+    if (s == 0) {
+        MB4_NCCL(ctx, D.api.allReduce(out + 1, out + 1, mb4cu::kObsFields, ncclDouble, ncclSum, D.comm, D.comms));
+        MB4_NCCL(ctx, D.api.allReduce(out + 6, out + 6, 1, ncclDouble, ncclMax, D.comm, D.comms));
+    }
+    MB4_CUDA(ctx, mb4cu::launch_dist_converge(D.d_out, kOutStride, s, ctx->eps, D.d_state, D.comms));
+    MB4_CUDA(ctx, cudaEventRecord(D.ev_x, D.comms));
+    ctx->prof.other_launches += 1;
+    return MB4CU_OK;
+}
+
+int dn_read(mb4cu_ctx* ctx, int rows) {
+    DistNative& D = *ctx->dn;
+    MB4_CUDA(ctx, cudaMemcpyAsync(D.h_state, D.d_state, 4 * sizeof(int), cudaMemcpyDeviceToHost, D.comms));
+    MB4_CUDA(ctx, cudaMemcpyAsync(D.h_out, D.d_out, sizeof(double) * kOutStride * rows, cudaMemcpyDeviceToHost,
+                                  D.comms));
+    MB4_CUDA(ctx, cudaStreamSynchronize(D.comms));
+    return MB4CU_OK;
+}
+
+// global max|u0|^2 of a newly set state (all ranks), once per set_state
+int dn_refresh_amax2(mb4cu_ctx* ctx) {
+    if (ctx->amax2_valid) return MB4CU_OK;
+    DistNative& D = *ctx->dn;
+    if (int rc = dn_comms_after_compute(ctx)) return rc;  // (after the set_state copy)
+    const size_t off = static_cast<size_t>(ctx->ghost) * ctx->pitch + ctx->ghost;
+    MB4_CUDA(ctx, cudaMemsetAsync(ctx->d_rmax, 0, sizeof(unsigned long long), D.comms));
+    MB4_CUDA(ctx, mb4cu::launch_amax2_2d(ctx->u0 + off, ctx->nx, ctx->ny, ctx->pitch, ctx->d_rmax, D.comms));
+    // non-negative doubles: max of the bit patterns == max of the values; reduce as doubles
+    MB4_NCCL(ctx, D.api.allReduce(ctx->d_rmax, ctx->d_rmax, 1, ncclDouble, ncclMax, D.comm, D.comms));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_rmax, ctx->d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  D.comms));
+    MB4_CUDA(ctx, cudaStreamSynchronize(D.comms));
+    track_amax2(ctx, decode_bits(*ctx->h_rmax));
+    return MB4CU_OK;
+}
+
+// One decomposed sub-step of size h: *sweeps, *last_res, entry sums5 + amax2 in out7.
+int dn_substep(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res, double* entry7) {
+    DistNative& D = *ctx->dn;
+    MB4_CUDA(ctx, cudaMemsetAsync(D.d_state, 0, 4 * sizeof(int), D.comms));
+    if (!D.u0_halo_ok) {
+        if (int rc = dn_comms_after_compute(ctx)) return rc;
+        if (int rc = dn_exchange(ctx, 0)) return rc;
+    }
+    MB4_CUDA(ctx, cudaEventRecord(D.ev_x, D.comms));
+    D.u0_halo_ok = false;
+    const int guess = ctx->last_sweeps;  // the previous sub-step's count (0: none)
+    const int ahead = std::min(std::max(guess, 1), ctx->max_iters);
+    for (int s = 0; s < ahead; ++s)
+        if (int rc = dn_launch_sweep(ctx, h, s, s > 0 && s == guess - 1)) return rc;
+    int launched = ahead - 1;
+    bool last_was_final = launched > 0 && launched == guess - 1;
+    bool redone = false;
+    for (;;) {
+        if (int rc = dn_read(ctx, launched + 1)) return rc;
+        std::memcpy(entry7, D.h_out + 1, sizeof(double) * 6);  // sweep 0: the entry state's sums, max|u0|^2
+        const int done = D.h_state[0], diverged = D.h_state[2];
+        if (diverged) {
+            *last_res = INFINITY;
+            ctx->last_sweeps = 0;
+            return fail(ctx, MB4CU_NONCONVERGED, "stage iteration diverged (non-finite update)");
+        }
+        if (done) {
+            const int sw = D.h_state[1];
+            *sweeps = sw;
+            *last_res = D.h_out[static_cast<size_t>(sw - 1) * kOutStride];
+            mb4cu_commit_step(ctx, sw);
+            D.u0_halo_ok = true;  // the last sweep's exchange carried U3 ghost wide
+            ctx->last_sweeps = sw;
+            track_amax2(ctx, D.h_out[6]);
+            adapt_neumann(ctx, sw);
+            if (ctx->profiling) {
+                ctx->prof.sweeps += sw;
+                const bool spec_hit = sw >= 2 && sw == guess && !redone;  // the U3-only final sweep converged
+                ctx->prof.alg_bytes += static_cast<double>(ctx->n) * (72.0 + 120.0 * (sw - 1) - (spec_hit ? 32.0 : 0.0));
+            }
+            return MB4CU_OK;
+        }
+        *last_res = D.h_out[static_cast<size_t>(launched) * kOutStride];
+        if (last_was_final) {
+            // the predicted final sweep stored U3 only and did not converge: repeat it with all stages
+            if (int rc = dn_launch_sweep(ctx, h, launched, false)) return rc;
+            last_was_final = false;
+            redone = true;
+            ctx->prof.redone += 1;
+            continue;
+        }
+        if (launched + 1 >= ctx->max_iters) break;
+        ++launched;
+        if (int rc = dn_launch_sweep(ctx, h, launched, false)) return rc;
+    }
+    ctx->last_sweeps = 0;
+    return fail(ctx, MB4CU_NONCONVERGED,
+                "stage iteration: no convergence after " + std::to_string(ctx->max_iters) + " sweeps");
+}
+
+void dn_state_set(mb4cu_ctx* ctx) {
+    if (ctx->dn) ctx->dn->u0_halo_ok = false;
+}
+
+void dn_free(mb4cu_ctx* ctx) {
+    DistNative* D = ctx->dn;
+    if (!D) return;
+    if (D->comms) cudaStreamSynchronize(D->comms);
+    if (D->comm && D->api.commDestroy) D->api.commDestroy(D->comm);
+    for (int k = 0; k < 4; ++k) {
+        cudaFree(D->sbuf[k]);
+        cudaFree(D->rbuf[k]);
+    }
+    cudaFree(D->d_out);
+    cudaFreeHost(D->h_out);
+    cudaFree(D->d_state);
+    cudaFreeHost(D->h_state);
+    cudaFree(D->u0bak);
+    if (D->ev_frame) cudaEventDestroy(D->ev_frame);
+    if (D->ev_int) cudaEventDestroy(D->ev_int);
+    if (D->ev_x) cudaEventDestroy(D->ev_x);
+    if (D->comms) cudaStreamDestroy(D->comms);
+    delete D;
+    ctx->dn = nullptr;
+}
+
+}  // namespace
+
+int mb4cu_nccl_unique_id(const char* libnccl, unsigned char id[128]) {
+    g_create_error.clear();
+    if (!id) return MB4CU_INVALID;
+    NcclApi api;
+    if (!nccl_open(api, libnccl, g_create_error)) return MB4CU_COMM_ERROR;
+    ncclUniqueId u;
+    const ncclResult_t r = api.getUniqueId(&u);
+    if (r != ncclSuccess) {
+        g_create_error = std::string("ncclGetUniqueId: ") + api.errorString(r);
+        return MB4CU_COMM_ERROR;
+    }
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId layout");
+    std::memcpy(id, &u, 128);
+    return MB4CU_OK;
+}
+
+int mb4cu_dist_attach(mb4cu_ctx* ctx, const char* libnccl, const unsigned char id[128], int nranks, int rank,
+                      const int neighbours[4], int px, int py, int grid_cap, int force_p2p, int adaptive_m) {
+    if (!ctx || ctx->ghost <= 0 || !id || !neighbours || nranks < 1 || rank < 0 || rank >= nranks || px < 1 ||
+        py < 1 || px * py != nranks)
+        return fail(ctx, MB4CU_INVALID, "dist_attach: sub-domain context, id, neighbours, px * py == nranks");
+    if (ctx->kernel != 0 || !mb4cu::march2_supported(ctx->mf, ctx->m) || ctx->mf < 4)
+        return fail(ctx, MB4CU_INVALID, "dist_attach: the production sweep kernels (neumann_first >= 4)");
+    if (ctx->dn) return fail(ctx, MB4CU_INVALID, "dist_attach: already attached");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    ctx->dn = new DistNative();
+    DistNative& D = *ctx->dn;
+    std::string why;
+    if (!nccl_open(D.api, libnccl, why)) {
+        dn_free(ctx);
+        return fail(ctx, MB4CU_COMM_ERROR, why);
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    D.nranks = nranks;
+    D.rank = rank;
+    D.px = px;
+    D.py = py;
+    for (int k = 0; k < 4; ++k) D.nbr[k] = neighbours[k];
+    D.force_p2p = force_p2p != 0;
+    D.grid_cap = grid_cap;
+    auto bail = [&](int rc) {
+        dn_free(ctx);
+        return rc;
+    };
+    const ncclResult_t r = D.api.commInitRank(&D.comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+        const std::string e = std::string("ncclCommInitRank: ") + D.api.errorString(r);
+        dn_free(ctx);
+        return fail(ctx, MB4CU_COMM_ERROR, e);
+    }
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&D.comms, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(ctx, e, "stream"));
+    if ((e = cudaEventCreateWithFlags(&D.ev_frame, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&D.ev_int, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&D.ev_x, cudaEventDisableTiming)) != cudaSuccess)
+        return bail(cuda_fail(ctx, e, "event"));
+    for (int f = 0; f < 6; ++f)
+        for (int side = 0; side < 4; ++side) D.cap = std::max(D.cap, mb4cu_halo_count(ctx, f, side));
+    for (int k = 0; k < 4; ++k)
+        if ((e = cudaMalloc(&D.sbuf[k], D.cap * sizeof(double))) != cudaSuccess ||
+            (e = cudaMalloc(&D.rbuf[k], D.cap * sizeof(double))) != cudaSuccess)
+            return bail(cuda_fail(ctx, e, "cudaMalloc(halo)"));
+    if ((e = cudaMalloc(&D.d_out, sizeof(double) * kOutStride * (ctx->max_iters + 1))) != cudaSuccess ||
+        (e = cudaMallocHost(&D.h_out, sizeof(double) * kOutStride * (ctx->max_iters + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&D.d_state, 4 * sizeof(int))) != cudaSuccess ||
+        (e = cudaMallocHost(&D.h_state, 4 * sizeof(int))) != cudaSuccess)
+        return bail(cuda_fail(ctx, e, "cudaMalloc(dist)"));
+    // the whole lattice's max|V| and min V: every rank then places the same Chebyshev
+    // polynomial (and the same later-sweep depth policy) as the single domain would
+    double* d2 = nullptr;
+    if ((e = cudaMalloc(&d2, 2 * sizeof(double))) != cudaSuccess) return bail(cuda_fail(ctx, e, "cudaMalloc"));
+    const double h2[2] = {ctx->vmax, -ctx->vmin};
+    cudaMemcpy(d2, h2, sizeof(h2), cudaMemcpyHostToDevice);
+    const ncclResult_t r2 = D.api.allReduce(d2, d2, 2, ncclDouble, ncclMax, D.comm, D.comms);
+    double g2[2] = {0.0, 0.0};
+    cudaStreamSynchronize(D.comms);
+    cudaMemcpy(g2, d2, sizeof(g2), cudaMemcpyDeviceToHost);
+    cudaFree(d2);
+    if (r2 != ncclSuccess) return bail(fail(ctx, MB4CU_COMM_ERROR, "NCCL all-reduce of max|V|"));
+    ctx->vmax = g2[0];
+    ctx->vmin = -g2[1];
+    if (ctx->first_poly_auto) ctx->first_poly = ctx->vmin >= 0.0 && ctx->gamma <= 0.0 ? 2 : 1;
+    ctx->rho_override = 0.0;
+    ctx->m_auto = adaptive_m != 0 && mb4cu::march2_supported(ctx->mf, 2) && ctx->ghost >= 3;
+    ctx->last_sweeps = 0;
+    // V halos once (stream-ordered after set_state / create)
+    if (int rc = dn_comms_after_compute(ctx)) return bail(rc);
+    if (int rc = dn_exchange(ctx, 1)) return bail(rc);
+    if ((e = cudaStreamSynchronize(D.comms)) != cudaSuccess) return bail(cuda_fail(ctx, e, "exchange(V)"));
+    return MB4CU_OK;
+}
+
+int mb4cu_dist_step(mb4cu_ctx* ctx, double h, mb4cu_stats* stats, double* entry_sums5) {
+    if (!ctx || !ctx->dn) return fail(ctx, MB4CU_INVALID, "dist_step: no NCCL transport (mb4cu_dist_attach)");
+    if (!(h > 0.0)) return fail(ctx, MB4CU_INVALID, "mb4_step: h must be positive");
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    DistNative& D = *ctx->dn;
+    if (int rc = dn_refresh_amax2(ctx)) return rc;
+    double last = 0.0, entry7[6] = {0, 0, 0, 0, 0, 0};
+    int rc = MB4CU_NONCONVERGED, used = 0, total = 0;
+    const size_t pb = ctx->alloc_n * sizeof(double2);
+    for (int hv = 0; hv <= ctx->max_halvings; ++hv) {
+        const int sub = 1 << hv;
+        if (hv == 1) {
+            if (!D.u0bak) MB4_CUDA(ctx, cudaMalloc(&D.u0bak, pb));
+            // (the first attempt left u0 untouched: only commits move it)
+            MB4_CUDA(ctx, cudaMemcpyAsync(D.u0bak, ctx->u0, pb, cudaMemcpyDeviceToDevice, ctx->stream));
+        } else if (hv > 1) {
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, D.u0bak, pb, cudaMemcpyDeviceToDevice, ctx->stream));
+            D.u0_halo_ok = false;
+        }
+        bool ok = true;
+        int attempt = 0;
+        for (int k = 0; k < sub; ++k) {
+            int sw = 0;
+            double e7[6] = {0, 0, 0, 0, 0, 0};
+            rc = dn_substep(ctx, h / sub, &sw, &last, e7);
+            if (hv == 0 && k == 0) std::memcpy(entry7, e7, sizeof(e7));  // the step's entry state
+            attempt += sw;
+            if (rc == MB4CU_NONCONVERGED) {
+                ok = false;
+                break;
+            }
+            if (rc != MB4CU_OK) return rc;
+        }
+        if (ok) {
+            used = hv;
+            total = attempt;
+            rc = MB4CU_OK;
+            break;
+        }
+    }
+    if (rc != MB4CU_OK) {
+        if (ctx->max_halvings >= 1 && D.u0bak) {
+            MB4_CUDA(ctx, cudaMemcpyAsync(ctx->u0, D.u0bak, pb, cudaMemcpyDeviceToDevice, ctx->stream));
+            D.u0_halo_ok = false;
+        }
+        MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (stats) stats->last_residual = last;
+        return fail(ctx, MB4CU_NONCONVERGED,
+                    "mb4_step: no convergence after " + std::to_string(ctx->max_halvings) + " step halvings");
+    }
+    if (entry_sums5) std::memcpy(entry_sums5, entry7, sizeof(double) * mb4cu::kObsFields);
+    if (stats) {
+        stats->newton_iters += total;
+        stats->halvings += used;
+        stats->last_residual = last;
+    }
+    return MB4CU_OK;
+}
+
+int mb4cu_dist_observables(mb4cu_ctx* ctx, double* sums5) {
+    if (!ctx || !ctx->dn || !sums5) return fail(ctx, MB4CU_INVALID, "dist_observables: attached context, output");
+    DistNative& D = *ctx->dn;
+    MB4_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (!D.u0_halo_ok) {
+        if (int rc = dn_comms_after_compute(ctx)) return rc;
+        if (int rc = dn_exchange(ctx, 0)) return rc;
+        D.u0_halo_ok = true;
+    }
+    if (int rc = dn_compute_after_comms(ctx)) return rc;
+    mb4cu::ObsArgs a{};
+    a.nx = ctx->nx;
+    a.ny = ctx->ny;
+    a.cx = ctx->cx;
+    a.cy = ctx->cy;
+    a.diag = 2.0 * ctx->cx + 2.0 * ctx->cy;
+    a.u = ctx->u0;
+    a.V = ctx->V;
+    a.partial = ctx->d_obs_partial;
+    MB4_CUDA(ctx, mb4cu::launch_observables_ghost(a, ctx->ghost, ctx->pitch, ctx->d_obs5, ctx->stream));
+    if (int rc = dn_comms_after_compute(ctx)) return rc;
+    MB4_NCCL(ctx, D.api.allReduce(ctx->d_obs5, ctx->d_obs5, mb4cu::kObsFields, ncclDouble, ncclSum, D.comm, D.comms));
+    MB4_CUDA(ctx, cudaMemcpyAsync(ctx->h_obs5, ctx->d_obs5, sizeof(double) * mb4cu::kObsFields,
+                                  cudaMemcpyDeviceToHost, D.comms));
+    MB4_CUDA(ctx, cudaStreamSynchronize(D.comms));
+    std::memcpy(sums5, ctx->h_obs5, sizeof(double) * mb4cu::kObsFields);
+    return MB4CU_OK;
+}
+
+int mb4cu_dist_detach(mb4cu_ctx* ctx) {
+    if (!ctx) return MB4CU_INVALID;
+    dn_free(ctx);
+    return MB4CU_OK;
+}
 }  // extern "C"

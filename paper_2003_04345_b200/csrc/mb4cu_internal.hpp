@@ -164,6 +164,7 @@ struct StepArgs {
     int expect_sweeps;
     int switch_sweeps;          // 0: none
     double amax2_lo, amax2_hi;  // the batch's step constants hold while max|u0|^2 stays inside
+    const int* skip;            // != nullptr and *skip != 0: the launch does nothing (read only)
 };
 
 // batch control of launch_step_march2 (see StepArgs::batch_abort)
@@ -172,6 +173,7 @@ struct BatchCtl {
     int expect_sweeps;
     int switch_sweeps;
     double amax2_lo, amax2_hi;
+    const int* skip;  // (decomposed sub-steps: the device convergence flag)
 };
 
 // ---- the other integrators (methods.cu) ------------------------------------
@@ -206,6 +208,7 @@ void avf4_coupling(double mt[2][2]);
 // One Arnoldi (CGS2) step in one cooperative launch (krylov.cu); partial must hold
 // (j+1) * arnoldi_grid(n) doubles, hbuf j+1, hcol j+2 (device)
 int arnoldi_grid(size_t n);
+int arnoldi_capacity();  // co-resident Arnoldi blocks on the current device
 cudaError_t kr_arnoldi(double2* w, double2* const* v_dev, int j, size_t n, double* partial, double* hbuf,
                        double* hcol, cudaStream_t s, int* jdev = nullptr);
 // y = v[*jdev] (device-indexed basis vector, for graph-captured Arnoldi steps)
@@ -236,18 +239,25 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
                                const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0,
-                               const BatchCtl* batch = nullptr);
+                               const BatchCtl* batch = nullptr, int pitch = 0);
 int march2_grid_size(int mf, int m, int device);
+// output columns per band of the sub-domain sweep kernels (0: no band structure)
+int march2_band_width(int mf, int m, bool first);
 
 // Halo transfer between a padded sub-domain array set and a contiguous buffer
 // (halo.cu).  Rectangle [x0, x0+w) x [y0, y0+h) in local coordinates (ghosts
 // negative / >= n); buffer layout [array][row][col].
 cudaError_t launch_halo_copy2(double2* const* arrays, int narr, int pitch, int ghost, int x0, int y0,
                               int w, int h, double2* buf, bool pack, cudaStream_t s);
+// periodic self-wrap of a halo phase (0: columns, 1: rows) of narr double2 arrays or of d1
+cudaError_t launch_halo_wrap(double2* const* arrays, double* d1, int narr, int pitch, int ghost, int nx, int ny,
+                             int g, int phase, cudaStream_t s);
 cudaError_t launch_halo_copy1(double* array, int pitch, int ghost, int x0, int y0, int w, int h,
                               double* buf, bool pack, cudaStream_t s);
 // Energy sums of a padded sub-domain state (ghosts of u must be current).
 cudaError_t launch_observables_ghost(const ObsArgs& a, int ghost, int pitch, double* out5, cudaStream_t s);
+// device-side convergence test of sweep s of a decomposed sub-step (native NCCL stepping)
+cudaError_t launch_dist_converge(const double* out, int stride, int s, double eps, int* state, cudaStream_t st);
 // Newton-Krylov stage solver kernels (krylov.cu).
 int krylov_blocks(size_t n);
 cudaError_t kr_phibar(int nx, int ny, const double2* u0, const double2* const st[3], const double* V,

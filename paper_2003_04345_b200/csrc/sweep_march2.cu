@@ -1370,6 +1370,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     // a batched step after one that ended the batch: nothing to do (the flag was set by
     // an earlier launch on this stream, so every CTA of this grid reads the same value)
     if (a.batch_abort && *reinterpret_cast<volatile const int*>(a.batch_abort)) return;
+    if (a.skip && *reinterpret_cast<volatile const int*>(a.skip)) return;
     cg::grid_group grid = cg::this_grid();
     double acc[kAccSize] = {};  // energy sums, max |u0|^2, carries (monitor_add)
 #if MB4_CONSTS_IN_SMEM
@@ -1651,7 +1652,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
-                               int obs_accumulate, int grid_cap, const BatchCtl* batch) {
+                               int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch) {
     StepArgs a{};
     if (batch) {
         a.batch_abort = batch->abort;
@@ -1659,6 +1660,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
         a.switch_sweeps = batch->switch_sweeps;
         a.amax2_lo = batch->amax2_lo;
         a.amax2_hi = batch->amax2_hi;
+        a.skip = batch->skip;
     }
     a.nrect = nrect;
     for (int r = 0; r < nrect && r < 4; ++r)
@@ -1678,7 +1680,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
     a.eps = eps;
     a.want_obs = want_obs;
     a.ghost = ghost;
-    a.pitch = nx + 2 * ghost;
+    a.pitch = pitch > 0 ? pitch : nx + 2 * ghost;  // (sub-domain contexts pad it to 8 sites)
     a.sweep0 = sweep0;
     a.spec_sweep = spec_sweep;
 #ifdef MB4_DEBUG_FIRST_ONLY
@@ -1688,6 +1690,20 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
     MB4_MARCH2_PAIRS(MB4_PAIR_LAUNCH)
 #undef MB4_PAIR_LAUNCH
     return cudaErrorInvalidValue;
+}
+
+int march2_band_width(int mf, int m, bool first) {
+    // output columns per band of the sub-domain sweep kernels (MB4_NT_FIRST / MB4_NT_LATER wide)
+    if (!first) {
+        if (m == 1) return Geom3<1, MB4_NT_LATER>::TX;
+        return m == 2 ? Geom3<2, MB4_NT_LATER>::TX : Geom3<0, MB4_NT_LATER>::TX;
+    }
+    switch (mf) {
+        case 6: return first_sweep_tx<6, MB4_NT_FIRST>();
+        case 5: return first_sweep_tx<5, MB4_NT_FIRST>();
+        case 4: return first_sweep_tx<4, MB4_NT_FIRST>();
+        default: return 0;
+    }
 }
 
 int march2_grid_size(int mf, int m, int device) {

@@ -454,12 +454,93 @@ class DistributedSession:
         return np.array(rows), np.array(sweeps)
 
 
+def nccl_library() -> Optional[str]:
+    """Path of the libnccl.so.2 torch loads (its nvidia-nccl wheel); None: the loader's."""
+    import os
+
+    try:
+        import nvidia.nccl  # noqa: F401
+
+        path = os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib", "libnccl.so.2")
+        return path if os.path.exists(path) else None
+    except Exception:
+        return None
+
+
+def nccl_unique_id(lib=None) -> bytes:
+    """A new NCCL communicator id (rank 0), for NativeSession's broadcast."""
+    L = lib or _lib.lib()
+    buf = C.create_string_buffer(128)
+    path = nccl_library()
+    rc = L.mb4cu_nccl_unique_id(path.encode() if path else None, buf)
+    if rc:
+        raise RuntimeError(L.mb4cu_create_error().decode())
+    return buf.raw
+
+
+class NativeSession:
+    """The decomposed MB4 step inside the library (mb4cu_dist_*): NCCL transport opened from
+    torch's libnccl, the halo exchange of each sweep's boundary frame concurrent with the
+    interior, the residual / energy all-reduces and the stopping test on the device, and one
+    host read per step when the previous step's sweep count holds (DistributedSession reads
+    once per sweep).  Same step / run / observables interface as DistributedSession, and the
+    same trajectory as the single-domain kernel, bit for bit.
+
+    nccl_id: the same 128 bytes on every rank (rank 0's nccl_unique_id(), broadcast by the
+    caller, e.g. torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, dec: Decomposition, backend: "CudaBackend", nccl_id: bytes, gamma: float, cx: float,
+                 cy: float, adaptive_m: bool = False, force_p2p: bool = False, grid_cap: int = 0):
+        self.dec, self.b = dec, backend
+        self.L = backend.L
+        self.gamma, self.cx, self.cy = gamma, cx, cy
+        nb = (C.c_int * 4)(*[dec.neighbor(k) for k in (WEST, EAST, SOUTH, NORTH)])
+        path = nccl_library()
+        rc = self.L.mb4cu_dist_attach(backend.ctx, path.encode() if path else None, nccl_id, dec.px * dec.py,
+                                      dec.rank, nb, dec.px, dec.py, grid_cap, int(force_p2p), int(adaptive_m))
+        if rc:
+            raise RuntimeError(f"mb4cu_dist_attach: {self.L.mb4cu_last_error(backend.ctx).decode()}")
+        self.entry_sums: Optional[np.ndarray] = None
+
+    finish = DistributedSession.finish
+
+    def observables(self) -> np.ndarray:
+        sums = np.zeros(5)
+        self.b._chk(self.L.mb4cu_dist_observables(self.b.ctx, _lib.dptr(sums)))
+        return self.finish(sums)
+
+    def step(self, h: float) -> Tuple[int, int]:
+        """One MB4 step with the reference halving policy; returns (sweeps, halvings)."""
+        st = _lib.Stats()
+        sums = np.zeros(5)
+        rc = self.L.mb4cu_dist_step(self.b.ctx, h, C.byref(st), _lib.dptr(sums))
+        if rc == _lib.MB4CU_NONCONVERGED:
+            raise NonConvergence(self.L.mb4cu_last_error(self.b.ctx).decode(), st.last_residual)
+        self.b._chk(rc)
+        self.entry_sums = sums
+        return st.newton_iters, st.halvings
+
+    def run(self, h: float, nsteps: int):
+        """nsteps steps; returns (obs[(nsteps+1),7], sweeps[nsteps]) with the fused energy record."""
+        rows, sweeps = [], []
+        for _ in range(nsteps):
+            n, _ = self.step(h)
+            sweeps.append(n)
+            rows.append(self.finish(self.entry_sums))
+        rows.append(self.observables())
+        return np.array(rows), np.array(sweeps)
+
+    def close(self) -> None:
+        if self.b.ctx:
+            self.L.mb4cu_dist_detach(self.b.ctx)
+
+
 class CudaBackend:
     """libmb4cu sub-domain context on this rank's GPU (ghost mode)."""
 
     def __init__(self, dec: Decomposition, V_block: np.ndarray, scheme, gamma: float, cx: float, cy: float,
                  epsilon: float, max_iters: int, neumann_terms: int, device: int,
-                 neumann_first: int = 6, overlap: bool = False, reserve_sms: int = 0):
+                 neumann_first: int = 6, overlap: bool = False, reserve_sms: int = 0, max_step_halvings: int = 0):
         """overlap: sweep the boundary frame first and exchange its halos on a side
         stream while the interior is swept (the interior launch leaves reserve_sms
         SMs to the concurrent NCCL kernels)."""
@@ -473,7 +554,8 @@ class CudaBackend:
         p.cx, p.cy, p.gamma = cx, cy, gamma
         self._v = np.ascontiguousarray(V_block, dtype=np.float64)
         p.V = _lib.dptr(self._v)
-        p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, 0
+        # (halving: DistributedSession drives it; the native stepper in the library uses this)
+        p.epsilon, p.max_iters, p.max_step_halvings = epsilon, max_iters, max_step_halvings
         p.neumann_terms = neumann_terms
         self.m = neumann_terms
         p.neumann_first = neumann_first

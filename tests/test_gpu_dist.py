@@ -316,3 +316,36 @@ def test_nan_block_on_one_rank_is_reported_by_every_rank(overlap):
     if errs:
         raise errs[0]
     assert res == ["diverged", "diverged"]
+
+
+@pytest.mark.parametrize("name,force_p2p,adaptive", [("cfg2", False, False), ("cfg2", True, False),
+                                                     ("cfg1", True, True)])
+def test_native_nccl_stepper_matches_single_domain(name, force_p2p, adaptive):
+    """The decomposed step inside the library (dist.NativeSession / mb4cu_dist_*: NCCL
+    transport, device-side stopping test, one host read per step) on a 1-rank NCCL
+    communicator -- with force_p2p the periodic halos go through NCCL send / recv to
+    oneself -- reproduces the single-domain production kernel bit for bit (cfg2 changes its
+    sweep count from step to step: predicted-sweep misses and repeated final sweeps; cfg1
+    with the adaptive depth crosses the m switch)."""
+    cfg = configs.CONFIGS[name]
+    nsteps = 6
+    V, psi = configs.make_inputs(cfg)
+    dec = D.Decomposition(cfg.nx, cfg.ny, 1, 1, 0)
+    be = D.CudaBackend(dec, V, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, cfg.max_iters, 1, 0,
+                       max_step_halvings=cfg.max_step_halvings)
+    be.set_state(psi)
+    ns = D.NativeSession(dec, be, D.nccl_unique_id(), cfg.gamma, 1.0, 1.0, adaptive_m=adaptive,
+                         force_p2p=force_p2p)
+    obs_d, sweeps_d = ns.run(cfg.dt, nsteps)
+    u_d = be.get_state()
+    ns.close()
+    be.close()
+    with nls2d.Session(configs.model_for(cfg, V), nls2d.Mb4Scheme(), configs.newton_for(cfg),
+                       neumann_terms=None if adaptive else 1) as s:
+        s.set_state(psi)
+        obs, sweeps = s.run(cfg.dt, nsteps)
+        u = s.get_state()
+    assert list(sweeps_d) == list(sweeps)
+    assert np.array_equal(u_d, u), np.abs(u_d - u).max()
+    H = obs[:, 3]
+    assert np.abs(obs_d[:, 3] - H).max() <= 1e-14 * abs(H[0])
