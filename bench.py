@@ -195,10 +195,26 @@ def schedule_key(args) -> str:
     return f"mf{args.neumann_first}_m{args.neumann}"
 
 
+def _kernel_source_hash() -> str:
+    """sha256[:16] of the sweep-kernel sources (the same as tools/update_traffic.py stamps)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in ("sweep_march2.cu", "site_math.cuh", "async_copy.cuh", "mb4cu_internal.hpp"):
+        with open(os.path.join(ROOT, "paper_2003_04345_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _traffic_entry(cfg_name: str, schedule: str):
+    """The committed ncu capture of this workload, only if it was taken of the kernel
+    sources in the tree (stamped kernel_src_sha16): a stale capture is not reported."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(f"{cfg_name}_{schedule}")
+            e = json.load(f).get(f"{cfg_name}_{schedule}")
+        if e is None or e.get("kernel_src_sha16") != _kernel_source_hash():
+            return None
+        return e
     except Exception:
         return None
 
