@@ -194,20 +194,37 @@ __global__ void __launch_bounds__(kObsThreads) observables_partial_kernel(const 
         auto at = [&](int j) { return a.u + static_cast<size_t>(j) * a.nx; };
         double2 dn = at(y0 == 0 ? a.ny - 1 : y0 - 1)[i];
         double2 u = at(y0)[i];
-        for (int j = y0; j < y1; ++j) {
-            const double2* row = at(j);
-            const double2 up = at(j == a.ny - 1 ? 0 : j + 1)[i];
-            const double2 l = row[il], r = row[ir];
-            const double kx = fma(a.diag, u.x, -(a.cx * (l.x + r.x) + a.cy * (dn.x + up.x)));
-            const double ky = fma(a.diag, u.y, -(a.cx * (l.y + r.y) + a.cy * (dn.y + up.y)));
-            two_sum_add(acc[0], car[0], fma(u.x, kx, u.y * ky));  // Re conj(u) Ku
-            acc[1] += fma(u.x, ky, -u.y * kx);                    // Im conj(u) Ku (health check)
-            const double n2 = fma(u.x, u.x, u.y * u.y);
-            two_sum_add(acc[2], car[2], n2);
-            two_sum_add(acc[3], car[3], n2 * n2);
-            two_sum_add(acc[4], car[4], a.V[static_cast<size_t>(j) * a.nx + i] * n2);
-            dn = u;
-            u = up;
+        // rows in groups of kObsRows: all their loads issued before the arithmetic (the
+        // march is latency-bound with one row's loads in flight per thread)
+        constexpr int kObsRows = 4;
+        for (int j0 = y0; j0 < y1; j0 += kObsRows) {
+            double2 up[kObsRows], l[kObsRows], r[kObsRows];
+            double v[kObsRows];
+#pragma unroll
+            for (int k = 0; k < kObsRows; ++k) {
+                const int j = j0 + k;
+                if (j < y1) {
+                    const double2* row = at(j);
+                    up[k] = __ldcs(at(j == a.ny - 1 ? 0 : j + 1) + i);
+                    l[k] = row[il];
+                    r[k] = row[ir];
+                    v[k] = __ldcs(a.V + static_cast<size_t>(j) * a.nx + i);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kObsRows; ++k) {
+                if (j0 + k >= y1) break;
+                const double kx = fma(a.diag, u.x, -(a.cx * (l[k].x + r[k].x) + a.cy * (dn.x + up[k].x)));
+                const double ky = fma(a.diag, u.y, -(a.cx * (l[k].y + r[k].y) + a.cy * (dn.y + up[k].y)));
+                two_sum_add(acc[0], car[0], fma(u.x, kx, u.y * ky));  // Re conj(u) Ku
+                acc[1] += fma(u.x, ky, -u.y * kx);                    // Im conj(u) Ku (health check)
+                const double n2 = fma(u.x, u.x, u.y * u.y);
+                two_sum_add(acc[2], car[2], n2);
+                two_sum_add(acc[3], car[3], n2 * n2);
+                two_sum_add(acc[4], car[4], v[k] * n2);
+                dn = u;
+                u = up[k];
+            }
         }
     }
     block_csum_store<kObsThreads, kObsFields>(acc, car, a.partial + blockIdx.x * kObsFields);
