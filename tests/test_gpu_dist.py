@@ -349,3 +349,40 @@ def test_native_nccl_stepper_matches_single_domain(name, force_p2p, adaptive):
     assert np.array_equal(u_d, u), np.abs(u_d - u).max()
     H = obs[:, 3]
     assert np.abs(obs_d[:, 3] - H).max() <= 1e-14 * abs(H[0])
+
+
+def test_native_nccl_stepper_halving_and_divergence():
+    """The native stepper's failure paths: with max_iters = 3 some cfg2 steps need more
+    sweeps, fail on the device (one host read) and are halved -- the same trajectory, sweep
+    and halving counts as the Python-driven decomposed loop (DistributedSession, which halves
+    the same way; the single-domain library would first try Newton-Krylov); a NaN in the state
+    is reported as non-convergence."""
+    cfg = configs.CONFIGS["cfg2"]
+    V, psi = configs.make_inputs(cfg)
+    dec = D.Decomposition(cfg.nx, cfg.ny, 1, 1, 0)
+
+    def backend():
+        be = D.CudaBackend(dec, V, nls2d.Mb4Scheme(), cfg.gamma, 1.0, 1.0, cfg.epsilon, 3, 1, 0,
+                           max_step_halvings=4)
+        be.set_state(psi)
+        return be
+
+    be = backend()
+    ns = D.NativeSession(dec, be, D.nccl_unique_id(), cfg.gamma, 1.0, 1.0, force_p2p=True)
+    got = [ns.step(cfg.dt) for _ in range(3)]
+    u_d = be.get_state()
+    bad = psi.copy()
+    bad[5] = np.nan
+    be.set_state(bad)
+    with pytest.raises(D.NonConvergence):
+        ns.step(cfg.dt)
+    ns.close()
+    be.close()
+    be = backend()
+    ps = D.DistributedSession(dec, be, LoopbackComm(Hub(1), 0), cfg.gamma, 1.0, 1.0, cfg.epsilon, max_iters=3,
+                              max_step_halvings=4)
+    ref = [ps.step(cfg.dt) for _ in range(3)]
+    u = be.get_state()
+    be.close()
+    assert got == ref and max(hv for _, hv in got) >= 1
+    assert np.array_equal(u_d, u)
