@@ -329,6 +329,14 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         c.hls2[k] = cc * c.hlam2[k];
     }
     for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            long double a = 0.0L;
+            for (int k = 0; k < 3; ++k)
+                a += static_cast<long double>(s.T[i][k]) * s.lam[k] * static_cast<long double>(s.Tinv[k][j]);
+            c.hA[i][j] = static_cast<double>(h * a);
+            c.hAs[i][j] = static_cast<double>(cc * (h * a));
+        }
+    for (int i = 0; i < 3; ++i)
         for (int n = 0; n <= mb4cu::kMaxNeumannFirst; ++n) {
             double acc = 0.0;
             for (int k = 0; k < 3; ++k) acc += s.T[i][k] * c.first_s[k] * pc[k][n];

@@ -49,6 +49,10 @@ struct SweepConsts {
     // interpolant 1 + s_k (b x + b^2 x^2) on i[-rho, rho] (first_poly 2); c * that if ISO
     double hlam2[3];
     double hls2[3];
+    // depth-1 later sweeps in stage space: r = Phi + hA (J Phi) with hA = T diag(h lam) T^-1
+    // (the stage coupling h A of the collocation system; hAs = c * hA if ISO)
+    double hA[3][3];
+    double hAs[3][3];
     int def;            // scheme tables equal the generated default ones (defscheme.inc)
     // First sweep at Neumann depth MF from U = (u0,u0,u0): every phibar_k is a
     // multiple of f(u0), so the recursion needs only g_n = J^n f (n <= MF) once,

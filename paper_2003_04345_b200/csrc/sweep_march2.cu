@@ -84,6 +84,12 @@
 #ifndef MB4_LATER_PQR
 #define MB4_LATER_PQR 1
 #endif
+// later sweeps at depth 1 in stage space: r = Phi + hA (J Phi), hA = T diag(h lam) T^-1
+// (no T^-1 / T transforms: 24 fewer FP64 operations per site; same operator, the
+// correction rounds differently at the 1e-16 level)
+#ifndef MB4_LATER_DIRECT
+#define MB4_LATER_DIRECT 1
+#endif
 // first sweep: J applied through per-site coefficients (P, Q, R) formed once per site
 #ifndef MB4_FIRST_PQR
 #define MB4_FIRST_PQR 1
@@ -204,6 +210,7 @@ struct Coef {
     __device__ __forceinline__ double g() const { return ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double hl(int k) const { return ISO ? c.hls[k] : c.hlam[k]; }
     __device__ __forceinline__ double hl2(int k) const { return ISO ? c.hls2[k] : c.hlam2[k]; }
+    __device__ __forceinline__ double hA(int q, int k) const { return ISO ? c.hAs[q][k] : c.hA[q][k]; }
     __device__ __forceinline__ double fs(int k) const { return ISO ? c.first_ss[k] : c.first_s[k]; }
     __device__ __forceinline__ double fc(int k) const { return ISO ? c.first_cs[k] : c.first_c[k]; }
     // stencil diagonal incl. potential
@@ -269,6 +276,8 @@ struct Coef {
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF = false>
 struct March3 {
     using G = Geom3<M, NT>;
+    // depth-1 later sweeps publish Phi itself (not T^-1 Phi) and correct by Phi + hA J Phi
+    static constexpr bool DIRECT = M == 1 && !FIRST && MB4_LATER_DIRECT && MB4_LATER_PQR;
     // element offset of local site (x, y) (both may lie in the halo)
     __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
         if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
@@ -558,6 +567,9 @@ struct March3 {
                             track(rmax, phi[q]);
                         }
                     }
+                } else if (DIRECT) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) pb[k] = phi[k];
                 } else {
                     cf.to_eigen(phi, pb);
                 }
@@ -566,6 +578,37 @@ struct March3 {
         if (M == 0) return;
 
         // ---- level 1 at row i - 1 ----------------------------------------------
+        if constexpr (DIRECT) {
+            // r = Phi + hA J Phi at row i - 1 (J of each stage's Phi through the site's
+            // (P, Q, R); Phi of rows i - 2 / i - 1 own column and the neighbours from the
+            // published rows)
+            const auto K1 = cf.pqr(cf.dv(vw[S_DN]), zw[S_DN][0]);
+            double2 jk[3], tc[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double2* prow = pub_row(0, ppar, k);  // Phi row i - 1
+                tc[k] = prow[cc];
+                const double2 td = pub_row(0, par, k)[cc];  // row i - 2
+                jk[k] = cf.jt_pqr(K1, tc[k], cf.nsum(prow[cc - 1], prow[cc + 1], td, pb[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) pub_row(0, par, k)[cc] = pb[k];
+            if (out_ok) {
+                const size_t gi = at(a, xout, s.Y0 + yrel);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    double rx = fma(cf.hA(q, 0), jk[0].x, tc[q].x), ry = fma(cf.hA(q, 0), jk[0].y, tc[q].y);
+                    rx = fma(cf.hA(q, 1), jk[1].x, rx);
+                    ry = fma(cf.hA(q, 1), jk[1].y, ry);
+                    rx = fma(cf.hA(q, 2), jk[2].x, rx);
+                    ry = fma(cf.hA(q, 2), jk[2].y, ry);
+                    const double2 uo = zw[S_DN][q + 1];
+                    if ((s.smask >> q) & 1) uout[q][gi] = make_double2(uo.x - rx, uo.y - ry);
+                    track(rmax, make_double2(rx, ry));
+                }
+            }
+            return;
+        }
         double2 b1[3];
         {
             const double2 u0m = zw[S_DN][0];          // u0 of row i - 1 (z row j - 2)
@@ -1634,7 +1677,11 @@ int grid3(int device) {
 }  // namespace
 
 // (first-sweep depth, later-sweep depth) pairs with a compiled kernel
+#ifdef MB4_QUICK_PAIRS  // register / SASS checks of the production pair only (not a usable library)
+#define MB4_MARCH2_PAIRS(X) X(6, 1)
+#else
 #define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(4, 2) X(5, 2) X(6, 2) X(6, 0)
+#endif
 
 int march2_launches(int mf, int ghost, int sweep0, int max_iters) {
     return MB4_SPLIT && mf >= 4 && ghost == 0 && sweep0 == 0 && max_iters > 1 ? 2 : 1;
