@@ -305,6 +305,16 @@ SweepConsts make_consts(const mb4cu_ctx* ctx, double h) {
         for (int j = 0; j < 4; ++j) c.Es[i][j] = cc * s.E[i][j];
     c.gs = ctx->gamma / cc;
     c.hs = cc * h;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 4; ++j) {
+            c.hE[i][j] = h * s.E[i][j];
+            c.hEs[i][j] = (cc * h) * s.E[i][j];
+        }
+        for (int q = 0; q < 6; ++q) {
+            c.hgW[i][q] = (h * ctx->gamma) * s.WA[i][q];
+            c.hgW8[i][q] = 0.125 * c.hgW[i][q];
+        }
+    }
     c.def = is_default_scheme(s);
     for (int k = 0; k < 3; ++k) {
         c.hls[k] = cc * c.hlam[k];

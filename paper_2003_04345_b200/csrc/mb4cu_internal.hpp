@@ -53,6 +53,12 @@ struct SweepConsts {
     // (the stage coupling h A of the collocation system; hAs = c * hA if ISO)
     double hA[3][3];
     double hAs[3][3];
+    // later sweeps, Phi accumulated in one chain (MB4_PHI_FUSED): h E (hEs = c h E if ISO),
+    // h gamma WA and the same / 8 (default-scheme node values at twice their scale)
+    double hE[3][4];
+    double hEs[3][4];
+    double hgW[3][6];
+    double hgW8[3][6];
     int def;            // scheme tables equal the generated default ones (defscheme.inc)
     // First sweep at Neumann depth MF from U = (u0,u0,u0): every phibar_k is a
     // multiple of f(u0), so the recursion needs only g_n = J^n f (n <= MF) once,

@@ -115,6 +115,15 @@
 #ifndef MB4_CUBIC_EARLY
 #define MB4_CUBIC_EARLY 0
 #endif
+// later sweeps: Phi_k accumulated in ONE FMA chain per stage and component -- from
+// z_k - z_0 through the six cubic node terms (weights h gamma WA) and the four stencil
+// terms (weights h E) -- instead of separate cubic / stencil combinations joined by two
+// more FMAs; with the default scheme the node values at twice their scale, the even part
+// of the collocation polynomial from s12 + c_q (s03 - s12) (18 fewer FP64 operations per
+// site; the own-column d = 4 + V/c window saves one more).  1: depth-1 later sweeps.
+#ifndef MB4_PHI_FUSED
+#define MB4_PHI_FUSED 1
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
@@ -188,6 +197,11 @@ struct Coef {
     __device__ __forceinline__ double E0(int i, int j) const {
         return DEF ? dsv::E[i][j] : (ISO ? c.Es[i][j] : c.E[i][j]);
     }
+    // fused Phi chains: h E (isotropic: c h E) and h gamma WA (/ 8 for node values at twice
+    // their scale)
+    __device__ __forceinline__ double hE(int k, int b) const { return ISO ? c.hEs[k][b] : c.hE[k][b]; }
+    __device__ __forceinline__ double hgW(int k, int q) const { return c.hgW[k][q]; }
+    __device__ __forceinline__ double hgW8(int k, int q) const { return c.hgW8[k][q]; }
     __device__ __forceinline__ double g0() const { return DEF && ISO ? c.gs : c.gamma; }
     __device__ __forceinline__ double h0() const { return DEF && ISO ? c.hs : c.h; }
     // phibar = T^-1 phi, r = T rbar
@@ -278,6 +292,8 @@ struct March3 {
     using G = Geom3<M, NT>;
     // depth-1 later sweeps publish Phi itself (not T^-1 Phi) and correct by Phi + hA J Phi
     static constexpr bool DIRECT = M == 1 && !FIRST && MB4_LATER_DIRECT && MB4_LATER_PQR;
+    // Phi accumulated in one chain per stage and component (MB4_PHI_FUSED)
+    static constexpr bool FUSED = !FIRST && (MB4_PHI_FUSED == 2 || (MB4_PHI_FUSED == 1 && DIRECT));
     // element offset of local site (x, y) (both may lie in the halo)
     __device__ __forceinline__ static size_t at(const StepArgs& a, int x, int y) {
         if (GHOST) return static_cast<size_t>(y + a.ghost) * a.pitch + (x + a.ghost);
@@ -436,6 +452,56 @@ struct March3 {
         }
     }
 
+    // Fused form: adds the cubic term of Phi_k to phi[k] (which holds z_k+1 - z_0):
+    //   phi[k].x += sum_q (h gamma WA[k][q]) Im(|U_q|^2 U_q),  phi[k].y -= ... Re(...)
+    __device__ __forceinline__ static void cubic_into(const Coef<ISO, DEF>& cf, const double2 z[4], double2 phi[3]) {
+        if constexpr (DEF && MB4_SYM_PAIRS) {
+            // default scheme (nodes 0, 1/3, 2/3, 1): with s = tau - 1/2 the even part of 2 U
+            // is s12 + ce(s) (s03 - s12), ce = (36 s^2 - 1) / 8 = 2 LS[q][0]; the odd part
+            // 2 (LD[q][0] d03 + LD[q][1] d12).  Node values at twice their scale: weights / 8.
+            const double2 s03 = make_double2(z[0].x + z[3].x, z[0].y + z[3].y);
+            const double2 d03 = make_double2(z[0].x - z[3].x, z[0].y - z[3].y);
+            const double2 s12 = make_double2(z[1].x + z[2].x, z[1].y + z[2].y);
+            const double2 d12 = make_double2(z[1].x - z[2].x, z[1].y - z[2].y);
+            const double2 ds = make_double2(s03.x - s12.x, s03.y - s12.y);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double ce = 2.0 * dsv::LS[q][0], o0 = 2.0 * dsv::LD[q][0], o1 = 2.0 * dsv::LD[q][1];
+                const double ex = fma(ce, ds.x, s12.x), ey = fma(ce, ds.y, s12.y);
+                const double ox = fma(o1, d12.x, o0 * d03.x), oy = fma(o1, d12.y, o0 * d03.y);
+#pragma unroll
+                for (int side = 0; side < 2; ++side) {
+                    const int qq = side ? 5 - q : q;
+                    const double ur = side ? ex - ox : ex + ox, ui = side ? ey - oy : ey + oy;
+                    const double n2 = fma(ur, ur, ui * ui);
+                    const double gr = n2 * ur, gi = n2 * ui;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        phi[k].x = fma(cf.hgW8(k, qq), gi, phi[k].x);
+                        phi[k].y = fma(-cf.hgW8(k, qq), gr, phi[k].y);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                double ur = cf.Lq(q, 0) * z[0].x, ui = cf.Lq(q, 0) * z[0].y;
+#pragma unroll
+                for (int b = 1; b < 4; ++b) {
+                    ur = fma(cf.Lq(q, b), z[b].x, ur);
+                    ui = fma(cf.Lq(q, b), z[b].y, ui);
+                }
+                const double n2 = fma(ur, ur, ui * ui);
+                const double gr = n2 * ur, gi = n2 * ui;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    phi[k].x = fma(cf.hgW(k, q), gi, phi[k].x);
+                    phi[k].y = fma(-cf.hgW(k, q), gr, phi[k].y);
+                }
+            }
+        }
+    }
+
     // Iteration j (level-0 row i = j - 2).  PH = j mod 3 (static); h3 = 3 * ((j / 3) & 1).
     template <int PH>
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO, DEF>& cf,
@@ -471,7 +537,8 @@ struct March3 {
         if (j < s.nzrows) mbar_wait(&bars[slot_new], (j / G::S) & 1);
 #endif
         zw[S_NEW][0] = zu0[slot_new * G::ZWP + cc];
-        vw[S_NEW] = zv[slot_new * G::ZW + cc];
+        // (fused later sweeps keep the stencil diagonal d = dv(V) in the window, not V)
+        vw[S_NEW] = FUSED ? cf.dv(zv[slot_new * G::ZW + cc]) : zv[slot_new * G::ZW + cc];
         if (!FIRST) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) zw[S_NEW][q + 1] = zU[(slot_new * 3 + q) * G::ZWP + cc];
@@ -499,7 +566,7 @@ struct March3 {
 
         // ---- level 0 at row i ---------------------------------------------------
         const double v = vw[S_CEN];
-        const double d0 = cf.dv(v);
+        const double d0 = FUSED ? v : cf.dv(v);
         const double2 u0c = zw[S_CEN][0];
         double2 pb[3];
         {
@@ -542,8 +609,21 @@ struct March3 {
                     z[q] = zw[S_CEN][q];
                     w[q] = cf.kv(d0, z[q], row[cc - 1], row[cc + 1], zw[S_DN][q], zw[S_NEW][q]);
                 }
-                if (!MB4_CUBIC_EARLY) cubic_site(cf, z, cub);
                 double2 phi[3];
+                if constexpr (FUSED) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) phi[k] = make_double2(z[k + 1].x - z[0].x, z[k + 1].y - z[0].y);
+                    cubic_into(cf, z, phi);  // (own column only: may be scheduled before the neighbour loads)
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            phi[k].x = fma(-cf.hE(k, b), w[b].y, phi[k].x);
+                            phi[k].y = fma(cf.hE(k, b), w[b].x, phi[k].y);
+                        }
+                    }
+                } else {
+                if (!MB4_CUBIC_EARLY) cubic_site(cf, z, cub);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
                     double kr = cf.E0(k, 0) * w[0].x, ki = cf.E0(k, 0) * w[0].y;
@@ -556,6 +636,7 @@ struct March3 {
                     const double ri = fma(cf.g0(), cub[k].x, -kr);
                     phi[k].x = fma(-cf.h0(), rr, z[k + 1].x - z[0].x);
                     phi[k].y = fma(-cf.h0(), ri, z[k + 1].y - z[0].y);
+                }
                 }
                 if (M == 0) {
                     if (out_ok) {
@@ -582,7 +663,7 @@ struct March3 {
             // r = Phi + hA J Phi at row i - 1 (J of each stage's Phi through the site's
             // (P, Q, R); Phi of rows i - 2 / i - 1 own column and the neighbours from the
             // published rows)
-            const auto K1 = cf.pqr(cf.dv(vw[S_DN]), zw[S_DN][0]);
+            const auto K1 = cf.pqr(FUSED ? vw[S_DN] : cf.dv(vw[S_DN]), zw[S_DN][0]);
             double2 jk[3], tc[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -612,7 +693,7 @@ struct March3 {
         double2 b1[3];
         {
             const double2 u0m = zw[S_DN][0];          // u0 of row i - 1 (z row j - 2)
-            const double dm = cf.dv(vw[S_DN]);
+            const double dm = FUSED ? vw[S_DN] : cf.dv(vw[S_DN]);
 #if MB4_LATER_PQR
             const auto K1 = cf.pqr(dm, u0m);  // J at the site, formed once for the 3 stages
 #endif
@@ -1678,7 +1759,7 @@ int grid3(int device) {
 
 // (first-sweep depth, later-sweep depth) pairs with a compiled kernel
 #ifdef MB4_QUICK_PAIRS  // register / SASS checks of the production pair only (not a usable library)
-#define MB4_MARCH2_PAIRS(X) X(6, 1)
+#define MB4_MARCH2_PAIRS(X) X(6, 1) X(6, 2)
 #else
 #define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(4, 2) X(5, 2) X(6, 2) X(6, 0)
 #endif

@@ -6,5 +6,5 @@ for lib in "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read())
 r=d['roofline']
-print('$lib', d['config']['workload'][:5], 'm=%s'%d['config']['neumann_terms'], '%.3e'%d['value'], d['sweeps_per_step'], 'frac=%.3f'%r['frac'], 'ms/step=%.3f'%r.get('kernel_ms_per_step', r['kernel_ms_per_launch']), r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'))"
+print('$lib', d['config']['workload'][:5], 'm=%s'%d['config']['neumann_terms'], '%.3e'%d['value'], d['sweeps_per_step'], 'frac=%.3f'%r['frac'], 'ms/step=%.3f'%r.get('kernel_ms_per_step', r['kernel_ms_per_launch']), r.get('sweep_ms_by_index'), (d['clocks'] or {}).get('sm_mhz'), 'drift=%.17g'%d['energy_drift'])"
 done
