@@ -64,6 +64,7 @@ struct mb4cu_ctx {
     cudaEvent_t pev0 = nullptr, pev1 = nullptr;
     // persistent-kernel path
     unsigned long long* d_rmax_arr = nullptr;  // [max_iters + 1]: residual bits per sweep, max |u0|^2
+    unsigned* d_work = nullptr;                // [kWorkCounters]: chunk counters of the later sweeps
     double* d_obs_march = nullptr;             // [grid][kObsFields]
     mb4cu::StepStatus* d_status = nullptr;
     mb4cu::StepStatus* h_status = nullptr;     // pinned
@@ -384,7 +385,7 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
                                                 ctx->max_iters, ctx->eps, 1, c, ctx->device,
-                                                ctx->stream, 0, 0, spec));
+                                                ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, nullptr, 0, ctx->d_work));
     } else {
         MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
@@ -1327,6 +1328,8 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
         if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * (ctx->max_iters + 1))) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
+        if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
+            return bail(e, "cudaMalloc(work)");
         if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * grid)) != cudaSuccess)
             return bail(e, "cudaMalloc(obs_march)");
         ctx->obs_grid = grid;
@@ -1379,6 +1382,7 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
     cudaFree(ctx->d_obs5);
     cudaFreeHost(ctx->h_obs5);
     cudaFree(ctx->d_rmax_arr);
+    cudaFree(ctx->d_work);
     cudaFree(ctx->d_obs_march);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
@@ -1717,7 +1721,8 @@ int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, 
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, u0p, ctx->V, Up,
                                                 ctx->d_brmax + static_cast<size_t>(k) * rstride,
                                                 ctx->d_obs_march, ctx->d_bstatus + k, ctx->max_iters, ctx->eps, 1, c,
-                                                ctx->device, ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, &ctl));
+                                                ctx->device, ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, &ctl, 0,
+                                                ctx->d_work));
         MB4_CUDA(ctx, cudaEventRecord(ctx->bev[k + 1], ctx->stream));
         // the predicted commit: u0 <-> U[set][2]
         double2* nu0 = Up[set][2];

@@ -175,7 +175,12 @@ struct StepArgs {
     int switch_sweeps;          // 0: none
     double amax2_lo, amax2_hi;  // the batch's step constants hold while max|u0|^2 stays inside
     const int* skip;            // != nullptr and *skip != 0: the launch does nothing (read only)
+    // Dynamic work split of the later sweeps (split launches of a whole domain): one chunk
+    // counter per sweep pass, [kWorkCounters], zeroed by the first-sweep launch of the step.
+    // nullptr: the static even split.
+    unsigned* work;
 };
+constexpr int kWorkCounters = 128;
 
 // batch control of launch_step_march2 (see StepArgs::batch_abort)
 struct BatchCtl {
@@ -249,7 +254,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
                                const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0,
-                               const BatchCtl* batch = nullptr, int pitch = 0);
+                               const BatchCtl* batch = nullptr, int pitch = 0, unsigned* work = nullptr);
 int march2_grid_size(int mf, int m, int device);
 // output columns per band of the sub-domain sweep kernels (0: no band structure)
 int march2_band_width(int mf, int m, bool first);

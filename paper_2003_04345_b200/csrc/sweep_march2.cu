@@ -124,12 +124,34 @@
 #ifndef MB4_PHI_FUSED
 #define MB4_PHI_FUSED 1
 #endif
+// Later sweeps of a split step: the band-rows are handed out in chunks from a device
+// counter (guided: the first round of chunks covers half of the rows, every further round
+// half of the rest, down to MB4_DYN_SMIN rows) instead of one fixed share per CTA.  The
+// CTAs that share an SM do not advance at the same rate (the warp schedulers favour one of
+// them: with fixed shares the three CTAs of an SM finished at 0.87 / 1.13 / 1.39 ms at
+// cfg5 and the SM ran its last third with one warp per scheduler); with chunks every CTA
+// works until the rows run out.  Which CTA computes a row does not change its arithmetic.
+#ifndef MB4_DYN_SPLIT
+#define MB4_DYN_SPLIT 1
+#endif
+#ifndef MB4_DYN_SMIN
+#define MB4_DYN_SMIN 32
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
 #endif
 
 namespace cg = cooperative_groups;
+
+#ifdef MB4_CTA_TIMES
+// profiling builds: per-CTA (start, end of its last sweep, SM id) of the latest step launch
+// of each phase (tools/cta_times.py)
+__device__ unsigned long long g_cta_times[4][2048][3];
+extern "C" int mb4cu_debug_cta_times(unsigned long long* out) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, g_cta_times, sizeof(g_cta_times)));
+}
+#endif
 
 namespace mb4cu {
 namespace {
@@ -1427,10 +1449,51 @@ __device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) 
     }
 }
 
+// The same march over chunks of band-rows taken from the counter *ctr (whole domain only).
+// Chunk c of round c / G (G = gridDim.x) has q >> (round + 1) rows, q = total / G, at least
+// MB4_DYN_SMIN: a fixed map chunk -> rows, so only the CTA that computes a row varies.
+template <int TX, class Run>
+__device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ctr, const Run& run) {
+    __shared__ unsigned s_chunk[2];
+    const int nbands = (a.nx + TX - 1) / TX;
+    const long long total = static_cast<long long>(nbands) * a.ny;
+    const long long G = gridDim.x;
+    const long long q = total / G;
+    int flip = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_chunk[flip] = atomicAdd(ctr, 1u);
+        __syncthreads();
+        long long cc = s_chunk[flip];
+        flip ^= 1;
+        long long start = 0, sz = q >> 1;
+        for (;;) {
+            if (sz <= MB4_DYN_SMIN) {
+                sz = MB4_DYN_SMIN;
+                break;
+            }
+            if (cc < G) break;
+            start += G * sz;
+            cc -= G;
+            sz >>= 1;
+        }
+        const long long p0 = start + cc * sz;
+        if (p0 >= total) break;
+        const long long p1 = p0 + sz < total ? p0 + sz : total;
+        for (long long pos = p0; pos < p1;) {
+            const int band = static_cast<int>(pos / a.ny);
+            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
+            const long long band_end = static_cast<long long>(band + 1) * a.ny;
+            const long long seg_end = band_end < p1 ? band_end : p1;
+            run(band * TX, a.nx, row, static_cast<int>(seg_end - pos));
+            pos = seg_end;
+        }
+    }
+}
+
 template <int M, int NT, bool FIRST, bool ISO, bool GHOST, bool DEF>
 __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned char* smem,
                            const double2* const uin[3], double2* const uout[3],
-                           unsigned& rmax, double* acc, int smask = 7) {
+                           unsigned& rmax, double* acc, int smask = 7, unsigned* work = nullptr) {
     if constexpr (FIRST && M >= 3 && M <= 7 && MB4_FIRST_V2) {
         using MFirst = MarchFirst2<M, NT, ISO, GHOST>;
         MFirst mf(smem);
@@ -1446,9 +1509,14 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
     } else {
         March3<M, NT, FIRST, ISO, GHOST, DEF> m(smem);
         // band-rows of this sweep's band width (TX depends on M)
-        for_segments<Geom3<M, NT>::TX>(a, [&](int X0, int xlim, int Y0, int R) {
-            m.run(a, c, uin, uout, X0, xlim, Y0, R, rmax, acc, smask);
-        });
+        auto seg = [&](int X0, int xlim, int Y0, int R) { m.run(a, c, uin, uout, X0, xlim, Y0, R, rmax, acc, smask); };
+        // (depth-2 sweeps run 2 CTAs per SM, which finish together: measured 2.5 % slower
+        // with chunks at cfg4, so they keep the fixed shares)
+        if (MB4_DYN_SPLIT && !FIRST && !GHOST && M == 1 && work) {
+            for_segments_dyn<Geom3<M, NT>::TX>(a, work, seg);
+        } else {
+            for_segments<Geom3<M, NT>::TX>(a, seg);
+        }
     }
 }
 
@@ -1496,6 +1564,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     if (a.batch_abort && *reinterpret_cast<volatile const int*>(a.batch_abort)) return;
     if (a.skip && *reinterpret_cast<volatile const int*>(a.skip)) return;
     cg::grid_group grid = cg::this_grid();
+#ifdef MB4_CTA_TIMES
+    const unsigned long long cta_t0 = global_timer_ns();
+#endif
     double acc[kAccSize] = {};  // energy sums, max |u0|^2, carries (monitor_add)
 #if MB4_CONSTS_IN_SMEM
     // M = 2: scheme / step constants as a shared-memory broadcast table (LDS)
@@ -1522,6 +1593,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         reinterpret_cast<unsigned long long*>(smem)[q] = MB4_POISON_SMEM;
     __syncthreads();
 #endif
+    // the later-sweep launch of this step takes its chunks from these counters
+    if (PH == 1 && a.work && blockIdx.x == 0)
+        for (int q = threadIdx.x; q < kWorkCounters; q += NT) a.work[q] = 0u;
+    int pass = 0;  // sweep passes of this launch (one chunk counter each)
     int sweeps = 0, set = 0, converged = 0, redone = 0;
     bool redo = false;  // this pass repeats the missed speculative sweep with all stages
     double rlast = 0.0;
@@ -1570,9 +1645,21 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             // (same inputs, same arithmetic, so the result is independent of the guess).
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
+            unsigned* const work = PH == 2 && a.work && pass < kWorkCounters ? a.work + pass : nullptr;
+            ++pass;
             sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc,
-                                                       sg == a.spec_sweep && !redo ? 4 : 7);
+                                                       sg == a.spec_sweep && !redo ? 4 : 7, work);
         }
+#ifdef MB4_CTA_TIMES
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x < 2048) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_cta_times[PH][blockIdx.x][0] = cta_t0;
+            g_cta_times[PH][blockIdx.x][1] = global_timer_ns();
+            g_cta_times[PH][blockIdx.x][2] = smid;
+        }
+#endif
         if constexpr (PH == 1) {  // the later-sweep launch takes it from here
             block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[0]);
             return;
@@ -1693,7 +1780,11 @@ cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStrea
 }
 
 template <int MF, int M>
-cudaError_t dispatch3(const StepArgs& a, const SweepConsts& c, int device, cudaStream_t s) {
+cudaError_t dispatch3(const StepArgs& a0, const SweepConsts& c, int device, cudaStream_t s) {
+    StepArgs a = a0;
+    // chunk counters: only the split pair of a whole domain (its first-sweep launch zeroes them)
+    const bool split = MB4_SPLIT && MF >= 4 && a.ghost == 0 && a.sweep0 == 0 && a.max_iters > 1;
+    if (!split || a.nrect > 0) a.work = nullptr;
     if constexpr (MB4_SPLIT && MF >= 4) {
         if (a.ghost == 0 && a.sweep0 == 0 && a.max_iters > 1) {
             if (c.iso && c.def) return launch_split<MF, M, MB4_NT, true, true>(a, c, device, s);
@@ -1780,8 +1871,9 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
-                               int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch) {
+                               int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch, unsigned* work) {
     StepArgs a{};
+    a.work = work;
     if (batch) {
         a.batch_abort = batch->abort;
         a.expect_sweeps = batch->expect_sweeps;
