@@ -385,7 +385,8 @@ int substep_march(mb4cu_ctx* ctx, double h, int* sweeps, double* last_res) {
         MB4_CUDA(ctx, mb4cu::launch_step_march2(ctx->mf, ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
                                                 ctx->max_iters, ctx->eps, 1, c, ctx->device,
-                                                ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, nullptr, 0, ctx->d_work));
+                                                ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, nullptr, 0, ctx->d_work,
+                                                ctx->obs_grid * mb4cu::kObsSlotsPerCta));
     } else {
         MB4_CUDA(ctx, mb4cu::launch_step_march(ctx->m, ctx->nx, ctx->ny, ctx->u0, ctx->V, ctx->U,
                                                ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status,
@@ -1330,7 +1331,10 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
             return bail(e, "cudaMalloc(rmax_arr)");
         if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
             return bail(e, "cudaMalloc(work)");
-        if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * grid)) != cudaSuccess)
+        if ((e = cudaMemset(ctx->d_work, 0, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
+            return bail(e, "cudaMemset(work)");
+        if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * mb4cu::kObsSlotsPerCta * grid)) !=
+            cudaSuccess)
             return bail(e, "cudaMalloc(obs_march)");
         ctx->obs_grid = grid;
         if ((e = cudaMalloc(&ctx->d_status, sizeof(mb4cu::StepStatus))) != cudaSuccess)
@@ -1424,7 +1428,7 @@ int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m) {
     if (grid > ctx->obs_grid) {
         MB4_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         double* fresh = nullptr;
-        MB4_CUDA(ctx, cudaMalloc(&fresh, sizeof(double) * mb4cu::kObsFields * grid));
+        MB4_CUDA(ctx, cudaMalloc(&fresh, sizeof(double) * mb4cu::kObsFields * mb4cu::kObsSlotsPerCta * grid));
         cudaFree(ctx->d_obs_march);
         ctx->d_obs_march = fresh;
         ctx->obs_grid = grid;
@@ -1722,7 +1726,7 @@ int run_batch(mb4cu_ctx* ctx, double h, int nmax, double* obs_rows, int* iters, 
                                                 ctx->d_brmax + static_cast<size_t>(k) * rstride,
                                                 ctx->d_obs_march, ctx->d_bstatus + k, ctx->max_iters, ctx->eps, 1, c,
                                                 ctx->device, ctx->stream, 0, 0, spec, 0, nullptr, 0, 0, &ctl, 0,
-                                                ctx->d_work));
+                                                ctx->d_work, ctx->obs_grid * mb4cu::kObsSlotsPerCta));
         MB4_CUDA(ctx, cudaEventRecord(ctx->bev[k + 1], ctx->stream));
         // the predicted commit: u0 <-> U[set][2]
         double2* nu0 = Up[set][2];

@@ -179,8 +179,15 @@ struct StepArgs {
     // counter per sweep pass, [kWorkCounters], zeroed by the first-sweep launch of the step.
     // nullptr: the static even split.
     unsigned* work;
+    // work != nullptr: the first-sweep launch takes chunks as well (counter 0; the later
+    // sweeps use counters 1..), and writes one set of energy partial sums per chunk
+    int dyn_first;
+    int obs_cap;                // partial-sum slots obs_partial holds (0: one per CTA of the largest grid)
 };
 constexpr int kWorkCounters = 128;
+// energy partial-sum slots allocated per CTA of the largest co-resident grid (a chunked first
+// sweep writes ~log2(rows per CTA / MB4_DYN_SMIN) + 3 partials per CTA)
+constexpr int kObsSlotsPerCta = 24;
 
 // batch control of launch_step_march2 (see StepArgs::batch_abort)
 struct BatchCtl {
@@ -254,7 +261,8 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
                                const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0,
-                               const BatchCtl* batch = nullptr, int pitch = 0, unsigned* work = nullptr);
+                               const BatchCtl* batch = nullptr, int pitch = 0, unsigned* work = nullptr,
+                               int obs_cap = 0);
 int march2_grid_size(int mf, int m, int device);
 // output columns per band of the sub-domain sweep kernels (0: no band structure)
 int march2_band_width(int mf, int m, bool first);

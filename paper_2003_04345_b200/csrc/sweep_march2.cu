@@ -137,6 +137,13 @@
 #ifndef MB4_DYN_SMIN
 #define MB4_DYN_SMIN 32
 #endif
+// the first sweep of a split step in chunks as well (its two CTAs per SM finish 6 % apart
+// with fixed shares); every chunk stores its own energy partial sums, so the energy record
+// does not depend on which CTA took which chunk.  Measured slower (cfg5 1.40 -> 1.49 ms):
+// every chunk restarts the 2 MF + 2 = 14 warm-up rows of the depth-6 chain.  Off.
+#ifndef MB4_DYN_FIRST
+#define MB4_DYN_FIRST 0
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
@@ -1449,36 +1456,53 @@ __device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) 
     }
 }
 
+// Chunk c of the guided split of `total` band-rows over a grid of G CTAs -> [p0, p1); false
+// past the last chunk.  Round c / G has chunks of (total / G) >> (round + 1) rows, at least smin.
+__host__ __device__ inline bool dyn_chunk(long long c, long long total, long long G, long long smin, long long& p0,
+                                          long long& p1) {
+    long long start = 0, sz = (total / G) >> 1;
+    for (;;) {
+        if (sz <= smin) {
+            sz = smin;
+            break;
+        }
+        if (c < G) break;
+        start += G * sz;
+        c -= G;
+        sz >>= 1;
+    }
+    p0 = start + c * sz;
+    if (p0 >= total) return false;
+    p1 = p0 + sz < total ? p0 + sz : total;
+    return true;
+}
+inline long long dyn_chunk_count(long long total, long long G, long long smin) {
+    long long n = 0, start = 0, sz = (total / G) >> 1;
+    while (sz > smin && start + G * sz <= total) {  // full rounds
+        start += G * sz;
+        n += G;
+        sz >>= 1;
+    }
+    if (sz < smin) sz = smin;
+    return n + (total - start + sz - 1) / sz;
+}
+
 // The same march over chunks of band-rows taken from the counter *ctr (whole domain only).
 // Chunk c of round c / G (G = gridDim.x) has q >> (round + 1) rows, q = total / G, at least
 // MB4_DYN_SMIN: a fixed map chunk -> rows, so only the CTA that computes a row varies.
-template <int TX, class Run>
-__device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ctr, const Run& run) {
+template <int TX, class Run, class Done>
+__device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ctr, const Run& run, const Done& done) {
     __shared__ unsigned s_chunk[2];
     const int nbands = (a.nx + TX - 1) / TX;
     const long long total = static_cast<long long>(nbands) * a.ny;
-    const long long G = gridDim.x;
-    const long long q = total / G;
     int flip = 0;
     for (;;) {
         if (threadIdx.x == 0) s_chunk[flip] = atomicAdd(ctr, 1u);
         __syncthreads();
-        long long cc = s_chunk[flip];
+        const long long c = s_chunk[flip];
         flip ^= 1;
-        long long start = 0, sz = q >> 1;
-        for (;;) {
-            if (sz <= MB4_DYN_SMIN) {
-                sz = MB4_DYN_SMIN;
-                break;
-            }
-            if (cc < G) break;
-            start += G * sz;
-            cc -= G;
-            sz >>= 1;
-        }
-        const long long p0 = start + cc * sz;
-        if (p0 >= total) break;
-        const long long p1 = p0 + sz < total ? p0 + sz : total;
+        long long p0, p1;
+        if (!dyn_chunk(c, total, gridDim.x, MB4_DYN_SMIN, p0, p1)) break;
         for (long long pos = p0; pos < p1;) {
             const int band = static_cast<int>(pos / a.ny);
             const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
@@ -1487,6 +1511,7 @@ __device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ct
             run(band * TX, a.nx, row, static_cast<int>(seg_end - pos));
             pos = seg_end;
         }
+        done(c);
     }
 }
 
@@ -1497,9 +1522,19 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
     if constexpr (FIRST && M >= 3 && M <= 7 && MB4_FIRST_V2) {
         using MFirst = MarchFirst2<M, NT, ISO, GHOST>;
         MFirst mf(smem);
-        for_segments<MFirst::TX>(a, [&](int X0, int xlim, int Y0, int R) {
-            mf.run(a, c, uout, X0, xlim, Y0, R, rmax, acc);
-        });
+        auto seg = [&](int X0, int xlim, int Y0, int R) { mf.run(a, c, uout, X0, xlim, Y0, R, rmax, acc); };
+        if (MB4_DYN_SPLIT && MB4_DYN_FIRST && !GHOST && work) {
+            for_segments_dyn<MFirst::TX>(a, work, seg, [&](long long chunk) {
+                if (!a.want_obs) return;
+                // this chunk's energy sums (compensated warp and block trees)
+                monitor_flush(acc);
+                block_csum_store<NT, kObsFields>(acc + kAccTot, acc + kAccCarry, a.obs_partial + chunk * kObsFields);
+#pragma unroll
+                for (int f = 0; f < kObsFields; ++f) acc[kAccTot + f] = acc[kAccCarry + f] = 0.0;
+            });
+        } else {
+            for_segments<MFirst::TX>(a, seg);
+        }
     } else if constexpr (FIRST && M >= 1) {
         using MFirst = MarchFirst<M, NT, ISO, GHOST>;
         MFirst mf(smem);
@@ -1513,7 +1548,7 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
         // (depth-2 sweeps run 2 CTAs per SM, which finish together: measured 2.5 % slower
         // with chunks at cfg4, so they keep the fixed shares)
         if (MB4_DYN_SPLIT && !FIRST && !GHOST && M == 1 && work) {
-            for_segments_dyn<Geom3<M, NT>::TX>(a, work, seg);
+            for_segments_dyn<Geom3<M, NT>::TX>(a, work, seg, [](long long) {});
         } else {
             for_segments<Geom3<M, NT>::TX>(a, seg);
         }
@@ -1555,6 +1590,25 @@ struct KGeom {
                                           : (M == 2 ? 2 : MB4_MINB_M1);
 };
 
+// The energy record of the step's entry state: the first sweep's partial sums (one per CTA,
+// or per chunk of a chunked first sweep), each thread of block 0 a fixed strided subset, then
+// the compensated warp and block trees -- a fixed order.
+template <int NT>
+__device__ __forceinline__ void reduce_obs(const StepArgs& a) {
+    if (!a.want_obs || blockIdx.x != 0) return;
+    double v[kObsFields] = {}, cv[kObsFields] = {};
+    const int nb = a.obs_blocks > 0 ? a.obs_blocks : static_cast<int>(gridDim.x);
+    for (int b = threadIdx.x; b < nb; b += NT) {
+#pragma unroll
+        for (int f = 0; f < kObsFields; ++f) two_sum_add(v[f], cv[f], a.obs_partial[b * kObsFields + f]);
+    }
+    if (a.obs_accumulate && threadIdx.x == 0) {
+#pragma unroll
+        for (int f = 0; f < kObsFields; ++f) two_sum_add(v[f], cv[f], a.status->obs[f]);
+    }
+    block_csum_store<NT, kObsFields>(v, cv, a.status->obs);
+}
+
 template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH>
 __global__ void __launch_bounds__(NT, (KGeom<MF, M, NT, PH>::MINB))
 mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
@@ -1594,8 +1648,15 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     __syncthreads();
 #endif
     // the later-sweep launch of this step takes its chunks from these counters
+    // (counter 0 is the first sweep's own: the later-sweep launch of the previous step reset it)
     if (PH == 1 && a.work && blockIdx.x == 0)
-        for (int q = threadIdx.x; q < kWorkCounters; q += NT) a.work[q] = 0u;
+        for (int q = 1 + threadIdx.x; q < kWorkCounters; q += NT) a.work[q] = 0u;
+    if (PH == 2 && a.work && blockIdx.x == 0 && threadIdx.x == 0) a.work[0] = 0u;
+    // The later-sweep launch of a split step sums the first-sweep launch's energy partials
+    // before its sweeps, not after them (a serial pass of ~17 us at cfg5 by one warp of
+    // block 0: the chunked sweeps give its rows to the other CTAs meanwhile).
+    const bool obs_early = PH == 2 && a.sweep0 == 0;
+    if (obs_early) reduce_obs<NT>(a);
     int pass = 0;  // sweep passes of this launch (one chunk counter each)
     int sweeps = 0, set = 0, converged = 0, redone = 0;
     bool redo = false;  // this pass repeats the missed speculative sweep with all stages
@@ -1625,12 +1686,17 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
         unsigned rmax = 0u;
         if (PH == 1 || PH == 3 || (PH == 0 && sg == 0)) {
             const double2* const uin[3] = {a.u0, a.u0, a.u0};
+            // (chunked first sweep of a split step: counter 0, one set of partials per chunk)
+            unsigned* const fwork = PH == 1 && a.work && a.dyn_first ? a.work : nullptr;
             if constexpr (PH != 2)  // (not instantiated for the later-sweep kernel)
-                sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc);
+                sweep_all3<MF, NT, true, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc, 7, fwork);
             if (a.want_obs) {
                 // compensated warp and block trees; one rounding per block partial
-                monitor_flush(acc);
-                block_csum_store<NT, kObsFields>(acc + kAccTot, acc + kAccCarry, a.obs_partial + blockIdx.x * kObsFields);
+                if (!(MB4_DYN_SPLIT && MB4_DYN_FIRST && MF >= 3 && MF <= 7 && MB4_FIRST_V2 && fwork)) {
+                    monitor_flush(acc);
+                    block_csum_store<NT, kObsFields>(acc + kAccTot, acc + kAccCarry,
+                                                     a.obs_partial + blockIdx.x * kObsFields);
+                }
                 // max |u0|^2 of the entry state (non-negative: its bits order as integers)
                 double mx = acc[kAccMax];
 #pragma unroll
@@ -1645,7 +1711,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             // (same inputs, same arithmetic, so the result is independent of the guess).
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            unsigned* const work = PH == 2 && a.work && pass < kWorkCounters ? a.work + pass : nullptr;
+            unsigned* const work = PH == 2 && a.work && pass + 1 < kWorkCounters ? a.work + 1 + pass : nullptr;
             ++pass;
             sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc,
                                                        sg == a.spec_sweep && !redo ? 4 : 7, work);
@@ -1704,13 +1770,7 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
              !(amax2 >= a.amax2_lo && amax2 <= a.amax2_hi)))
             *a.batch_abort = 1;
     }
-    if (a.want_obs && blockIdx.x == 0 && threadIdx.x < kObsFields) {
-        double v = 0.0, cv = 0.0;  // fixed block order, compensated
-        const int nb = a.obs_blocks > 0 ? a.obs_blocks : static_cast<int>(gridDim.x);
-        for (int b = 0; b < nb; ++b) two_sum_add(v, cv, a.obs_partial[b * kObsFields + threadIdx.x]);
-        if (a.obs_accumulate) two_sum_add(v, cv, a.status->obs[threadIdx.x]);
-        a.status->obs[threadIdx.x] = v + cv;
-    }
+    if (!obs_early) reduce_obs<NT>(a);
 }
 
 template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH = 0>
@@ -1774,6 +1834,19 @@ struct Launcher3 {
 template <int MF, int M, int NT, bool ISO, bool DEF>
 cudaError_t launch_split(StepArgs a, const SweepConsts& c, int device, cudaStream_t s) {
     a.obs_blocks = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::launch_grid(a, device);
+    a.dyn_first = 0;
+    if constexpr (MB4_DYN_SPLIT && MB4_DYN_FIRST && MF >= 3 && MF <= 7 && MB4_FIRST_V2) {
+        if (a.work) {
+            // one set of energy partials per chunk of the first sweep, if the buffer holds them
+            constexpr int TXF = first_sweep_tx<MF, MB4_NT_FIRST>();
+            const long long total = static_cast<long long>((a.nx + TXF - 1) / TXF) * a.ny;
+            const long long chunks = dyn_chunk_count(total, a.obs_blocks, MB4_DYN_SMIN);
+            if (chunks <= a.obs_cap) {
+                a.dyn_first = 1;
+                a.obs_blocks = static_cast<int>(chunks);
+            }
+        }
+    }
     const cudaError_t e = Launcher3<MF, M, MB4_NT_FIRST, ISO, false, DEF, 1>::launch(a, c, device, s);
     if (e != cudaSuccess) return e;
     return Launcher3<MF, M, MB4_NT_LATER, ISO, false, DEF, 2>::launch(a, c, device, s);
@@ -1871,9 +1944,11 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                double* obs_partial, void* status, int max_iters, double eps,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
-                               int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch, unsigned* work) {
+                               int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch, unsigned* work,
+                               int obs_cap) {
     StepArgs a{};
     a.work = work;
+    a.obs_cap = obs_cap;
     if (batch) {
         a.batch_abort = batch->abort;
         a.expect_sweeps = batch->expect_sweeps;
