@@ -144,6 +144,14 @@
 #ifndef MB4_DYN_FIRST
 #define MB4_DYN_FIRST 0
 #endif
+// depth-1 later sweeps: no halo columns in the z rings.  Every thread fills its own column
+// only; the band is one more column wider than its output on either side (TX = NT - 4), and
+// lanes 0 / NT - 1 read an unfilled neighbour column, which only reaches masked lanes.  The
+// halo fill was a divergent second copy pass (address arithmetic + 5 copies for 2 lanes)
+// that warp 0 of every CTA ran on every row before the row's barrier partners could go on.
+#ifndef MB4_NOHALO
+#define MB4_NOHALO 1
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
@@ -166,7 +174,8 @@ namespace {
 template <int M, int NT>
 struct Geom3 {
     static_assert(M >= 0 && M <= 2, "march v3 supports Neumann depth 0..2");
-    static constexpr int TX = NT - 2 * M;   // output columns per band
+    static constexpr int SH = MB4_NOHALO && M == 1 ? 1 : 0;  // unfilled ring columns per side
+    static constexpr int TX = NT - 2 * (M + SH);  // output columns per band
     static constexpr int ZW = NT + 2;       // columns per smem row (1-site pad each side)
     static constexpr int S = 6;             // z ring rows (divisible by the unroll of 3)
     static constexpr int BACK = M == 2 ? 3 : 1;  // oldest z row still read: j - BACK
@@ -402,7 +411,7 @@ struct March3 {
 #endif
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                if (h == 1 && t >= 2) break;
+                if (h == 1 && (G::SH || t >= 2)) break;
                 // thread t fills its own column t + 1 (so it may read it before the row
                 // barrier); threads 0 / 1 also fill the halo columns 0 / NT + 1
                 const int col = h ? (t == 0 ? 0 : NT + 1) : t + 1;
@@ -578,8 +587,8 @@ struct March3 {
         issue_row(a, uin, s, j + G::P, ring(-G::P));
 
         const int yrel = i - 2 * M;  // output row offset from Y0
-        const int xout = s.X0 - M + t;
-        const bool out_ok = yrel >= 0 && yrel < s.R && t >= M && t < NT - M && xout < s.xlim;
+        const int xout = s.X0 - (M + G::SH) + t;
+        const bool out_ok = yrel >= 0 && yrel < s.R && t >= M + G::SH && t < NT - (M + G::SH) && xout < s.xlim;
         const int par = j & 1, ppar = par ^ 1;
 
         // own-column level history, read before this iteration overwrites it
@@ -622,7 +631,7 @@ struct March3 {
                     for (int k = 0; k < 3; ++k) pb[k] = make_double2(cf.fs(k) * f.x, cf.fs(k) * f.y);
                 }
                 // energy monitor of u0 on owned sites (lattice.cpp:106-137)
-                if (i >= M && i < M + s.R && t >= M && t < NT - M && xout < s.xlim) {
+                if (i >= M && i < M + s.R && t >= M + G::SH && t < NT - (M + G::SH) && xout < s.xlim) {
                     const double vn = v * n2;
                     const double sc = ISO ? c.cx : 1.0;
                     monitor_add(acc, fma(sc, fma(u0c.x, w0.x, u0c.y * w0.y), -vn), sc * fma(u0c.x, w0.y, -u0c.y * w0.x), n2,
@@ -813,7 +822,7 @@ struct March3 {
             s.next_row = wrap_index(s.yz0, a.ny);
             s.next_off = static_cast<size_t>(s.next_row) * a.nx;
         }
-        const int xz0 = s.X0 - M - 1;  // global column of smem column 0
+        const int xz0 = s.X0 - M - 1 - G::SH;  // global column of smem column 0
         const int t = static_cast<int>(threadIdx.x);
         const int xa = xz0 + t + 1, xb = t == 0 ? xz0 : xz0 + NT + 1;  // see issue_row
         if (GHOST) {
