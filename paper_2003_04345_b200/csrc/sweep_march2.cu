@@ -152,6 +152,12 @@
 #ifndef MB4_NOHALO
 #define MB4_NOHALO 1
 #endif
+// depth-1 later sweeps: the own-column Phi of the last two rows in a register window (slot =
+// row mod 3, static after the unroll by 3) instead of re-read from the published rows
+// (6 LDS.128 = 24 of ~128 shared-memory wavefronts per warp-row)
+#ifndef MB4_PHI_REGS
+#define MB4_PHI_REGS 1
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
@@ -346,6 +352,7 @@ struct March3 {
 
     double2 zw[3][4];  // own-column z rows; slot of z row k = k mod 3
     double vw[3];
+    double2 pw[3][3];  // own-column Phi rows (MB4_PHI_REGS); slot of the row of iteration j = j mod 3
 #if MB4_BULK
     unsigned long long* bars;  // one mbarrier per z ring slot (bulk row copies)
     __device__ static unsigned long long* ring_bars() {
@@ -706,9 +713,10 @@ struct March3 {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const double2* prow = pub_row(0, ppar, k);  // Phi row i - 1
-                tc[k] = prow[cc];
-                const double2 td = pub_row(0, par, k)[cc];  // row i - 2
+                tc[k] = MB4_PHI_REGS ? pw[S_CEN][k] : prow[cc];
+                const double2 td = MB4_PHI_REGS == 1 ? pw[S_DN][k] : pub_row(0, par, k)[cc];  // row i - 2
                 jk[k] = cf.jt_pqr(K1, tc[k], cf.nsum(prow[cc - 1], prow[cc + 1], td, pb[k]));
+                if (MB4_PHI_REGS) pw[S_NEW][k] = pb[k];
             }
 #pragma unroll
             for (int k = 0; k < 3; ++k) pub_row(0, par, k)[cc] = pb[k];
