@@ -137,6 +137,10 @@
 #ifndef MB4_DYN_SMIN
 #define MB4_DYN_SMIN 32
 #endif
+// rows of a first-round chunk = (rows per CTA) * MB4_DYN_NUM / 8
+#ifndef MB4_DYN_NUM
+#define MB4_DYN_NUM 4
+#endif
 // the first sweep of a split step in chunks as well (its two CTAs per SM finish 6 % apart
 // with fixed shares); every chunk stores its own energy partial sums, so the energy record
 // does not depend on which CTA took which chunk.  Measured slower (cfg5 1.40 -> 1.49 ms):
@@ -1477,7 +1481,7 @@ __device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) 
 // past the last chunk.  Round c / G has chunks of (total / G) >> (round + 1) rows, at least smin.
 __host__ __device__ inline bool dyn_chunk(long long c, long long total, long long G, long long smin, long long& p0,
                                           long long& p1) {
-    long long start = 0, sz = (total / G) >> 1;
+    long long start = 0, sz = (total / G) * MB4_DYN_NUM / 8;
     for (;;) {
         if (sz <= smin) {
             sz = smin;
@@ -1494,7 +1498,7 @@ __host__ __device__ inline bool dyn_chunk(long long c, long long total, long lon
     return true;
 }
 inline long long dyn_chunk_count(long long total, long long G, long long smin) {
-    long long n = 0, start = 0, sz = (total / G) >> 1;
+    long long n = 0, start = 0, sz = (total / G) * MB4_DYN_NUM / 8;
     while (sz > smin && start + G * sz <= total) {  // full rounds
         start += G * sz;
         n += G;
