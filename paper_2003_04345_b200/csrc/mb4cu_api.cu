@@ -65,6 +65,7 @@ struct mb4cu_ctx {
     // persistent-kernel path
     unsigned long long* d_rmax_arr = nullptr;  // [max_iters + 1]: residual bits per sweep, max |u0|^2
     unsigned* d_work = nullptr;                // [kWorkCounters]: chunk counters of the later sweeps
+    int work_seq = 0;                          // sub-domain sweep launches so far (rotating counter index)
     double* d_obs_march = nullptr;             // [grid][kObsFields]
     mb4cu::StepStatus* d_status = nullptr;
     mb4cu::StepStatus* h_status = nullptr;     // pinned
@@ -2178,7 +2179,9 @@ int sweep_region_impl(mb4cu_ctx* ctx, double h, int s, int final_guess, int regi
                                                 ctx->d_rmax_arr, ctx->d_obs_march, ctx->d_status, 1, -1.0,
                                                 s == 0 ? 1 : 0, c, ctx->device, ctx->stream, ctx->ghost, s,
                                                 final_guess && s > 0 ? s : -1, nrect, rects, region == 2 ? 1 : 0,
-                                                region == 2 ? grid_cap : 0, skip ? &skipctl : nullptr, ctx->pitch));
+                                                region == 2 ? grid_cap : 0, skip ? &skipctl : nullptr, ctx->pitch,
+                                                ctx->d_work, 0,
+                                                s > 0 ? ctx->work_seq++ % mb4cu::kWorkCounters : -1));
         if (ctx->profiling) ctx->prof.launches += 1;
     }
     if (region != 1) {

@@ -181,6 +181,7 @@ struct StepArgs {
     unsigned* work;
     // work != nullptr: the first-sweep launch takes chunks as well (counter 0; the later
     // sweeps use counters 1..), and writes one set of energy partial sums per chunk
+    int work_idx;               // >= 0: a one-sweep launch that takes its chunks from work[work_idx]
     int dyn_first;
     int obs_cap;                // partial-sum slots obs_partial holds (0: one per CTA of the largest grid)
 };
@@ -262,7 +263,7 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                int ghost, int sweep0, int spec_sweep = -1, int nrect = 0,
                                const int (*rects)[4] = nullptr, int obs_accumulate = 0, int grid_cap = 0,
                                const BatchCtl* batch = nullptr, int pitch = 0, unsigned* work = nullptr,
-                               int obs_cap = 0);
+                               int obs_cap = 0, int work_idx = -1);
 int march2_grid_size(int mf, int m, int device);
 // output columns per band of the sub-domain sweep kernels (0: no band structure)
 int march2_band_width(int mf, int m, bool first);

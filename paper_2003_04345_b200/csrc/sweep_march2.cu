@@ -1446,35 +1446,51 @@ struct MarchFirst2 {
 
 // Split the band-rows of this launch's output rectangles evenly over the grid and
 // march each segment (a run of rows of one band of one rectangle).
-template <int TX, class Run>
-__device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) {
-    const int nr = a.nrect > 0 ? a.nrect : 1;
-    auto rect = [&](int r, int k) {
+// Band-rows of this launch's output rectangles (the whole domain if it has none) in one flat
+// order: rectangle by rectangle, band by band, row by row.
+template <int TX>
+struct BandRows {
+    const StepArgs& a;
+    int nr;
+    __device__ explicit BandRows(const StepArgs& args) : a(args), nr(args.nrect > 0 ? args.nrect : 1) {}
+    __device__ __forceinline__ int rect(int r, int k) const {
         if (a.nrect > 0) return a.rect[r][k];
         return k == 2 ? a.nx : (k == 3 ? a.ny : 0);
-    };
-    long long total = 0;
-    for (int r = 0; r < nr; ++r) total += static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
-    const long long G = gridDim.x;
-    const long long b0 = total * blockIdx.x / G;
-    const long long b1 = total * (blockIdx.x + 1) / G;
-    for (long long pos = b0; pos < b1;) {
-        long long base = 0;
-        int r = 0;
-        for (; r + 1 < nr; ++r) {
-            const long long cnt = static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
-            if (pos < base + cnt) break;
-            base += cnt;
-        }
-        const int h = rect(r, 3);
-        const long long local = pos - base;
-        const int band = static_cast<int>(local / h);
-        const int row = static_cast<int>(local - static_cast<long long>(band) * h);
-        const long long band_end = base + static_cast<long long>(band + 1) * h;
-        const long long seg_end = band_end < b1 ? band_end : b1;
-        run(rect(r, 0) + band * TX, rect(r, 0) + rect(r, 2), rect(r, 1) + row, static_cast<int>(seg_end - pos));
-        pos = seg_end;
     }
+    __device__ __forceinline__ long long total() const {
+        long long t = 0;
+        for (int r = 0; r < nr; ++r) t += static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
+        return t;
+    }
+    // march the band-rows [p0, p1): one segment per run of rows of one band
+    template <class Run>
+    __device__ __forceinline__ void march(long long p0, long long p1, const Run& run) const {
+        for (long long pos = p0; pos < p1;) {
+            long long base = 0;
+            int r = 0;
+            for (; r + 1 < nr; ++r) {
+                const long long cnt = static_cast<long long>((rect(r, 2) + TX - 1) / TX) * rect(r, 3);
+                if (pos < base + cnt) break;
+                base += cnt;
+            }
+            const int h = rect(r, 3);
+            const long long local = pos - base;
+            const int band = static_cast<int>(local / h);
+            const int row = static_cast<int>(local - static_cast<long long>(band) * h);
+            const long long band_end = base + static_cast<long long>(band + 1) * h;
+            const long long seg_end = band_end < p1 ? band_end : p1;
+            run(rect(r, 0) + band * TX, rect(r, 0) + rect(r, 2), rect(r, 1) + row, static_cast<int>(seg_end - pos));
+            pos = seg_end;
+        }
+    }
+};
+
+template <int TX, class Run>
+__device__ __forceinline__ void for_segments(const StepArgs& a, const Run& run) {
+    const BandRows<TX> rows(a);
+    const long long total = rows.total();
+    const long long G = gridDim.x;
+    rows.march(total * blockIdx.x / G, total * (blockIdx.x + 1) / G, run);
 }
 
 // Chunk c of the guided split of `total` band-rows over a grid of G CTAs -> [p0, p1); false
@@ -1508,14 +1524,14 @@ inline long long dyn_chunk_count(long long total, long long G, long long smin) {
     return n + (total - start + sz - 1) / sz;
 }
 
-// The same march over chunks of band-rows taken from the counter *ctr (whole domain only).
+// The same march over chunks of band-rows taken from the counter *ctr.
 // Chunk c of round c / G (G = gridDim.x) has q >> (round + 1) rows, q = total / G, at least
 // MB4_DYN_SMIN: a fixed map chunk -> rows, so only the CTA that computes a row varies.
 template <int TX, class Run, class Done>
 __device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ctr, const Run& run, const Done& done) {
     __shared__ unsigned s_chunk[2];
-    const int nbands = (a.nx + TX - 1) / TX;
-    const long long total = static_cast<long long>(nbands) * a.ny;
+    const BandRows<TX> rows(a);
+    const long long total = rows.total();
     int flip = 0;
     for (;;) {
         if (threadIdx.x == 0) s_chunk[flip] = atomicAdd(ctr, 1u);
@@ -1524,14 +1540,7 @@ __device__ __forceinline__ void for_segments_dyn(const StepArgs& a, unsigned* ct
         flip ^= 1;
         long long p0, p1;
         if (!dyn_chunk(c, total, gridDim.x, MB4_DYN_SMIN, p0, p1)) break;
-        for (long long pos = p0; pos < p1;) {
-            const int band = static_cast<int>(pos / a.ny);
-            const int row = static_cast<int>(pos - static_cast<long long>(band) * a.ny);
-            const long long band_end = static_cast<long long>(band + 1) * a.ny;
-            const long long seg_end = band_end < p1 ? band_end : p1;
-            run(band * TX, a.nx, row, static_cast<int>(seg_end - pos));
-            pos = seg_end;
-        }
+        rows.march(p0, p1, run);
         done(c);
     }
 }
@@ -1568,7 +1577,7 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
         auto seg = [&](int X0, int xlim, int Y0, int R) { m.run(a, c, uin, uout, X0, xlim, Y0, R, rmax, acc, smask); };
         // (depth-2 sweeps run 2 CTAs per SM, which finish together: measured 2.5 % slower
         // with chunks at cfg4, so they keep the fixed shares)
-        if (MB4_DYN_SPLIT && !FIRST && !GHOST && M == 1 && work) {
+        if (MB4_DYN_SPLIT && !FIRST && M == 1 && work) {
             for_segments_dyn<Geom3<M, NT>::TX>(a, work, seg, [](long long) {});
         } else {
             for_segments<Geom3<M, NT>::TX>(a, seg);
@@ -1636,6 +1645,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     extern __shared__ __align__(16) unsigned char smem[];
     // a batched step after one that ended the batch: nothing to do (the flag was set by
     // an earlier launch on this stream, so every CTA of this grid reads the same value)
+    // (one-sweep launches rotate through the chunk counters: this one resets the counter of the
+    // launch kWorkCounters / 2 launches ahead -- also when it is skipped below)
+    if (PH == 2 && a.work && a.work_idx >= 0 && blockIdx.x == 0 && threadIdx.x == 0)
+        a.work[(a.work_idx + kWorkCounters / 2) % kWorkCounters] = 0u;
     if (a.batch_abort && *reinterpret_cast<volatile const int*>(a.batch_abort)) return;
     if (a.skip && *reinterpret_cast<volatile const int*>(a.skip)) return;
     cg::grid_group grid = cg::this_grid();
@@ -1670,9 +1683,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 #endif
     // the later-sweep launch of this step takes its chunks from these counters
     // (counter 0 is the first sweep's own: the later-sweep launch of the previous step reset it)
-    if (PH == 1 && a.work && blockIdx.x == 0)
+    if (PH == 1 && a.work && a.work_idx < 0 && blockIdx.x == 0)
         for (int q = 1 + threadIdx.x; q < kWorkCounters; q += NT) a.work[q] = 0u;
-    if (PH == 2 && a.work && blockIdx.x == 0 && threadIdx.x == 0) a.work[0] = 0u;
+    if (PH == 2 && a.work && a.work_idx < 0 && blockIdx.x == 0 && threadIdx.x == 0) a.work[0] = 0u;
     // The later-sweep launch of a split step sums the first-sweep launch's energy partials
     // before its sweeps, not after them (a serial pass of ~17 us at cfg5 by one warp of
     // block 0: the chunked sweeps give its rows to the other CTAs meanwhile).
@@ -1732,7 +1745,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             // (same inputs, same arithmetic, so the result is independent of the guess).
             const int in = 1 - out;
             const double2* const uin[3] = {a.U[in][0], a.U[in][1], a.U[in][2]};
-            unsigned* const work = PH == 2 && a.work && pass + 1 < kWorkCounters ? a.work + 1 + pass : nullptr;
+            unsigned* const work = PH != 2 || !a.work ? nullptr
+                                   : a.work_idx >= 0           ? a.work + a.work_idx  // (one-sweep launches)
+                                   : pass + 1 < kWorkCounters  ? a.work + 1 + pass
+                                                               : nullptr;
             ++pass;
             sweep_all3<M, NT, false, ISO, GHOST, DEF>(a, cc, smem, uin, uout, rmax, acc,
                                                        sg == a.spec_sweep && !redo ? 4 : 7, work);
@@ -1878,7 +1894,9 @@ cudaError_t dispatch3(const StepArgs& a0, const SweepConsts& c, int device, cuda
     StepArgs a = a0;
     // chunk counters: only the split pair of a whole domain (its first-sweep launch zeroes them)
     const bool split = MB4_SPLIT && MF >= 4 && a.ghost == 0 && a.sweep0 == 0 && a.max_iters > 1;
-    if (!split || a.nrect > 0) a.work = nullptr;
+    // ... and the one-sweep later-sweep launches of a sub-domain (a rotating counter, work_idx)
+    const bool region = MB4_SPLIT && MF >= 4 && a.ghost > 0 && a.max_iters == 1 && a.sweep0 > 0 && a.work_idx >= 0;
+    if (!(split && a.nrect == 0 && a.work_idx < 0) && !region) a.work = nullptr;
     if constexpr (MB4_SPLIT && MF >= 4) {
         if (a.ghost == 0 && a.sweep0 == 0 && a.max_iters > 1) {
             if (c.iso && c.def) return launch_split<MF, M, MB4_NT, true, true>(a, c, device, s);
@@ -1966,9 +1984,10 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                int want_obs, const SweepConsts& c, int device, cudaStream_t s,
                                int ghost, int sweep0, int spec_sweep, int nrect, const int (*rects)[4],
                                int obs_accumulate, int grid_cap, const BatchCtl* batch, int pitch, unsigned* work,
-                               int obs_cap) {
+                               int obs_cap, int work_idx) {
     StepArgs a{};
     a.work = work;
+    a.work_idx = work && work_idx >= 0 ? work_idx % kWorkCounters : -1;
     a.obs_cap = obs_cap;
     if (batch) {
         a.batch_abort = batch->abort;
