@@ -1577,7 +1577,11 @@ __device__ void sweep_all3(const StepArgs& a, const SweepConsts& c, unsigned cha
         auto seg = [&](int X0, int xlim, int Y0, int R) { m.run(a, c, uin, uout, X0, xlim, Y0, R, rmax, acc, smask); };
         // (depth-2 sweeps run 2 CTAs per SM, which finish together: measured 2.5 % slower
         // with chunks at cfg4, so they keep the fixed shares)
-        if (MB4_DYN_SPLIT && !FIRST && M == 1 && work) {
+        // (small lattices keep the fixed shares too: below ~4 minimum chunks per CTA the chunk
+        // restarts and the idle CTAs cost more than the uneven finish -- cfg1's depth-1 sweeps
+        // ran 0.023 instead of 0.0075 ms in chunks)
+        if (MB4_DYN_SPLIT && !FIRST && M == 1 && work &&
+            BandRows<Geom3<M, NT>::TX>(a).total() >= 4ll * MB4_DYN_SMIN * gridDim.x) {
             for_segments_dyn<Geom3<M, NT>::TX>(a, work, seg, [](long long) {});
         } else {
             for_segments<Geom3<M, NT>::TX>(a, seg);
