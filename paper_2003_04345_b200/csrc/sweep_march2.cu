@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "async_copy.cuh"
 #include "mb4cu_internal.hpp"
@@ -161,6 +162,18 @@
 // (6 LDS.128 = 24 of ~128 shared-memory wavefronts per warp-row)
 #ifndef MB4_PHI_REGS
 #define MB4_PHI_REGS 1
+#endif
+// first sweep at depth 6: the row loop unrolled by 6, so the register pipelines of the site
+// coefficients (6 rows of P, Q, R) and the u0 / V window (3 rows) rotate by static indices
+// instead of ~60 register moves per row (20 % of the row's instructions)
+#ifndef MB4_FIRST_UNROLL6
+#define MB4_FIRST_UNROLL6 1
+#endif
+// ... and with static slots the own-column history of g_3 (a ring of 3 iterations) and g_2
+// (of 6) holds the value the output row needs: two fewer history reads from shared memory
+// (8 of ~119 wavefronts per warp-row).  0: off, 1: g_3, 2: g_3 and g_2, 3: and g_1.
+#ifndef MB4_FIRST_GREG
+#define MB4_FIRST_GREG 3
 #endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
@@ -1199,7 +1212,18 @@ struct MarchFirst2 {
     double2 zw[NZW];
     double vw[NZW];
 #endif
-    double2 gp[MF][2];  // own-column g_n of the last two iterations (slot = parity)
+    // own-column g_n of the last iterations: slot = iteration mod gring(n) (2 = parity)
+    static constexpr bool U6pre = MB4_FIRST_UNROLL6 && MB4_FIRST_PQR && MF == 6;
+    __host__ __device__ static constexpr int gring(int n) {
+        return U6pre && MB4_FIRST_GREG >= 1 && n == MF - 3 ? 3
+               : U6pre && ((MB4_FIRST_GREG >= 2 && n == MF - 4) || (MB4_FIRST_GREG >= 3 && n == MF - 5)) ? 6
+                                                                                                         : 2;
+    }
+    double2 gp[MF][U6pre ? 6 : 2];
+    // MB4_FIRST_UNROLL6: physical slots of the logical pipeline entries at iteration j, ROT = j mod 6
+    static constexpr bool U6 = MB4_FIRST_UNROLL6 && MB4_FIRST_PQR && MF == 6;
+    __host__ __device__ static constexpr int kix(int k, int rot) { return U6 ? (k - 2 + 12 - rot) % 6 + 2 : k; }
+    __host__ __device__ static constexpr int zix(int k, int rot) { return U6 ? (k + 6 - rot) % 3 : k; }
 
 #if MB4_BULK
     unsigned long long* bars;  // one mbarrier per z ring slot (bulk u0 row copies)
@@ -1256,14 +1280,16 @@ struct MarchFirst2 {
 
     struct Chain {
         double2 up, low, mid, u0o;
+        double2 old3, old4, old5;  // g_{MF-3}, g_{MF-4}, g_{MF-5} of the output row (MB4_FIRST_GREG)
     };
 
     // level N: g_N at row i - N from g_{N-1} rows i-N-1 (register), i-N (ring, previous
     // iteration), i-N+1 (this iteration, ch.up)
-    template <int N, int PAR>
+    template <int N, int ROT>
     __device__ __forceinline__ void levels(const Coef<ISO>& cf, unsigned char* smt, unsigned char* smv,
                                            int jrb, int o8, int p8, int o4, int p4, Chain& ch) {
         if constexpr (N <= MF) {
+            constexpr int PAR = ROT & 1;
             constexpr int n = N - 1;
             constexpr int D = depth(n);
             constexpr int HB = H0 + hrow(n) * RB;
@@ -1271,10 +1297,16 @@ struct MarchFirst2 {
             const int sp = D == 2 ? (PAR ^ 1) * RB : (D == 8 ? p8 : p4);
             unsigned char* crow = smt + HB + sp;  // g_n, iteration j - 1
             unsigned char* own = smt + HB + so;   // g_n, iteration j
-            const double2 gc = gp[n][PAR ^ 1];
-            const double2 gd = gp[n][PAR];
+            constexpr int RS = gring(n);
+            constexpr int S_NOW = ROT % RS, S_M1 = (ROT + RS - 1) % RS, S_M2 = (ROT + RS - 2) % RS;
+            const double2 gc = gp[n][S_M1];
+            const double2 gd = gp[n][S_M2];
+            // the output row's g_n: written MF - n iterations ago
+            if constexpr (RS == 3) ch.old3 = gp[n][S_NOW];
+            if constexpr (RS == 6 && n == MF - 4) ch.old4 = gp[n][(ROT + 6 - (MF - n)) % 6];
+            if constexpr (RS == 6 && n == MF - 5) ch.old5 = gp[n][(ROT + 6 - (MF - n)) % 6];
 #if MB4_FIRST_PQR
-            const double2 gn = cf.jt_pqr(kw[N + 1], gc, cf.nsum(ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up));
+            const double2 gn = cf.jt_pqr(kw[kix(N + 1, ROT)], gc, cf.nsum(ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up));
 #else
             double2 u0n;
             double vn;
@@ -1291,11 +1323,11 @@ struct MarchFirst2 {
             if (N == MF) ch.u0o = u0n;
 #endif
             ref<double2>(own) = ch.up;
-            gp[n][PAR] = ch.up;
+            gp[n][S_NOW] = ch.up;
             if (N == MF - 1) ch.low = gd;
             if (N == MF) ch.mid = gc;
             ch.up = gn;
-            levels<N + 1, PAR>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
+            levels<N + 1, ROT>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
         }
     }
 
@@ -1303,16 +1335,19 @@ struct MarchFirst2 {
     template <int N>
     __device__ __forceinline__ void gather(unsigned char* smt, int jrb, double2* gout) {
         if constexpr (N + 3 <= MF) {
-            constexpr int D = depth(N);
-            const int so = (jrb - (MF - N) * RB) & (D * RB - 1);
-            gout[N] = ref<double2>(smt + H0 + hrow(N) * RB + so);
+            if constexpr (gring(N) == 2) {
+                constexpr int D = depth(N);
+                const int so = (jrb - (MF - N) * RB) & (D * RB - 1);
+                gout[N] = ref<double2>(smt + H0 + hrow(N) * RB + so);
+            }
             gather<N + 1>(smt, jrb, gout);
         }
     }
 
-    template <int PAR>  // = j & 1
+    template <int ROT>  // = j mod 6 (MB4_FIRST_UNROLL6) or j & 1
     __device__ __forceinline__ void body(const StepArgs& a, const Coef<ISO>& cf, double2* const uout[3], Seg& s,
                                          int j, unsigned& rmax, double* acc) {
+        constexpr int Z0 = zix(0, ROT), Z1 = zix(1, ROT), Z2 = zix(2, ROT);
         const SweepConsts& c = cf.c;
         const int t = threadIdx.x, i = j - 2;
         unsigned char* smt = sm + t * 16;
@@ -1335,15 +1370,15 @@ struct MarchFirst2 {
         const bool lane_ok = t >= MF + 1 && t < NT - MF - 1 && xout < s.xlim;
         const bool out_ok = lane_ok && yrel >= 0 && yrel < s.R;
 
-        zw[0] = ref<double2>(smt + ZU + zn);
-        vw[0] = ref<double>(smv + ZV + (zn >> 1));
+        zw[Z0] = ref<double2>(smt + ZU + zn);
+        vw[Z0] = ref<double>(smv + ZV + (zn >> 1));
 
         // ---- level 0 at row i: f(u0) and the energy monitor --------------------
-        const double v = vw[1];
-        const double2 u0c = zw[1];
+        const double v = vw[Z1];
+        const double2 u0c = zw[Z1];
         const double d0 = cf.dv(v);
         const double2 w0 = cf.kv(d0, u0c, ref<double2>(smt + ZU + zc - 16), ref<double2>(smt + ZU + zc + 16),
-                                 zw[2], zw[0]);
+                                 zw[Z2], zw[Z0]);
         const double n2 = fma(u0c.x, u0c.x, u0c.y * u0c.y);
         const double gx = fma(-cf.g() * n2, u0c.x, w0.x);
         const double gy = fma(-cf.g() * n2, u0c.y, w0.y);
@@ -1357,11 +1392,14 @@ struct MarchFirst2 {
 
         // ---- levels 1..MF --------------------------------------------------------
         Chain ch{f, f, f, f};
-        levels<1, PAR>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
+        levels<1, ROT>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
 
         if (out_ok) {
             double2 gout[MF + 1];
             gather<0>(smt, jrb, gout);
+            if constexpr (gring(MF - 3) == 3) gout[MF - 3] = ch.old3;
+            if constexpr (MF >= 4 && gring(MF >= 4 ? MF - 4 : 0) == 6) gout[MF - 4] = ch.old4;
+            if constexpr (MF >= 5 && gring(MF >= 5 ? MF - 5 : 0) == 6) gout[MF - 5] = ch.old5;
             gout[MF - 2] = ch.low;
             gout[MF - 1] = ch.mid;
             gout[MF] = ch.up;
@@ -1385,14 +1423,21 @@ struct MarchFirst2 {
             }
         }
 #if MB4_FIRST_PQR
+        if constexpr (U6) {
+            // the next iteration's entry 2 takes the slot of this iteration's oldest entry
+            kw[kix(2, (ROT + 1) % 6)] = cf.pqr(d0, u0c);
+        } else {
 #pragma unroll
-        for (int k = MF + 1; k > 2; --k) kw[k] = kw[k - 1];
-        kw[2] = cf.pqr(d0, u0c);  // z row j - 1 becomes row j - 2 for level 1
+            for (int k = MF + 1; k > 2; --k) kw[k] = kw[k - 1];
+            kw[2] = cf.pqr(d0, u0c);  // z row j - 1 becomes row j - 2 for level 1
+        }
 #endif
+        if constexpr (!U6) {
 #pragma unroll
-        for (int k = NZW - 1; k > 0; --k) {
-            zw[k] = zw[k - 1];
-            vw[k] = vw[k - 1];
+            for (int k = NZW - 1; k > 0; --k) {
+                zw[k] = zw[k - 1];
+                vw[k] = vw[k - 1];
+            }
         }
     }
 
@@ -1433,12 +1478,25 @@ struct MarchFirst2 {
         for (int k = 0; k < P; ++k) issue_row(a, s, k);
         const int jend = R + 2 * MF + 2;
         int j = 0;
-        for (; j + 1 < jend; j += 2) {
-            body<0>(a, cf, uout, s, j, rmax, acc);
-            body<1>(a, cf, uout, s, j + 1, rmax, acc);
-            if ((j & (kMonitorRows - 1)) == kMonitorRows - 2) monitor_flush(acc);  // every kMonitorRows rows
+        if constexpr (U6) {
+            // (up to five iterations past the last row: they read the rings and store nothing)
+            for (; j < jend; j += 6) {
+                body<0>(a, cf, uout, s, j, rmax, acc);
+                body<1>(a, cf, uout, s, j + 1, rmax, acc);
+                body<2>(a, cf, uout, s, j + 2, rmax, acc);
+                body<3>(a, cf, uout, s, j + 3, rmax, acc);
+                body<4>(a, cf, uout, s, j + 4, rmax, acc);
+                body<5>(a, cf, uout, s, j + 5, rmax, acc);
+                if ((j / 6) & 1) monitor_flush(acc);  // every 12 rows
+            }
+        } else {
+            for (; j + 1 < jend; j += 2) {
+                body<0>(a, cf, uout, s, j, rmax, acc);
+                body<1>(a, cf, uout, s, j + 1, rmax, acc);
+                if ((j & (kMonitorRows - 1)) == kMonitorRows - 2) monitor_flush(acc);  // every kMonitorRows rows
+            }
+            if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
         }
-        if (j < jend) body<0>(a, cf, uout, s, j, rmax, acc);
         cp_async_wait<0>();
         __syncthreads();
     }
@@ -1843,6 +1901,13 @@ struct Launcher3 {
     // the band-rows to march (no CTAs that only take part in the grid barriers)
     static int launch_grid(const StepArgs& a, int device) {
         int grid = grid_size(device);
+#ifdef MB4_CTA_TIMES
+        // profiling builds: MB4_DEBUG_GRID_CAP=<CTAs> (e.g. one CTA per SM: a warp's own stalls)
+        if (const char* e = std::getenv("MB4_DEBUG_GRID_CAP")) {
+            const int cap = std::atoi(e);
+            if (PH == 2 && cap > 0 && cap < grid) grid = cap;
+        }
+#endif
         if (a.grid_cap > 0 && a.grid_cap < grid) {
             grid = a.grid_cap;
         } else if (a.grid_cap < 0) {  // leave -grid_cap SMs to concurrent kernels (NCCL)
