@@ -1417,6 +1417,16 @@ int mb4cu_destroy(mb4cu_ctx* ctx) {
 
 const char* mb4cu_last_error(const mb4cu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+// Test hook (not part of the boundary, tests/test_chunks.py): chunk c of the chunked later
+// sweeps' split of `total` band-rows over G CTAs -> [*p0, *p1), 0 past the last chunk; c < 0
+// returns the number of chunks.
+extern "C" long long mb4cu_debug_chunk(long long c, long long total, long long G, long long* p0, long long* p1) {
+    if (total <= 0 || G <= 0) return -1;
+    if (c < 0) return mb4cu::march2_chunk_count(total, G);
+    if (!p0 || !p1) return -1;
+    return mb4cu::march2_chunk_range(c, total, G, p0, p1) ? 1 : 0;
+}
+
 int mb4cu_set_neumann_terms(mb4cu_ctx* ctx, int m) {
     if (!ctx) return MB4CU_INVALID;
     if (ctx->kernel != 0 || m < 0 || m > 2 || !mb4cu::march2_supported(ctx->mf, m) ||

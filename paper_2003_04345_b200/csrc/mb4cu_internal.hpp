@@ -265,6 +265,9 @@ cudaError_t launch_step_march2(int mf, int m, int nx, int ny, const double2* u0,
                                const BatchCtl* batch = nullptr, int pitch = 0, unsigned* work = nullptr,
                                int obs_cap = 0, int work_idx = -1);
 int march2_grid_size(int mf, int m, int device);
+// chunk map of the chunked later sweeps (test hooks)
+bool march2_chunk_range(long long c, long long total, long long G, long long* p0, long long* p1);
+long long march2_chunk_count(long long total, long long G);
 // output columns per band of the sub-domain sweep kernels (0: no band structure)
 int march2_band_width(int mf, int m, bool first);
 

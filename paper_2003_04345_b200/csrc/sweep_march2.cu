@@ -2036,6 +2036,13 @@ int grid3(int device) {
 #define MB4_MARCH2_PAIRS(X) X(0, 0) X(1, 1) X(2, 2) X(2, 0) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(4, 2) X(5, 2) X(6, 2) X(6, 0)
 #endif
 
+// The chunk map of the chunked later sweeps, for the host-side tests (every band-row belongs
+// to exactly one chunk): chunk c of `total` band-rows over a grid of G CTAs.
+bool march2_chunk_range(long long c, long long total, long long G, long long* p0, long long* p1) {
+    return dyn_chunk(c, total, G, MB4_DYN_SMIN, *p0, *p1);
+}
+long long march2_chunk_count(long long total, long long G) { return dyn_chunk_count(total, G, MB4_DYN_SMIN); }
+
 int march2_launches(int mf, int ghost, int sweep0, int max_iters) {
     return MB4_SPLIT && mf >= 4 && ghost == 0 && sweep0 == 0 && max_iters > 1 ? 2 : 1;
 }
