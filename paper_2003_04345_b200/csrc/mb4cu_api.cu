@@ -1330,10 +1330,14 @@ int mb4cu_create(const mb4cu_problem* p, const mb4cu_scheme* scheme, mb4cu_ctx**
         if (grid <= 0) return bail(cudaErrorLaunchOutOfResources, "march_grid_size");
         if ((e = cudaMalloc(&ctx->d_rmax_arr, sizeof(unsigned long long) * (ctx->max_iters + 1))) != cudaSuccess)
             return bail(e, "cudaMalloc(rmax_arr)");
-        if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
-            return bail(e, "cudaMalloc(work)");
-        if ((e = cudaMemset(ctx->d_work, 0, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
-            return bail(e, "cudaMemset(work)");
+        // chunk counters of the later sweeps (MB4CU_FIXED_SHARES: A/B switch for the tests --
+        // without counters every launch uses the fixed even split)
+        if (std::getenv("MB4CU_FIXED_SHARES") == nullptr) {
+            if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
+                return bail(e, "cudaMalloc(work)");
+            if ((e = cudaMemset(ctx->d_work, 0, sizeof(unsigned) * mb4cu::kWorkCounters)) != cudaSuccess)
+                return bail(e, "cudaMemset(work)");
+        }
         if ((e = cudaMalloc(&ctx->d_obs_march, sizeof(double) * mb4cu::kObsFields * mb4cu::kObsSlotsPerCta * grid)) !=
             cudaSuccess)
             return bail(e, "cudaMalloc(obs_march)");

@@ -411,3 +411,30 @@ def test_spectral_bound_tracks_the_amplitude_per_step(monkeypatch):
     ref, _, _, _ = O.ref_run(n, n, float(n), float(n), gamma, np.zeros(n * n), u0, dt, nsteps, eps=1e-14,
                              solver="gmres", record=False)
     assert rel(u_step, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("name,nx,ny", [("cfg4", 4096, 4096), ("cfg5", 2048, 4096)])
+def test_chunked_later_sweeps_are_bit_identical_to_fixed_shares(name, nx, ny, monkeypatch):
+    """The depth-1 later sweeps hand out their band-rows in chunks from a device counter
+    (which CTA computes a row varies from run to run); the arithmetic of a row does not
+    depend on it: state, energy record and sweep counts equal the fixed even split
+    (MB4CU_FIXED_SHARES: contexts created without chunk counters) bit for bit, and reruns
+    of the chunked path are bit-identical."""
+    cfg = configs.CONFIGS[name].with_lattice(nx, ny)
+    V, psi = configs.make_inputs(cfg)
+
+    def run(fixed):
+        if fixed:
+            monkeypatch.setenv("MB4CU_FIXED_SHARES", "1")
+        else:
+            monkeypatch.delenv("MB4CU_FIXED_SHARES", raising=False)
+        with session(cfg, V, neumann_terms=1) as s:
+            s.set_state(psi)
+            obs, it = s.run(cfg.dt, 4)
+            return obs, list(it), s.get_state()
+
+    a, b, c = run(False), run(True), run(False)
+    monkeypatch.delenv("MB4CU_FIXED_SHARES", raising=False)
+    assert a[1] == b[1] == c[1]
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[2], c[2])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[0], c[0])
