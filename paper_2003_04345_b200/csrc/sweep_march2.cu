@@ -28,7 +28,13 @@
 //    the default scheme's tables are compile-time immediates (defscheme.inc).
 //  - The first sweep of a step (U = (u0,u0,u0)) uses the closed form
 //    Phi_i = -h c_i f(u0), c_i = sum_j E[i][j].
-//  - The later-sweep loop is unrolled by 3 so register-window slots are static.
+//  - The later-sweep loop is unrolled by 3 so register-window slots are static (z rows
+//    and, at depth 1, the own-column Phi rows); the deep first sweep's loop by 6 (its
+//    (P, Q, R) pipeline, u0 / V window and g_1..g_3 history rings rotate by static indices).
+//  - Depth-1 later sweeps evaluate Phi in one FMA chain per stage and component
+//    (MB4_PHI_FUSED), correct in stage space (r = Phi + hA J Phi), keep no halo columns
+//    in the z rings (MB4_NOHALO) and take their band-rows in guided chunks from a device
+//    counter (MB4_DYN_SPLIT: the CTAs sharing an SM advance at unequal rates).
 // HBM traffic per sweep: 120 B/site (72 B/site for the first sweep, 88 for a
 // U3-only final sweep).
 #include <cooperative_groups.h>
