@@ -191,7 +191,8 @@ namespace cg = cooperative_groups;
 #ifdef MB4_CTA_TIMES
 // profiling builds: per-CTA (start, end of its last sweep, SM id) of the latest step launch
 // of each phase (tools/cta_times.py)
-__device__ unsigned long long g_cta_times[4][2048][3];
+__device__ unsigned long long g_cta_times[4][2048][4];
+// [0][1][k]: start of the last two first-sweep launches (k = launch parity), [0][2][0]: a counter
 extern "C" int mb4cu_debug_cta_times(unsigned long long* out) {
     return static_cast<int>(cudaMemcpyFromSymbol(out, g_cta_times, sizeof(g_cta_times)));
 }
@@ -1722,6 +1723,10 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
     cg::grid_group grid = cg::this_grid();
 #ifdef MB4_CTA_TIMES
     const unsigned long long cta_t0 = global_timer_ns();
+    if (PH == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long n = g_cta_times[0][2][0]++;
+        g_cta_times[0][1][n & 1] = cta_t0;
+    }
 #endif
     double acc[kAccSize] = {};  // energy sums, max |u0|^2, carries (monitor_add)
 #if MB4_CONSTS_IN_SMEM
@@ -1833,6 +1838,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
 #endif
         if constexpr (PH == 1) {  // the later-sweep launch takes it from here
             block_max_to(rmax ? ((static_cast<unsigned long long>(rmax) << 32) | 0xFFFFFFFFull) : 0ull, &a.rmax[0]);
+#ifdef MB4_CTA_TIMES
+            if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_times[PH][blockIdx.x][3] = global_timer_ns();
+#endif
             return;
         }
         if (redo) {  // same residual as the speculative pass: no new test
@@ -1876,6 +1884,9 @@ mb4_step3_kernel(const StepArgs a, const __grid_constant__ SweepConsts c) {
             *a.batch_abort = 1;
     }
     if (!obs_early) reduce_obs<NT>(a);
+#ifdef MB4_CTA_TIMES
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_times[PH][blockIdx.x][3] = global_timer_ns();
+#endif
 }
 
 template <int MF, int M, int NT, bool ISO, bool GHOST, bool DEF, int PH = 0>

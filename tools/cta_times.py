@@ -15,11 +15,20 @@ V, psi = configs.make_inputs(cfg)
 model = configs.model_for(cfg, V)
 with nls2d.Session(model, nls2d.Mb4Scheme(), configs.newton_for(cfg), device=0) as s:
     s.set_state(psi)
-    s.run(cfg.dt, 3)
-    buf = np.zeros((4, 2048, 3), dtype=np.uint64)
+    s.run(cfg.dt, 8)
+    buf = np.zeros((4, 2048, 4), dtype=np.uint64)
     L = ctypes.CDLL(os.environ["MB4CU_LIB"])
     rc = L.mb4cu_debug_cta_times(buf.ctypes.data_as(ctypes.c_void_p))
     assert rc == 0, rc
+n1 = int((buf[1][:, 1] > 0).sum())
+t_first = int(buf[1][:n1, 0].min())
+starts = sorted(int(x) for x in buf[0][1][:2])
+print("timeline of the last step (us after its first-sweep launch's first CTA start): "
+      f"first-sweep CTAs left {(int(buf[1][:n1, 3].max()) - t_first) / 1e3:.1f}; "
+      f"later-sweep CTAs start {(int(buf[2][buf[2][:, 0] > 0, 0].min()) - t_first) / 1e3:.1f}, "
+      f"last sweep row done {(int(buf[2][:, 1].max()) - t_first) / 1e3:.1f}, "
+      f"last CTA leaves {(int(buf[2][:, 3].max()) - t_first) / 1e3:.1f}; "
+      f"period between the last two steps' first-sweep starts {(starts[1] - starts[0]) / 1e3:.1f}")
 for ph in (1, 2):
     b = buf[ph]
     n = int((b[:, 1] > 0).sum())
