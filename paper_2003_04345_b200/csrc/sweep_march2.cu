@@ -181,6 +181,11 @@
 #ifndef MB4_FIRST_GREG
 #define MB4_FIRST_GREG 3
 #endif
+// first sweep: the neighbour values of level N + 1 are loaded before level N's arithmetic
+// (they were published an iteration ago, so they do not depend on it), one level ahead
+#ifndef MB4_FIRST_PREFETCH
+#define MB4_FIRST_PREFETCH 1
+#endif
 // default-scheme later sweeps: the GL-6 nodes in symmetric pairs (experiment knob)
 #ifndef MB4_SYM_PAIRS
 #define MB4_SYM_PAIRS 1
@@ -1288,7 +1293,16 @@ struct MarchFirst2 {
     struct Chain {
         double2 up, low, mid, u0o;
         double2 old3, old4, old5;  // g_{MF-3}, g_{MF-4}, g_{MF-5} of the output row (MB4_FIRST_GREG)
+        double2 nl, nr;            // left / right neighbours of the level to come (MB4_FIRST_PREFETCH)
+        double2 nl2, nr2;          // ... and of the one after it (MB4_FIRST_PREFETCH == 2)
     };
+    // shared-memory row of g_n written in the previous iteration (this thread's column)
+    template <int n, int PAR>
+    __device__ __forceinline__ static unsigned char* prev_row(unsigned char* smt, int p8, int p4) {
+        constexpr int D = depth(n);
+        constexpr int HB = H0 + hrow(n) * RB;
+        return smt + HB + (D == 2 ? (PAR ^ 1) * RB : (D == 8 ? p8 : p4));
+    }
 
     // level N: g_N at row i - N from g_{N-1} rows i-N-1 (register), i-N (ring, previous
     // iteration), i-N+1 (this iteration, ch.up)
@@ -1313,7 +1327,26 @@ struct MarchFirst2 {
             if constexpr (RS == 6 && n == MF - 4) ch.old4 = gp[n][(ROT + 6 - (MF - n)) % 6];
             if constexpr (RS == 6 && n == MF - 5) ch.old5 = gp[n][(ROT + 6 - (MF - n)) % 6];
 #if MB4_FIRST_PQR
-            const double2 gn = cf.jt_pqr(kw[kix(N + 1, ROT)], gc, cf.nsum(ref<double2>(crow - 16), ref<double2>(crow + 16), gd, ch.up));
+            double2 nl, nr;
+            if constexpr (MB4_FIRST_PREFETCH) {
+                nl = ch.nl;
+                nr = ch.nr;
+                constexpr int AHEAD = MB4_FIRST_PREFETCH;  // levels ahead
+                if constexpr (AHEAD == 2) {
+                    ch.nl = ch.nl2;
+                    ch.nr = ch.nr2;
+                }
+                if constexpr (N + AHEAD <= MF) {
+                    // g_{N + AHEAD - 1} of the previous iteration
+                    unsigned char* nrow = prev_row<N + AHEAD - 1, PAR>(smt, p8, p4);
+                    (AHEAD == 2 ? ch.nl2 : ch.nl) = ref<double2>(nrow - 16);
+                    (AHEAD == 2 ? ch.nr2 : ch.nr) = ref<double2>(nrow + 16);
+                }
+            } else {
+                nl = ref<double2>(crow - 16);
+                nr = ref<double2>(crow + 16);
+            }
+            const double2 gn = cf.jt_pqr(kw[kix(N + 1, ROT)], gc, cf.nsum(nl, nr, gd, ch.up));
 #else
             double2 u0n;
             double vn;
@@ -1379,6 +1412,13 @@ struct MarchFirst2 {
 
         zw[Z0] = ref<double2>(smt + ZU + zn);
         vw[Z0] = ref<double>(smv + ZV + (zn >> 1));
+        // level 1's neighbours (g_0 of the previous iteration), loaded before level 0's arithmetic
+        double2 pre_l, pre_r;
+        if constexpr (MB4_FIRST_PREFETCH && MB4_FIRST_PQR) {
+            unsigned char* nrow = prev_row<0, (ROT & 1)>(smt, p8, p4);
+            pre_l = ref<double2>(nrow - 16);
+            pre_r = ref<double2>(nrow + 16);
+        }
 
         // ---- level 0 at row i: f(u0) and the energy monitor --------------------
         const double v = vw[Z1];
@@ -1399,6 +1439,15 @@ struct MarchFirst2 {
 
         // ---- levels 1..MF --------------------------------------------------------
         Chain ch{f, f, f, f};
+        if constexpr (MB4_FIRST_PREFETCH && MB4_FIRST_PQR) {
+            ch.nl = pre_l;
+            ch.nr = pre_r;
+            if constexpr (MB4_FIRST_PREFETCH == 2 && MF >= 2) {
+                unsigned char* nrow = prev_row<1, (ROT & 1)>(smt, p8, p4);
+                ch.nl2 = ref<double2>(nrow - 16);
+                ch.nr2 = ref<double2>(nrow + 16);
+            }
+        }
         levels<1, ROT>(cf, smt, smv, jrb, o8, p8, o4, p4, ch);
 
         if (out_ok) {
